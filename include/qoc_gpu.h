@@ -1,0 +1,216 @@
+/*
+ * qoc_gpu.h — C ABI of the B200-native ISM (Intermediate State Method) hot path.
+ *
+ * This is the drop-in boundary for the reference solver entry
+ *
+ *     IsmRun qoc::run_ism(const ControlProblem&, const ControlField& u0,
+ *                         const IsmConfig&, const SolverSpec&)
+ *       -- /root/reference/proj/core/include/qoc/ism.hpp:80-81, core/src/ism.cpp:211-612
+ *
+ * and for the helper entry points the reference exposes on the same path:
+ *
+ *     propagate_final        propagation.hpp:88 / propagation.cpp:194-200
+ *     evaluate_objective     objective.hpp:37-40 / objective.cpp:93-105
+ *     objective_gradient     objective.hpp:46-51 / objective.cpp:107-129
+ *     assemble_propagator    propagation.hpp:112 / propagation.cpp:236-249
+ *
+ * Plain C: pointers and sizes only, caller-owned host buffers, library-owned
+ * device state.  Complex arrays are interleaved (re, im) doubles in Eigen's
+ * column-major order, i.e. exactly the bytes of an Eigen::MatrixXcd / VectorXcd
+ * (`.data()`), so a reference-side shim passes Eigen buffers through unchanged.
+ * Controls are channels x steps, column-major: sample (c, j) at c + j*C
+ * (controls.hpp:54), again the bytes of the reference's RMat.
+ *
+ * Error behaviour mirrors the reference (ism.cpp:213-231, controls.cpp:16-18):
+ *   QOC_EINVAL   <-> std::invalid_argument   (bad shapes, L < 1, eta < 0, ...)
+ *   QOC_ERUNTIME <-> std::runtime_error      (decomposition errors)
+ *   QOC_ELOGIC   <-> std::logic_error        (unsupported kind/plan combination)
+ *   QOC_ECUDA / QOC_ENCCL                    (device / collective failures)
+ * Numerical aborts are NOT errors: they return QOC_OK with status.aborted = 1
+ * and the reference's reason text (ism.cpp:387,529-530,558).
+ *
+ * A context is bound to one device and is not thread-safe; distinct contexts
+ * are independent (no globals), matching the reference's re-entrancy.
+ */
+#ifndef QOC_GPU_H_
+#define QOC_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QOC_ABI_VERSION 1
+
+enum qoc_status_code {
+  QOC_OK = 0,
+  QOC_EINVAL = 1,
+  QOC_ELOGIC = 2,
+  QOC_ECUDA = 3,
+  QOC_ENCCL = 4,
+  QOC_ERUNTIME = 5
+};
+
+/* Operator classes.  All four implement the reference's HamiltonianModel
+ * plugin contract (propagation.hpp:20-38):
+ *   DENSE   - DenseModel (models.hpp:15-31): H(u) = H0 + sum u_c A_c + sum (u_c^2/2) B_c,
+ *             one-step map = Cayley / Crank-Nicolson (propagation.cpp:85-90).
+ *   TRIDIAG - the same model with Hermitian tridiagonal H0, A_c, B_c (rotor, models.cpp:349-359).
+ *   BITFLIP - spin register: diagonal H0 plus channels sum_i coef[c][i] sigma^{axis_c}_i
+ *             (Pauli matrices; spin i <-> bit (nspins-1-i) of the basis index, spin 0 most
+ *             significant as in spin_operator, models.cpp:296-318).
+ *   STRANG  - periodic-grid condensate, split-step Fourier (propagation.cpp:131-170),
+ *             TrappedCondensateModel-style potentials (models.cpp:77-127). */
+enum qoc_kind { QOC_KIND_DENSE = 0, QOC_KIND_TRIDIAG = 1, QOC_KIND_BITFLIP = 2, QOC_KIND_STRANG = 3 };
+
+/* Sampled potentials for QOC_KIND_STRANG.
+ *   TRAP    : models.cpp:95-127, pot_params = {trap_distance}
+ *   LATTICE : V(x,u) = 0.5*w2*x^2 + v0*cos^2(k (x - u)),  dV/du = v0*k*sin(2 k (x - u)),
+ *             pot_params = {w2, v0, k}  (BASELINE config 4) */
+enum qoc_potential { QOC_POT_TRAP = 0, QOC_POT_LATTICE = 1 };
+
+typedef struct qoc_problem_v1 {
+  int32_t abi_version; /* QOC_ABI_VERSION */
+  int32_t kind;        /* enum qoc_kind */
+  int32_t dim;         /* state length d */
+  int32_t channels;    /* C */
+  int32_t steps;       /* K (TimeGrid::steps) */
+  int32_t batch;       /* B independent problems sharing kind, d, C and the grid */
+  double t_start;      /* TimeGrid::t_start */
+  double dt;           /* TimeGrid::dt */
+  double ip_weight;    /* HamiltonianModel::ip_weight(): dx for STRANG, 1 otherwise */
+
+  /* DENSE:  h0 [B][d*d], linear [B][C][d*d], quadratic [B][C][d*d] or NULL (complex).
+   * BITFLIP: h0 [B][d] REAL diagonal. */
+  const double* h0;
+  const double* linear;
+  const double* quadratic;
+
+  /* TRIDIAG: nops = 1 + C (+ C when tri_has_quadratic), order H0, A_0.., B_0..
+   * tri_diag [B][nops][d] real diagonal; tri_sub [B][nops][d-1] complex entry (j+1, j);
+   * entry (j, j+1) is its conjugate. */
+  const double* tri_diag;
+  const double* tri_sub;
+  int32_t tri_has_quadratic;
+
+  /* BITFLIP channels. */
+  int32_t nspins;
+  const int32_t* bf_axis; /* [C]: 0 = sigma_x, 1 = sigma_y */
+  const double* bf_coef;  /* [B][C][nspins] */
+
+  /* STRANG. */
+  const double* kinetic; /* [d] kinetic spectrum, dft mode order (models.cpp:87-92) */
+  const double* grid_x;  /* [d] grid points */
+  int32_t potential;     /* enum qoc_potential */
+  double pot_params[4];
+  double kappa;          /* nonlinearity() */
+
+  /* States and penalty (ControlProblem, objective.hpp:18-24). */
+  const double* initial; /* [B][d] complex */
+  const double* target;  /* [B][d] complex */
+  const double* penalty; /* [K] per-step alpha_j (shared by the batch), or NULL = 0 */
+} qoc_problem_v1;
+
+enum qoc_variant { QOC_VARIANT_INTERPOLATED = 0, QOC_VARIANT_SPLIT = 1 };
+enum qoc_plan { QOC_PLAN_ASSEMBLED = 0, QOC_PLAN_DIRECT = 1 };
+/* Decomposition of the K steps into L subintervals.  UNIFORM is the reference's
+ * Decomposition::uniform (controls.cpp:110-120; fails with QOC_ERUNTIME when L does not
+ * divide K).  BALANCED gives the first K mod L parts ceil(K/L) steps and the rest
+ * floor(K/L) (identical to UNIFORM when L | K).  EXPLICIT takes node_index. */
+enum qoc_partition { QOC_PARTITION_BALANCED = 0, QOC_PARTITION_UNIFORM = 1, QOC_PARTITION_EXPLICIT = 2 };
+
+/* IsmConfig (ism.hpp:12-39). */
+typedef struct qoc_ism_config_v1 {
+  int32_t subintervals;        /* L */
+  int32_t workers;             /* accepted for API parity; the device schedules tasks */
+  int32_t max_outer;
+  int32_t variant;             /* enum qoc_variant */
+  int32_t plan;                /* enum qoc_plan */
+  int32_t compute_error;
+  int32_t log_exact_objective;
+  int32_t checkpoint_stride;   /* forwarded to gradient sweeps; results are bit-identical */
+  int32_t partition;           /* enum qoc_partition */
+  int32_t reserved;
+  double eta;
+  const int32_t* node_index;   /* [L+1] for QOC_PARTITION_EXPLICIT */
+} qoc_ism_config_v1;
+
+enum qoc_solver_kind { QOC_SOLVER_GRADIENT = 0, QOC_SOLVER_MONOTONIC = 1, QOC_SOLVER_NEWTON = 2 };
+
+/* SolverSpec (optimizers.hpp:9-30); only the constant-step gradient kind is on this path. */
+typedef struct qoc_solver_v1 {
+  int32_t kind;                    /* enum qoc_solver_kind; others return QOC_ELOGIC */
+  int32_t inner_iterations;
+  int32_t naive_nonlinear_adjoint; /* GradientOptions::naive_nonlinear_adjoint */
+  int32_t checkpoint_stride;       /* GradientOptions::checkpoint_stride */
+  double step_size;                /* rho */
+} qoc_solver_v1;
+
+/* IterationStat (runtime.hpp:44-63), one per recorded iteration (entry 0 = bootstrap). */
+typedef struct qoc_iter_record_v1 {
+  int32_t iteration;
+  int32_t has_error;
+  int32_t has_exact_objective;
+  int32_t reserved;
+  double objective;        /* NaN where the reference records NaN */
+  double exact_objective;
+  double error;
+  double device_seconds;   /* CUDA-event time of this iteration's device work */
+} qoc_iter_record_v1;
+
+/* RunRecord abort state (runtime.hpp:65-75), per batch member. */
+typedef struct qoc_run_status_v1 {
+  int32_t aborted;
+  int32_t iterations_recorded;
+  char abort_reason[240];
+} qoc_run_status_v1;
+
+typedef struct qoc_ctx qoc_ctx;
+
+typedef struct qoc_ctx_opts_v1 {
+  int32_t abi_version;
+  int32_t device;   /* CUDA ordinal, -1 = current */
+  int32_t reserved[6];
+} qoc_ctx_opts_v1;
+
+int32_t qoc_abi_version(void);
+int32_t qoc_ctx_create(const qoc_ctx_opts_v1* opts, qoc_ctx** out);
+void qoc_ctx_destroy(qoc_ctx* ctx);
+/* Text of the last error raised on this context (empty when none). */
+const char* qoc_ctx_last_error(const qoc_ctx* ctx);
+
+/* run_ism over a batch of B independent problems.
+ *   u0, u_out     [B][C*K]
+ *   recs          [B][rec_cap]   (rec_cap >= max_outer + 1)
+ *   task_values   [B][rec_cap][L] or NULL  (IterationStat::task_values)
+ *   status        [B]
+ * Returns an enum qoc_status_code; the message is in qoc_ctx_last_error. */
+int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* problem, const qoc_ism_config_v1* cfg,
+                    const qoc_solver_v1* solver, const double* u0, double* u_out,
+                    qoc_iter_record_v1* recs, int32_t rec_cap, double* task_values,
+                    qoc_run_status_v1* status);
+
+/* Objective forms (objective.hpp:16). */
+enum qoc_form { QOC_FORM_OVERLAP = 0, QOC_FORM_TRACKING = 1 };
+
+/* propagate_final for every batch member: states_out [B][d] complex. */
+int32_t qoc_propagate_final(qoc_ctx* ctx, const qoc_problem_v1* problem, const double* u,
+                            double* states_out);
+/* evaluate_objective + objective_gradient: value_out [B], grad_out [B][C*K] (either may be NULL). */
+int32_t qoc_objective_gradient(qoc_ctx* ctx, const qoc_problem_v1* problem, const double* u,
+                               int32_t form, int32_t naive_nonlinear_adjoint, double* value_out,
+                               double* grad_out);
+/* assemble_propagator: prop_out [B][d*d] complex, column-major (linear kinds only). */
+int32_t qoc_assemble_propagator(qoc_ctx* ctx, const qoc_problem_v1* problem, const double* u,
+                                double* prop_out);
+
+/* Kernel-launch counter of this context (for the bench's gpu_launches claim). */
+int64_t qoc_ctx_launch_count(const qoc_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QOC_GPU_H_ */

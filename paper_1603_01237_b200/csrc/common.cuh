@@ -1,0 +1,139 @@
+// common.cuh — device-side types shared by the ISM kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace qoc {
+
+// ---- complex128 as double2 ------------------------------------------------------------
+__host__ __device__ __forceinline__ double2 cx(double r, double i) { return make_double2(r, i); }
+__host__ __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return cx(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ double2 csub(double2 a, double2 b) { return cx(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return cx(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+__host__ __device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+  return cx(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+// conj(a) * b
+__host__ __device__ __forceinline__ double2 cconjmul(double2 a, double2 b) {
+  return cx(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__host__ __device__ __forceinline__ double2 cscale(double2 a, double s) { return cx(a.x * s, a.y * s); }
+__host__ __device__ __forceinline__ double2 cconj(double2 a) { return cx(a.x, -a.y); }
+__host__ __device__ __forceinline__ double2 cneg(double2 a) { return cx(-a.x, -a.y); }
+__host__ __device__ __forceinline__ double cabs2(double2 a) { return a.x * a.x + a.y * a.y; }
+// acc + a*b
+__host__ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
+  return cx(fma(a.x, b.x, fma(-a.y, b.y, acc.x)), fma(a.x, b.y, fma(a.y, b.x, acc.y)));
+}
+// acc - a*b
+__host__ __device__ __forceinline__ double2 cfms(double2 a, double2 b, double2 acc) {
+  return cx(fma(-a.x, b.x, fma(a.y, b.y, acc.x)), fma(-a.x, b.y, fma(-a.y, b.x, acc.y)));
+}
+// acc + conj(a)*b
+__host__ __device__ __forceinline__ double2 cfmaconj(double2 a, double2 b, double2 acc) {
+  return cx(fma(a.x, b.x, fma(a.y, b.y, acc.x)), fma(a.x, b.y, fma(-a.y, b.x, acc.y)));
+}
+__host__ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  const double den = b.x * b.x + b.y * b.y;
+  const double inv = 1.0 / den;
+  return cx((a.x * b.x + a.y * b.y) * inv, (a.y * b.x - a.x * b.y) * inv);
+}
+__host__ __device__ __forceinline__ double2 crcp(double2 b) {
+  const double inv = 1.0 / (b.x * b.x + b.y * b.y);
+  return cx(b.x * inv, -b.y * inv);
+}
+__device__ __forceinline__ bool cfinite(double2 a) { return isfinite(a.x) && isfinite(a.y); }
+
+__device__ __forceinline__ double2 shfl(double2 v, int src, int width = 32) {
+  return cx(__shfl_sync(0xffffffffu, v.x, src, width), __shfl_sync(0xffffffffu, v.y, src, width));
+}
+__device__ __forceinline__ double2 shfl_xor(double2 v, int m, int width = 32) {
+  return cx(__shfl_xor_sync(0xffffffffu, v.x, m, width), __shfl_xor_sync(0xffffffffu, v.y, m, width));
+}
+
+// ---- run modes of the task kernels -----------------------------------------------------
+enum TaskMode : int {
+  M_ENTRY = 1,      // entry value of the task at the current control -> entry[b][n]
+  M_UPDATE = 2,     // inner gradient steps, controls updated in place
+  M_ERROR = 4,      // residual sweep at the updated control -> err[b][n]
+  M_ASSEMBLE = 8,   // propagator product at the updated control -> prop[b][n]
+  M_LAGGED = 16,    // split refresh: psi_end / chi_start at the updated control
+  M_FINAL = 32,     // store the final state of the first forward sweep -> psi_end[b][n]
+  M_GRAD = 64,      // store the raw gradient (weight 1, no update) -> grad[b][K][C]
+};
+
+// ---- problem + run state as seen by kernels ------------------------------------------
+struct DevProblem {
+  int kind, d, C, K, B, L;
+  int has_quad;
+  double dt, ip_w;
+  // DENSE: row-major [B][d][d]; quad may be null.  Column 1-norms for the pivot bound.
+  const double2* h0;
+  const double2* lin;   // [B][C][d][d]
+  const double2* quad;  // [B][C][d][d]
+  const double* norm1;  // [B][1 + 2C] : ||H0||_1, ||A_c||_1, ||B_c||_1 (max column sums)
+  // TRIDIAG: [B][nops][d] real diag, [B][nops][d-1] complex sub
+  const double* tri_diag;
+  const double2* tri_sub;
+  // BITFLIP
+  int nspins;
+  const double* bf_diag;  // [B][d]
+  const int* bf_axis;     // [C]
+  const double* bf_coef;  // [B][C][nspins]
+  // STRANG
+  const double2* kin_fwd;  // [d] exp(-i dt/2 k)   (kinetic_half_phase, forward)
+  const double2* kin_adj;  // [d] exp(+i dt/2 k)
+  const double2* twiddle;  // FFT twiddles / DFT matrix
+  const double* grid_x;
+  int potential;
+  double pp[4];
+  double kappa;
+  // states and penalty
+  const double2* init;  // [B][d]
+  const double2* targ;  // [B][d]
+  const double* alpha;  // [K]
+  const int* node;      // [L+1]
+};
+
+struct DevRun {
+  double* u;            // [B][K][C] (column-major C x K per problem)
+  double* grad;         // [B][K][C] (M_GRAD)
+  double2* task_init;   // [B][L][d]
+  double2* task_targ;   // [B][L][d]
+  double2* psi_nodes;   // [B][L+1][d]
+  double2* chi_nodes;   // [B][L+1][d]
+  double2* prop;        // [B][L][d][d] row-major
+  double2* psi_end;     // [B][L][d]
+  double2* chi_start;   // [B][L][d]
+  double2* traj;        // workspace [B*L][traj_len][d]
+  int traj_len;         // >= max len + 1
+  double* entry;        // [B][L]
+  double* err;          // [B][L]
+  double* pen;          // [B][L] sum_j alpha_j |u_j|^2 over the task window (updated control)
+  int* bad_u;           // [B][L]
+  int* done;            // [B]
+  int* status;          // [B] abort kind: 0 none, 1 controls, 2 boundary, 3 bootstrap
+  int* abort_iter;      // [B]
+  int* n_recs;          // [B]
+  double* rec_obj;      // [B][cap]
+  double* rec_err;      // [B][cap]
+  double* rec_exact;    // [B][cap]
+  double* rec_tv;       // [B][cap][L]
+  int* rec_flags;       // [B][cap] bit 1 = has error, bit 2 = has exact objective
+  double* tot_err;      // [B] summed task residual of the current iteration
+  int cap;
+};
+
+struct TaskArgs {
+  int mode;
+  int form;      // 0 overlap, 1 tracking
+  int weighted;  // task weight K/len
+  int inner;     // inner gradient iterations
+  double rho;
+};
+
+}  // namespace qoc

@@ -1,0 +1,628 @@
+// driver.cu — host driver of the B200 ISM path behind the C ABI of include/qoc_gpu.h.
+//
+// qoc_ism_run restates the control flow of run_ism (ism.cpp:211-612) as a sequence of
+// device kernels on one stream: bootstrap, then per outer iteration
+//   task kernel (entry value + gradient update + residual + assembly / lagged refresh)
+//   -> penalty partials -> index-order merge -> boundary refresh (chain / lagged / direct)
+//   -> boundary objective + waypoint rebuild -> [exact payoff] -> record + eta stop,
+// then the trailing task-value evaluation.  Per-problem stop and abort state lives on the
+// device, so a batch of independent problems runs in one launch sequence with no host
+// round trip per iteration.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/qoc_gpu.h"
+#include "kernels.h"
+
+using namespace qoc;
+
+struct qoc_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  int64_t launches = 0;
+};
+
+namespace {
+
+struct Fail {
+  int32_t code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int32_t code, const std::string& msg) { throw Fail{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(QOC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// RAII device allocation
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  explicit DBuf(size_t n) : bytes(n) {
+    if (n) ck(cudaMalloc(&p, n), "cudaMalloc");
+  }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(bytes, o.bytes);
+    return *this;
+  }
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+template <class T>
+DBuf upload(const T* host, size_t n, cudaStream_t st) {
+  DBuf b(sizeof(T) * n);
+  if (n) ck(cudaMemcpyAsync(b.p, host, sizeof(T) * n, cudaMemcpyHostToDevice, st), "upload");
+  return b;
+}
+
+template <class T>
+DBuf filled(size_t n, T value, cudaStream_t st) {
+  std::vector<T> h(n, value);
+  DBuf b = upload(h.data(), n, st);
+  ck(cudaStreamSynchronize(st), "sync");
+  return b;
+}
+
+std::vector<int> decomposition(int K, int L, int mode, const int32_t* explicit_nodes) {
+  // Decomposition::uniform / from_times (controls.cpp:110-140), generalised
+  if (L < 1) fail(QOC_ERUNTIME, "Decomposition: parts must be positive");
+  std::vector<int> node;
+  if (mode == QOC_PARTITION_EXPLICIT) {
+    if (!explicit_nodes) fail(QOC_EINVAL, "explicit partition needs node_index");
+    for (int n = 0; n <= L; ++n) node.push_back(explicit_nodes[n]);
+    if (node.front() != 0 || node.back() != K)
+      fail(QOC_ERUNTIME, "Decomposition: boundaries must span the full grid");
+    for (int n = 0; n < L; ++n)
+      if (node[n + 1] <= node[n]) fail(QOC_ERUNTIME, "Decomposition: boundary times must strictly increase");
+    return node;
+  }
+  if (mode == QOC_PARTITION_UNIFORM && K % L != 0)
+    fail(QOC_ERUNTIME, "Decomposition: step count " + std::to_string(K) + " is not divisible into " +
+                           std::to_string(L) + " equal parts");
+  if (L > K) fail(QOC_ERUNTIME, "Decomposition: more parts than steps");
+  const int base = K / L, extra = K % L;
+  node.push_back(0);
+  for (int n = 0; n < L; ++n) node.push_back(node.back() + base + (n < extra ? 1 : 0));
+  return node;
+}
+
+// Device copy of a problem (operators converted to the kernels' layouts).
+struct DeviceProblem {
+  DevProblem P{};
+  std::vector<DBuf> bufs;
+  int stride = 0;  // state stride of the kind's trajectory workspace
+
+  template <class T>
+  const T* keep(DBuf&& b) {
+    bufs.push_back(std::move(b));
+    return bufs.back().as<T>();
+  }
+};
+
+void validate_problem(const qoc_problem_v1* p) {
+  if (!p) fail(QOC_EINVAL, "problem has no model");
+  if (p->abi_version != QOC_ABI_VERSION) fail(QOC_EINVAL, "problem ABI version mismatch");
+  if (p->dim < 1 || p->channels < 1 || p->steps < 1 || p->batch < 1)
+    fail(QOC_EINVAL, "dim, channels, steps and batch must be positive");
+  if (!(p->dt > 0.0)) fail(QOC_EINVAL, "TimeGrid: dt must be positive");
+  if (!p->initial || !p->target) fail(QOC_EINVAL, "initial and target states are required");
+}
+
+void hermitian_check(const double* m, int d, const char* what) {  // models.cpp:20-25
+  double scale = 1.0, defect = 0.0;
+  for (int j = 0; j < d; ++j)
+    for (int i = 0; i < d; ++i) {
+      const double ar = m[2 * (i + (size_t)j * d)], ai = m[2 * (i + (size_t)j * d) + 1];
+      const double br = m[2 * (j + (size_t)i * d)], bi = m[2 * (j + (size_t)i * d) + 1];
+      scale = std::max(scale, std::hypot(ar, ai));
+      defect = std::max(defect, std::hypot(ar - br, ai + bi));
+    }
+  if (defect > 1e-10 * scale) fail(QOC_EINVAL, std::string(what) + " must be Hermitian");
+}
+
+void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaStream_t st, DeviceProblem& out) {
+  validate_problem(p);
+  DevProblem& P = out.P;
+  const int d = p->dim, C = p->channels, B = p->batch, K = p->steps;
+  P.kind = p->kind;
+  P.d = d;
+  P.C = C;
+  P.K = K;
+  P.B = B;
+  P.L = static_cast<int>(node.size()) - 1;
+  P.dt = p->dt;
+  P.ip_w = p->ip_weight;
+  out.stride = d;
+  switch (p->kind) {
+    case QOC_KIND_DENSE: {
+      if (!p->h0 || !p->linear) fail(QOC_EINVAL, "dense model needs h0 and linear operators");
+      if (dense_pad(d) < 0) fail(QOC_ELOGIC, "dense device kernels support d <= 32; use a structured kind");
+      out.stride = dense_pad(d);
+      const size_t dd = (size_t)d * d;
+      P.has_quad = p->quadratic != nullptr;
+      const int nq = P.has_quad ? C : 0;
+      std::vector<double> h0((size_t)2 * B * dd), lin((size_t)2 * B * C * dd), quad((size_t)2 * B * nq * dd);
+      std::vector<double> norms((size_t)B * (1 + 2 * C), 0.0);
+      auto convert = [&](const double* src, double* dst, double* norm, const char* what) {
+        hermitian_check(src, d, what);
+        double best = 0.0;
+        for (int j = 0; j < d; ++j) {
+          double colsum = 0.0;
+          for (int i = 0; i < d; ++i) {
+            const double re = src[2 * (i + (size_t)j * d)], im = src[2 * (i + (size_t)j * d) + 1];
+            dst[2 * ((size_t)i * d + j)] = re;  // column-major -> row-major
+            dst[2 * ((size_t)i * d + j) + 1] = im;
+            colsum += std::hypot(re, im);
+          }
+          best = std::max(best, colsum);
+        }
+        *norm = best * (1.0 + 1e-12);
+      };
+      for (int b = 0; b < B; ++b) {
+        double* nb = norms.data() + (size_t)b * (1 + 2 * C);
+        convert(p->h0 + 2 * dd * b, h0.data() + 2 * dd * b, nb, "free Hamiltonian");
+        for (int c = 0; c < C; ++c)
+          convert(p->linear + 2 * dd * ((size_t)b * C + c), lin.data() + 2 * dd * ((size_t)b * C + c), nb + 1 + c,
+                  "control operator");
+        for (int c = 0; c < nq; ++c)
+          convert(p->quadratic + 2 * dd * ((size_t)b * C + c), quad.data() + 2 * dd * ((size_t)b * C + c),
+                  nb + 1 + C + c, "quadratic operator");
+      }
+      P.h0 = out.keep<double2>(upload(h0.data(), h0.size(), st));
+      P.lin = out.keep<double2>(upload(lin.data(), lin.size(), st));
+      P.quad = nq ? out.keep<double2>(upload(quad.data(), quad.size(), st)) : nullptr;
+      P.norm1 = out.keep<double>(upload(norms.data(), norms.size(), st));
+      break;
+    }
+    case QOC_KIND_TRIDIAG: {
+      if (!p->tri_diag || !p->tri_sub) fail(QOC_EINVAL, "tridiagonal model needs bands");
+      if (d > 32) fail(QOC_ELOGIC, "tridiagonal device kernels support d <= 32");
+      P.has_quad = p->tri_has_quadratic != 0;
+      const int nops = 1 + C + (P.has_quad ? C : 0);
+      P.tri_diag = out.keep<double>(upload(p->tri_diag, (size_t)B * nops * d, st));
+      P.tri_sub = out.keep<double2>(upload(reinterpret_cast<const double2*>(p->tri_sub), (size_t)B * nops * (d - 1), st));
+      break;
+    }
+    case QOC_KIND_BITFLIP: {
+      if (!p->h0 || !p->bf_axis || !p->bf_coef) fail(QOC_EINVAL, "bit-flip model needs h0/axis/coef");
+      if (p->nspins < 1 || p->nspins > 12 || (1 << p->nspins) != d)
+        fail(QOC_EINVAL, "bit-flip dim must be 2^nspins (nspins <= 12)");
+      P.nspins = p->nspins;
+      P.bf_diag = out.keep<double>(upload(p->h0, (size_t)B * d, st));
+      P.bf_axis = out.keep<int>(upload(p->bf_axis, (size_t)C, st));
+      P.bf_coef = out.keep<double>(upload(p->bf_coef, (size_t)B * C * p->nspins, st));
+      break;
+    }
+    case QOC_KIND_STRANG: {
+      if (!p->kinetic || !p->grid_x) fail(QOC_EINVAL, "condensate model needs kinetic/grid");
+      if (C != 1) fail(QOC_EINVAL, "single control channel expected");
+      if (d > 4096) fail(QOC_ELOGIC, "split-step device kernels support d <= 4096");
+      const bool pow2 = (d & (d - 1)) == 0;
+      if (!pow2 && d > 256) fail(QOC_ELOGIC, "split-step device kernels need a power-of-two grid above 256 points");
+      // kinetic_half_phase (propagation.cpp:33-40): polar(1, sign * 0.5 * dt * k)
+      std::vector<double> kf(2 * (size_t)d), ka(2 * (size_t)d);
+      for (int i = 0; i < d; ++i) {
+        const double af = -1.0 * 0.5 * p->dt * p->kinetic[i];
+        const double aa = 1.0 * 0.5 * p->dt * p->kinetic[i];
+        kf[2 * i] = std::cos(af);
+        kf[2 * i + 1] = std::sin(af);
+        ka[2 * i] = std::cos(aa);
+        ka[2 * i + 1] = std::sin(aa);
+      }
+      P.kin_fwd = out.keep<double2>(upload(reinterpret_cast<const double2*>(kf.data()), (size_t)d, st));
+      P.kin_adj = out.keep<double2>(upload(reinterpret_cast<const double2*>(ka.data()), (size_t)d, st));
+      // twiddles of linalg.cpp:26-27 (polar(1, ang * k), ang = -2 pi / n; the inverse
+      // transform conjugates) or the direct DFT kernel of linalg.cpp:37-50
+      std::vector<double> tw;
+      if (pow2) {
+        tw.resize(2 * (size_t)(d / 2 > 0 ? d / 2 : 1));
+        const double ang = -1.0 * 2.0 * M_PI / static_cast<double>(d);
+        for (int k = 0; k < d / 2; ++k) {
+          tw[2 * k] = std::cos(ang * k);
+          tw[2 * k + 1] = std::sin(ang * k);
+        }
+      } else {
+        tw.resize(2 * (size_t)d * d);
+        for (int k = 0; k < d; ++k)
+          for (int m = 0; m < d; ++m) {
+            const long long r = (static_cast<long long>(m) * k) % d;
+            const double a = -1.0 * 2.0 * M_PI * static_cast<double>(r) / static_cast<double>(d);
+            tw[2 * ((size_t)k * d + m)] = std::cos(a);
+            tw[2 * ((size_t)k * d + m) + 1] = std::sin(a);
+          }
+      }
+      P.twiddle = out.keep<double2>(upload(reinterpret_cast<const double2*>(tw.data()), tw.size() / 2, st));
+      P.grid_x = out.keep<double>(upload(p->grid_x, (size_t)d, st));
+      P.potential = p->potential;
+      for (int i = 0; i < 4; ++i) P.pp[i] = p->pot_params[i];
+      P.kappa = p->kappa;
+      break;
+    }
+    default:
+      fail(QOC_EINVAL, "unknown model kind");
+  }
+  P.init = out.keep<double2>(upload(reinterpret_cast<const double2*>(p->initial), (size_t)B * d, st));
+  P.targ = out.keep<double2>(upload(reinterpret_cast<const double2*>(p->target), (size_t)B * d, st));
+  std::vector<double> alpha(K, 0.0);
+  if (p->penalty) alpha.assign(p->penalty, p->penalty + K);
+  P.alpha = out.keep<double>(upload(alpha.data(), alpha.size(), st));
+  P.node = out.keep<int>(upload(node.data(), node.size(), st));
+}
+
+struct DeviceRun {
+  DevRun R{};
+  std::vector<DBuf> bufs;
+  template <class T>
+  T* alloc(size_t n) {
+    bufs.emplace_back(sizeof(T) * std::max<size_t>(n, 1));
+    return bufs.back().as<T>();
+  }
+};
+
+void alloc_run(const DeviceProblem& dp, int cap, const std::vector<int>& node, bool need_prop, bool need_grad,
+               cudaStream_t st, DeviceRun& out) {
+  const DevProblem& P = dp.P;
+  DevRun& R = out.R;
+  const size_t B = P.B, L = P.L, d = P.d, K = P.K, C = P.C;
+  int maxlen = 0;
+  for (size_t n = 0; n < L; ++n) maxlen = std::max(maxlen, node[n + 1] - node[n]);
+  R.cap = cap;
+  R.traj_len = maxlen + 1;
+  R.u = out.alloc<double>(B * K * C);
+  R.grad = need_grad ? out.alloc<double>(B * K * C) : nullptr;
+  R.task_init = out.alloc<double2>(B * L * d);
+  R.task_targ = out.alloc<double2>(B * L * d);
+  R.psi_nodes = out.alloc<double2>(B * (L + 1) * d);
+  R.chi_nodes = out.alloc<double2>(B * (L + 1) * d);
+  R.prop = need_prop ? out.alloc<double2>(B * L * d * d) : nullptr;
+  R.psi_end = out.alloc<double2>(B * L * d);
+  R.chi_start = out.alloc<double2>(B * L * d);
+  R.traj = out.alloc<double2>(B * L * (size_t)R.traj_len * dp.stride);
+  R.entry = out.alloc<double>(B * L);
+  R.err = out.alloc<double>(B * L);
+  R.pen = out.alloc<double>(B * L);
+  R.bad_u = out.alloc<int>(B * L);
+  R.done = out.alloc<int>(B);
+  R.status = out.alloc<int>(B);
+  R.abort_iter = out.alloc<int>(B);
+  R.n_recs = out.alloc<int>(B);
+  R.tot_err = out.alloc<double>(B);
+  R.rec_obj = out.alloc<double>(B * cap);
+  R.rec_err = out.alloc<double>(B * cap);
+  R.rec_exact = out.alloc<double>(B * cap);
+  R.rec_tv = out.alloc<double>(B * cap * L);
+  R.rec_flags = out.alloc<int>(B * cap);
+  ck(cudaMemsetAsync(R.done, 0, sizeof(int) * B, st), "memset");
+  ck(cudaMemsetAsync(R.status, 0, sizeof(int) * B, st), "memset");
+  ck(cudaMemsetAsync(R.abort_iter, 0, sizeof(int) * B, st), "memset");
+  ck(cudaMemsetAsync(R.err, 0, sizeof(double) * B * L, st), "memset");
+  ck(cudaMemsetAsync(R.rec_flags, 0, sizeof(int) * B * cap, st), "memset");
+  ck(cudaMemsetAsync(R.bad_u, 0, sizeof(int) * B * L, st), "memset");
+  // NaN fill (0xff bytes is a NaN pattern for doubles)
+  ck(cudaMemsetAsync(R.rec_obj, 0xff, sizeof(double) * B * cap, st), "memset");
+  ck(cudaMemsetAsync(R.rec_err, 0xff, sizeof(double) * B * cap, st), "memset");
+  ck(cudaMemsetAsync(R.rec_exact, 0xff, sizeof(double) * B * cap, st), "memset");
+  ck(cudaMemsetAsync(R.rec_tv, 0xff, sizeof(double) * B * cap * L, st), "memset");
+  std::vector<int> ones(B, 1);
+  ck(cudaMemcpyAsync(R.n_recs, ones.data(), sizeof(int) * B, cudaMemcpyHostToDevice, st), "n_recs");
+  ck(cudaStreamSynchronize(st), "sync");
+}
+
+// Kind dispatch ------------------------------------------------------------------------
+cudaError_t task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
+  switch (P.kind) {
+    case QOC_KIND_DENSE: return dense_task(P, R, A, ignore_done, st);
+    case QOC_KIND_TRIDIAG: return tridiag_task(P, R, A, ignore_done, st);
+    case QOC_KIND_BITFLIP: return bitflip_task(P, R, A, ignore_done, st);
+    case QOC_KIND_STRANG: return strang_task(P, R, A, ignore_done, st);
+  }
+  return cudaErrorInvalidValue;
+}
+cudaError_t horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
+  switch (P.kind) {
+    case QOC_KIND_DENSE: return dense_horizon(P, R, which, k, st);
+    case QOC_KIND_TRIDIAG: return tridiag_horizon(P, R, which, k, st);
+    case QOC_KIND_BITFLIP: return bitflip_horizon(P, R, which, k, st);
+    case QOC_KIND_STRANG: return strang_horizon(P, R, which, k, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+struct Launcher {
+  qoc_ctx* ctx;
+  void operator()(cudaError_t e, const char* what) {
+    ++ctx->launches;
+    if (e == cudaErrorNotSupported) fail(QOC_ELOGIC, std::string(what) + ": not supported for this model kind");
+    ck(e, what);
+  }
+};
+
+template <class F>
+int32_t guarded(qoc_ctx* ctx, F&& f) {
+  if (!ctx) return QOC_EINVAL;
+  try {
+    ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+    f();
+    ctx->last_error.clear();
+    return QOC_OK;
+  } catch (const Fail& e) {
+    ctx->last_error = e.msg;
+    if (e.code == QOC_ECUDA) cudaGetLastError();
+    return e.code;
+  } catch (const std::exception& e) {
+    ctx->last_error = e.what();
+    return QOC_ERUNTIME;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t qoc_abi_version(void) { return QOC_ABI_VERSION; }
+
+int32_t qoc_ctx_create(const qoc_ctx_opts_v1* opts, qoc_ctx** out) {
+  if (!out) return QOC_EINVAL;
+  *out = nullptr;
+  if (opts && opts->abi_version != QOC_ABI_VERSION) return QOC_EINVAL;
+  int dev = opts ? opts->device : -1;
+  if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) return QOC_ECUDA;
+  if (cudaSetDevice(dev) != cudaSuccess) return QOC_ECUDA;
+  cudaDeviceProp prop{};
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return QOC_ECUDA;
+  if (prop.major < 10) return QOC_ECUDA;  // built for sm_100a only
+  auto* c = new qoc_ctx;
+  c->device = dev;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return QOC_ECUDA;
+  }
+  *out = c;
+  return QOC_OK;
+}
+
+void qoc_ctx_destroy(qoc_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* qoc_ctx_last_error(const qoc_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
+
+int64_t qoc_ctx_launch_count(const qoc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_v1* cfg,
+                    const qoc_solver_v1* solver, const double* u0, double* u_out, qoc_iter_record_v1* recs,
+                    int32_t rec_cap, double* task_values, qoc_run_status_v1* status) {
+  return guarded(ctx, [&] {
+    validate_problem(p);
+    if (!cfg || !solver || !u0 || !u_out || !recs || !status) fail(QOC_EINVAL, "null argument");
+    // ism.cpp:213-231
+    if (cfg->subintervals < 1 || cfg->workers < 1 || cfg->max_outer < 0 || cfg->eta < 0.0)
+      fail(QOC_EINVAL, "subintervals and workers must be >= 1, max_outer and eta >= 0");
+    const bool split = cfg->variant == QOC_VARIANT_SPLIT;
+    if (!split && p->kind == QOC_KIND_STRANG)
+      fail(QOC_EINVAL,
+           "interpolated waypoints require linear one-step flows; use the split variant for split-step states");
+    if (solver->kind != QOC_SOLVER_GRADIENT) fail(QOC_ELOGIC, "only the gradient solver is on this path");
+    if (rec_cap < cfg->max_outer + 1) fail(QOC_EINVAL, "rec_cap must be >= max_outer + 1");
+    const std::vector<int> node = decomposition(p->steps, cfg->subintervals, cfg->partition, cfg->node_index);
+    const int L = cfg->subintervals, B = p->batch, C = p->channels, K = p->steps;
+    const bool direct = cfg->plan == QOC_PLAN_DIRECT;
+    const bool assembled_interp = L > 1 && !split && !direct;
+    cudaStream_t st = ctx->stream;
+    Launcher launch{ctx};
+
+    DeviceProblem dp;
+    upload_problem(p, node, st, dp);
+    const DevProblem& P = dp.P;
+    DeviceRun dr;
+    alloc_run(dp, rec_cap, node, assembled_interp, false, st, dr);
+    const DevRun& R = dr.R;
+    ck(cudaMemcpyAsync(R.u, u0, sizeof(double) * B * K * C, cudaMemcpyHostToDevice, st), "u0");
+
+    const int max_outer = cfg->max_outer;
+    std::vector<cudaEvent_t> ev(max_outer + 2);
+    for (auto& e : ev) ck(cudaEventCreate(&e), "event");
+    auto destroy_events = [&] {
+      for (auto& e : ev) cudaEventDestroy(e);
+    };
+    try {
+      ck(cudaEventRecord(ev[0], st), "event");
+      // ---- bootstrap (ism.cpp:344-393)
+      if (L > 1) {
+        if (assembled_interp) {
+          TaskArgs A{M_ASSEMBLE, QOC_FORM_TRACKING, 1, 1, 0.0};
+          launch(task(P, R, A, 0, st), "assemble");
+          launch(chain_propagators(P, R, st), "chain");
+        } else {
+          launch(horizon(P, R, 0, 0, st), "node sweeps");
+        }
+        launch(penalty_partials(P, R, 0, st), "penalty");
+        launch(boundary_update(P, R, 0, split, 1, st), "boundary");
+      } else {
+        launch(set_single_tasks(P, R, st), "tasks");
+      }
+      ck(cudaEventRecord(ev[1], st), "event");
+
+      const int form = split ? QOC_FORM_OVERLAP : QOC_FORM_TRACKING;
+      int mode = M_ENTRY | M_UPDATE;
+      if (cfg->compute_error) mode |= M_ERROR;
+      if (assembled_interp) mode |= M_ASSEMBLE;
+      if (L > 1 && split && !direct) mode |= M_LAGGED;
+      TaskArgs A{mode, form, split ? 0 : 1, std::max(0, solver->inner_iterations), solver->step_size};
+      std::vector<int> h_done(B), h_status(B);
+      int ran = 0;
+      for (int k = 1; k <= max_outer; ++k) {
+        launch(task(P, R, A, 0, st), "task");
+        launch(penalty_partials(P, R, 0, st), "penalty");
+        launch(merge_iteration(P, R, k, nullptr, st), "merge");
+        if (L > 1) {
+          if (direct) launch(horizon(P, R, 0, k, st), "node sweeps");
+          else if (split) launch(split_nodes(P, R, st), "split nodes");
+          else launch(chain_propagators(P, R, st), "chain");
+          launch(boundary_update(P, R, k, split, 0, st), "boundary");
+        }
+        if (cfg->log_exact_objective) launch(horizon(P, R, 1, k, st), "exact objective");
+        launch(finish_iteration_ex(P, R, k, cfg->compute_error, cfg->eta, cfg->log_exact_objective, st), "finish");
+        ck(cudaEventRecord(ev[k + 1], st), "event");
+        ran = k;
+        if (k % 8 == 0 || k == max_outer) {  // early exit once every problem stopped
+          ck(cudaMemcpyAsync(h_done.data(), R.done, sizeof(int) * B, cudaMemcpyDeviceToHost, st), "poll");
+          ck(cudaMemcpyAsync(h_status.data(), R.status, sizeof(int) * B, cudaMemcpyDeviceToHost, st), "poll");
+          ck(cudaStreamSynchronize(st), "poll");
+          bool all = true;
+          for (int b = 0; b < B; ++b) all = all && (h_done[b] || h_status[b]);
+          if (all) break;
+        }
+      }
+      // ---- trailing evaluation (ism.cpp:594-609)
+      {
+        TaskArgs T{M_ENTRY, form, split ? 0 : 1, 1, 0.0};
+        launch(task(P, R, T, 1, st), "trailing task");
+        launch(trailing_values(P, R, st), "trailing");
+      }
+      ck(cudaStreamSynchronize(st), "run");
+
+      // ---- download
+      std::vector<int> n_recs(B), stat(B), abort_iter(B), flags((size_t)B * rec_cap);
+      std::vector<double> obj((size_t)B * rec_cap), err((size_t)B * rec_cap), exact((size_t)B * rec_cap);
+      ck(cudaMemcpy(u_out, R.u, sizeof(double) * B * K * C, cudaMemcpyDeviceToHost), "u_out");
+      ck(cudaMemcpy(n_recs.data(), R.n_recs, sizeof(int) * B, cudaMemcpyDeviceToHost), "n_recs");
+      ck(cudaMemcpy(stat.data(), R.status, sizeof(int) * B, cudaMemcpyDeviceToHost), "status");
+      ck(cudaMemcpy(abort_iter.data(), R.abort_iter, sizeof(int) * B, cudaMemcpyDeviceToHost), "abort");
+      ck(cudaMemcpy(flags.data(), R.rec_flags, sizeof(int) * flags.size(), cudaMemcpyDeviceToHost), "flags");
+      ck(cudaMemcpy(obj.data(), R.rec_obj, sizeof(double) * obj.size(), cudaMemcpyDeviceToHost), "obj");
+      ck(cudaMemcpy(err.data(), R.rec_err, sizeof(double) * err.size(), cudaMemcpyDeviceToHost), "err");
+      ck(cudaMemcpy(exact.data(), R.rec_exact, sizeof(double) * exact.size(), cudaMemcpyDeviceToHost), "exact");
+      if (task_values)
+        ck(cudaMemcpy(task_values, R.rec_tv, sizeof(double) * (size_t)B * rec_cap * L, cudaMemcpyDeviceToHost),
+           "task values");
+      std::vector<float> secs(ran + 1, 0.f);
+      for (int k = 0; k <= ran; ++k) ck(cudaEventElapsedTime(&secs[k], ev[k], ev[k + 1]), "elapsed");
+      for (int b = 0; b < B; ++b) {
+        qoc_run_status_v1& s = status[b];
+        std::memset(&s, 0, sizeof(s));
+        s.aborted = stat[b] != 0;
+        s.iterations_recorded = n_recs[b];
+        if (stat[b] == 1)
+          std::snprintf(s.abort_reason, sizeof(s.abort_reason),
+                        "non-finite control after the task updates of iteration %d", abort_iter[b]);
+        else if (stat[b] == 2)
+          std::snprintf(s.abort_reason, sizeof(s.abort_reason), "non-finite boundary state at iteration %d",
+                        abort_iter[b]);
+        else if (stat[b] == 3)
+          std::snprintf(s.abort_reason, sizeof(s.abort_reason), "non-finite boundary state during bootstrap");
+        for (int k = 0; k < n_recs[b]; ++k) {
+          const size_t r = (size_t)b * rec_cap + k;
+          qoc_iter_record_v1& o = recs[r];
+          o.iteration = k;
+          o.objective = obj[r];
+          o.has_error = (flags[r] & 1) != 0;
+          o.error = err[r];
+          o.has_exact_objective = (flags[r] & 2) != 0;
+          o.exact_objective = exact[r];
+          o.device_seconds = k <= ran ? 1e-3 * secs[k] : 0.0;
+          o.reserved = 0;
+        }
+      }
+    } catch (...) {
+      cudaStreamSynchronize(st);
+      destroy_events();
+      throw;
+    }
+    destroy_events();
+  });
+}
+
+namespace {
+// Single-task helper runs for the reference's helper entry points (L = 1 over the horizon).
+void single_run(qoc_ctx* ctx, const qoc_problem_v1* p, const double* u, int mode, int form, bool need_prop,
+                bool need_grad, DeviceProblem& dp, DeviceRun& dr) {
+  const std::vector<int> node{0, p->steps};
+  cudaStream_t st = ctx->stream;
+  upload_problem(p, node, st, dp);
+  alloc_run(dp, 1, node, need_prop, need_grad, st, dr);
+  ck(cudaMemcpyAsync(dr.R.u, u, sizeof(double) * p->batch * p->steps * p->channels, cudaMemcpyHostToDevice, st),
+     "u");
+  Launcher launch{ctx};
+  launch(set_single_tasks(dp.P, dr.R, st), "tasks");
+  TaskArgs A{mode, form, 0, 1, 0.0};
+  launch(task(dp.P, dr.R, A, 0, st), "task");
+  ck(cudaStreamSynchronize(st), "run");
+}
+}  // namespace
+
+int32_t qoc_propagate_final(qoc_ctx* ctx, const qoc_problem_v1* p, const double* u, double* states_out) {
+  return guarded(ctx, [&] {
+    validate_problem(p);
+    if (!u || !states_out) fail(QOC_EINVAL, "null argument");
+    DeviceProblem dp;
+    DeviceRun dr;
+    single_run(ctx, p, u, M_FINAL, QOC_FORM_OVERLAP, false, false, dp, dr);
+    ck(cudaMemcpy(states_out, dr.R.psi_end, sizeof(double2) * p->batch * p->dim, cudaMemcpyDeviceToHost), "out");
+  });
+}
+
+int32_t qoc_objective_gradient(qoc_ctx* ctx, const qoc_problem_v1* p, const double* u, int32_t form,
+                               int32_t naive, double* value_out, double* grad_out) {
+  return guarded(ctx, [&] {
+    validate_problem(p);
+    if (!u) fail(QOC_EINVAL, "null argument");
+    if (naive && p->kind != QOC_KIND_STRANG) naive = 0;
+    DeviceProblem dp;
+    DeviceRun dr;
+    int mode = M_ENTRY | (grad_out ? M_GRAD : 0) | (naive ? (1 << 10) : 0);
+    single_run(ctx, p, u, mode, form, false, grad_out != nullptr, dp, dr);
+    if (value_out) ck(cudaMemcpy(value_out, dr.R.entry, sizeof(double) * p->batch, cudaMemcpyDeviceToHost), "value");
+    if (grad_out)
+      ck(cudaMemcpy(grad_out, dr.R.grad, sizeof(double) * p->batch * p->steps * p->channels,
+                    cudaMemcpyDeviceToHost),
+         "grad");
+  });
+}
+
+int32_t qoc_assemble_propagator(qoc_ctx* ctx, const qoc_problem_v1* p, const double* u, double* prop_out) {
+  return guarded(ctx, [&] {
+    validate_problem(p);
+    if (!u || !prop_out) fail(QOC_EINVAL, "null argument");
+    if (p->kind == QOC_KIND_STRANG)
+      fail(QOC_ELOGIC, "no dense one-step matrices to assemble for this propagator kind");
+    DeviceProblem dp;
+    DeviceRun dr;
+    single_run(ctx, p, u, M_ASSEMBLE, QOC_FORM_TRACKING, true, false, dp, dr);
+    const size_t B = p->batch, d = p->dim;
+    std::vector<double2> rm(B * d * d);
+    ck(cudaMemcpy(rm.data(), dr.R.prop, sizeof(double2) * rm.size(), cudaMemcpyDeviceToHost), "prop");
+    for (size_t b = 0; b < B; ++b)  // row-major -> column-major (Eigen layout)
+      for (size_t i = 0; i < d; ++i)
+        for (size_t j = 0; j < d; ++j) {
+          const double2 v = rm[b * d * d + i * d + j];
+          prop_out[2 * (b * d * d + i + j * d)] = v.x;
+          prop_out[2 * (b * d * d + i + j * d) + 1] = v.y;
+        }
+  });
+}
+
+}  // extern "C"

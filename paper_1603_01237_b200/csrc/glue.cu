@@ -1,0 +1,282 @@
+// glue.cu — kind-independent ISM coordinator kernels (sm_100a).
+//
+// These replace the serial coordinator of run_ism (ism.cpp:481-591): the deterministic
+// index-order merge of task results, the abort checks, the propagator chain
+// (compose_from_propagators, ism.cpp:298-312), the split-variant node refresh
+// (ism.cpp:546-552), the boundary objective (ism.cpp:285-296) and the waypoint rebuild
+// (interpolated_waypoints + make_subproblems, ism.cpp:100-159).  Every reduction runs in a
+// fixed order, so results do not depend on scheduling.
+#include <math.h>
+
+#include "kernels.h"
+
+namespace qoc {
+
+namespace {
+
+__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ULL); }
+
+template <int NT>
+__device__ double block_sum(double v, double* sh) {
+  sh[threadIdx.x] = v;
+  __syncthreads();
+#pragma unroll
+  for (int s = NT / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// sum_j alpha_j |u_j|^2 over each task window (weighted_l2_penalty, controls.cpp:174-181)
+// and the finite-control flag (ism.cpp:527-539).
+__global__ void penalty_kernel(DevProblem P, DevRun R, int ignore_done) {
+  const int n = blockIdx.x, b = blockIdx.y;
+  if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
+  const int j0 = P.node[n], j1 = P.node[n + 1];
+  const double* u = R.u + (size_t)b * P.K * P.C;
+  double acc = 0.0;
+  int bad = 0;
+  for (int j = j0 + (int)threadIdx.x; j < j1; j += 32) {
+    double sq = 0.0;
+    for (int c = 0; c < P.C; ++c) {
+      const double v = u[(size_t)j * P.C + c];
+      sq += v * v;
+      bad |= !isfinite(v);
+    }
+    acc += P.alpha[j] * sq;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  bad = __any_sync(0xffffffffu, bad);
+  if (threadIdx.x == 0) {
+    R.pen[(size_t)b * P.L + n] = acc;
+    R.bad_u[(size_t)b * P.L + n] = bad;
+  }
+}
+
+// Index-order merge of task results (ism.cpp:481-539).
+__global__ void merge_kernel(DevProblem P, DevRun R, int k) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= P.B || R.done[b] || R.status[b]) return;
+  double tot = 0.0, esum = 0.0;
+  int bad = 0;
+  double* tv = R.rec_tv + ((size_t)b * R.cap + (k - 1)) * P.L;
+  for (int n = 0; n < P.L; ++n) {
+    const double e = R.entry[(size_t)b * P.L + n];
+    tv[n] = e;
+    esum += e;
+    tot += R.err[(size_t)b * P.L + n];
+    bad |= R.bad_u[(size_t)b * P.L + n];
+  }
+  if (P.L == 1) R.rec_obj[(size_t)b * R.cap + (k - 1)] = esum;
+  R.tot_err[b] = tot;
+  if (bad) {
+    R.status[b] = 1;
+    R.abort_iter[b] = k;
+    R.rec_obj[(size_t)b * R.cap + k] = qnan();
+    R.rec_flags[(size_t)b * R.cap + k] = 0;
+    R.n_recs[b] = k + 1;
+  }
+}
+
+// compose_from_propagators for d <= 1024 held row-major: psi_{n+1} = M_n psi_n,
+// chi_n = M_n^dagger chi_{n+1}.  One CTA per problem, rows over threads.
+__global__ void chain_kernel(DevProblem P, DevRun R) {
+  extern __shared__ double2 vsh[];
+  const int b = blockIdx.x;
+  if (R.done[b] || R.status[b]) return;
+  const int d = P.d, L = P.L;
+  double2* psi = R.psi_nodes + (size_t)b * (L + 1) * d;
+  double2* chi = R.chi_nodes + (size_t)b * (L + 1) * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    psi[i] = P.init[(size_t)b * d + i];
+    chi[(size_t)L * d + i] = P.targ[(size_t)b * d + i];
+  }
+  __syncthreads();
+  for (int n = 0; n < L; ++n) {
+    const double2* M = R.prop + ((size_t)b * L + n) * (size_t)d * d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) vsh[i] = psi[(size_t)n * d + i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+      double2 acc = cx(0.0, 0.0);
+      for (int kk = 0; kk < d; ++kk) acc = cfma(M[(size_t)i * d + kk], vsh[kk], acc);
+      psi[(size_t)(n + 1) * d + i] = acc;
+    }
+    __syncthreads();
+  }
+  for (int n = L - 1; n >= 0; --n) {
+    const double2* M = R.prop + ((size_t)b * L + n) * (size_t)d * d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) vsh[i] = chi[(size_t)(n + 1) * d + i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+      double2 acc = cx(0.0, 0.0);
+      for (int kk = 0; kk < d; ++kk) acc = cfmaconj(M[(size_t)kk * d + i], vsh[kk], acc);
+      chi[(size_t)n * d + i] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+// Split variant, assembled plan: lagged endpoint states become the new nodes (ism.cpp:546-552).
+__global__ void split_nodes_kernel(DevProblem P, DevRun R) {
+  const int b = blockIdx.x;
+  if (R.done[b] || R.status[b]) return;
+  const int d = P.d, L = P.L;
+  double2* psi = R.psi_nodes + (size_t)b * (L + 1) * d;
+  double2* chi = R.chi_nodes + (size_t)b * (L + 1) * d;
+  for (int e = threadIdx.x; e < L * d; e += blockDim.x) {
+    const int n = e / d, i = e % d;
+    psi[(size_t)(n + 1) * d + i] = R.psi_end[((size_t)b * L + n) * d + i];
+    chi[(size_t)n * d + i] = R.chi_start[((size_t)b * L + n) * d + i];
+  }
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    psi[i] = P.init[(size_t)b * d + i];
+    chi[(size_t)L * d + i] = P.targ[(size_t)b * d + i];
+  }
+}
+
+// Finite checks of the nodes, boundary objective, task rebuild.
+template <int NT>
+__global__ void __launch_bounds__(NT) boundary_kernel(DevProblem P, DevRun R, int k, int split, int boot) {
+  __shared__ double sh[NT];
+  __shared__ int bad_sh;
+  const int b = blockIdx.x;
+  if (R.done[b] || R.status[b]) return;
+  const int d = P.d, L = P.L;
+  const double2* psi = R.psi_nodes + (size_t)b * (L + 1) * d;
+  const double2* chi = R.chi_nodes + (size_t)b * (L + 1) * d;
+  if (threadIdx.x == 0) bad_sh = 0;
+  __syncthreads();
+  int bad = 0;
+  for (int e = threadIdx.x; e < (L + 1) * d; e += NT) bad |= !cfinite(psi[e]) | !cfinite(chi[e]);
+  if (bad) atomicOr(&bad_sh, 1);
+  __syncthreads();
+  if (bad_sh) {
+    if (threadIdx.x == 0) {
+      R.status[b] = boot ? 3 : 2;
+      R.abort_iter[b] = k;
+      R.rec_obj[(size_t)b * R.cap + k] = qnan();
+      R.rec_flags[(size_t)b * R.cap + k] = 0;
+      R.n_recs[b] = k + 1;
+    }
+    return;
+  }
+  // boundary_objective (ism.cpp:285-296)
+  const double2* last = psi + (size_t)L * d;
+  const double2* tg = P.targ + (size_t)b * d;
+  double part = 0.0;
+  for (int i = threadIdx.x; i < d; i += NT) {
+    if (split) part += cconjmul(tg[i], last[i]).x;
+    else part += cabs2(csub(last[i], tg[i]));
+  }
+  const double s = block_sum<NT>(part, sh);
+  if (threadIdx.x == 0) {
+    double fid;
+    if (split) {
+      fid = P.ip_w * s;
+    } else {
+      const double dist = sqrt(fmax(0.0, P.ip_w * s));
+      fid = -0.5 * dist * dist;
+    }
+    double pen = 0.0;
+    for (int n = 0; n < L; ++n) pen += R.pen[(size_t)b * L + n];
+    R.rec_obj[(size_t)b * R.cap + k] = fid - 0.5 * P.dt * pen;
+  }
+  // rebuild_tasks (ism.cpp:260-280)
+  const double total = (double)P.K;
+  for (int e = threadIdx.x; e < L * d; e += NT) {
+    const int n = e / d, i = e % d;
+    double2 in, tgv;
+    if (split) {
+      in = psi[(size_t)n * d + i];
+      tgv = chi[(size_t)(n + 1) * d + i];
+    } else {
+      const int j0 = P.node[n], j1 = P.node[n + 1];
+      const double a0 = (total - j0) / total, b0 = j0 / total;
+      const double a1 = (total - j1) / total, b1 = j1 / total;
+      const double2 p0 = psi[(size_t)n * d + i], c0 = chi[(size_t)n * d + i];
+      const double2 p1 = psi[(size_t)(n + 1) * d + i], c1 = chi[(size_t)(n + 1) * d + i];
+      in = cx(a0 * p0.x + b0 * c0.x, a0 * p0.y + b0 * c0.y);
+      tgv = cx(a1 * p1.x + b1 * c1.x, a1 * p1.y + b1 * c1.y);
+    }
+    R.task_init[((size_t)b * L + n) * d + i] = in;
+    R.task_targ[((size_t)b * L + n) * d + i] = tgv;
+  }
+}
+
+__global__ void single_tasks_kernel(DevProblem P, DevRun R) {
+  const int b = blockIdx.x;
+  for (int i = threadIdx.x; i < P.d; i += blockDim.x) {
+    R.task_init[(size_t)b * P.d + i] = P.init[(size_t)b * P.d + i];
+    R.task_targ[(size_t)b * P.d + i] = P.targ[(size_t)b * P.d + i];
+  }
+}
+
+// Record the residual, stop on eta (ism.cpp:586-591).
+__global__ void finish_kernel(DevProblem P, DevRun R, int k, int compute_error, double eta, int log_exact) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= P.B || R.done[b] || R.status[b]) return;
+  const size_t r = (size_t)b * R.cap + k;
+  if (P.L == 1) R.rec_obj[r] = qnan();
+  R.rec_err[r] = compute_error ? R.tot_err[b] : qnan();
+  R.rec_flags[r] = (compute_error ? 1 : 0) | (log_exact ? 2 : 0);
+  R.n_recs[b] = k + 1;
+  if (compute_error && R.tot_err[b] <= eta) R.done[b] = 1;
+}
+
+// Trailing evaluation (ism.cpp:594-609).
+__global__ void trailing_kernel(DevProblem P, DevRun R) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= P.B || R.status[b]) return;
+  const int last = R.n_recs[b] - 1;
+  double* tv = R.rec_tv + ((size_t)b * R.cap + last) * P.L;
+  for (int n = 0; n < P.L; ++n) tv[n] = R.entry[(size_t)b * P.L + n];
+  if (P.L == 1) R.rec_obj[(size_t)b * R.cap + last] = R.entry[b];
+}
+
+}  // namespace
+
+cudaError_t penalty_partials(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st) {
+  penalty_kernel<<<dim3(P.L, P.B), 32, 0, st>>>(P, R, ignore_done);
+  return cudaGetLastError();
+}
+cudaError_t merge_iteration(const DevProblem& P, const DevRun& R, int k, double*, cudaStream_t st) {
+  merge_kernel<<<(P.B + 127) / 128, 128, 0, st>>>(P, R, k);
+  return cudaGetLastError();
+}
+cudaError_t chain_propagators(const DevProblem& P, const DevRun& R, cudaStream_t st) {
+  const int nt = P.d >= 256 ? 1024 : (P.d <= 32 ? 32 : 256);
+  chain_kernel<<<P.B, nt, sizeof(double2) * P.d, st>>>(P, R);
+  return cudaGetLastError();
+}
+cudaError_t split_nodes(const DevProblem& P, const DevRun& R, cudaStream_t st) {
+  split_nodes_kernel<<<P.B, 256, 0, st>>>(P, R);
+  return cudaGetLastError();
+}
+cudaError_t boundary_update(const DevProblem& P, const DevRun& R, int k, int split, int boot, cudaStream_t st) {
+  boundary_kernel<128><<<P.B, 128, 0, st>>>(P, R, k, split, boot);
+  return cudaGetLastError();
+}
+cudaError_t set_single_tasks(const DevProblem& P, const DevRun& R, cudaStream_t st) {
+  single_tasks_kernel<<<P.B, 128, 0, st>>>(P, R);
+  return cudaGetLastError();
+}
+cudaError_t finish_iteration(const DevProblem& P, const DevRun& R, int k, const double*, int compute_error,
+                             double eta, cudaStream_t st) {
+  finish_kernel<<<(P.B + 127) / 128, 128, 0, st>>>(P, R, k, compute_error, eta, 0);
+  return cudaGetLastError();
+}
+cudaError_t finish_iteration_ex(const DevProblem& P, const DevRun& R, int k, int compute_error, double eta,
+                                int log_exact, cudaStream_t st) {
+  finish_kernel<<<(P.B + 127) / 128, 128, 0, st>>>(P, R, k, compute_error, eta, log_exact);
+  return cudaGetLastError();
+}
+cudaError_t trailing_values(const DevProblem& P, const DevRun& R, cudaStream_t st) {
+  trailing_kernel<<<(P.B + 127) / 128, 128, 0, st>>>(P, R);
+  return cudaGetLastError();
+}
+
+}  // namespace qoc

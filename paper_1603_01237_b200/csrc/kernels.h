@@ -1,0 +1,38 @@
+// kernels.h — launchers exported by the kernel translation units to the host driver.
+#pragma once
+
+#include "common.cuh"
+
+namespace qoc {
+
+// dense (d <= 32)
+int dense_pad(int d);
+cudaError_t dense_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
+cudaError_t dense_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st);
+
+// tridiagonal (d <= 32)
+cudaError_t tridiag_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
+cudaError_t tridiag_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st);
+
+// bit-flip spin register (d = 2^n, n <= 12)
+cudaError_t bitflip_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
+cudaError_t bitflip_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st);
+
+// split-step condensate
+cudaError_t strang_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
+cudaError_t strang_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st);
+
+// glue (kind independent)
+cudaError_t penalty_partials(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st);
+cudaError_t merge_iteration(const DevProblem& P, const DevRun& R, int k, double* tot_err, cudaStream_t st);
+cudaError_t chain_propagators(const DevProblem& P, const DevRun& R, cudaStream_t st);
+cudaError_t split_nodes(const DevProblem& P, const DevRun& R, cudaStream_t st);
+cudaError_t boundary_update(const DevProblem& P, const DevRun& R, int k, int split, int boot, cudaStream_t st);
+cudaError_t set_single_tasks(const DevProblem& P, const DevRun& R, cudaStream_t st);
+cudaError_t finish_iteration(const DevProblem& P, const DevRun& R, int k, const double* tot_err, int compute_error,
+                             double eta, cudaStream_t st);
+cudaError_t finish_iteration_ex(const DevProblem& P, const DevRun& R, int k, int compute_error, double eta,
+                                int log_exact, cudaStream_t st);
+cudaError_t trailing_values(const DevProblem& P, const DevRun& R, cudaStream_t st);
+
+}  // namespace qoc

@@ -1,0 +1,378 @@
+"""Reference-facing API of the ISM hot path (the Python mirror of qoc's C++ solver API).
+
+    IsmRun run_ism(const ControlProblem&, const ControlField& u0, const IsmConfig&,
+                   const SolverSpec&)                      -- ism.hpp:80-81, ism.cpp:211-612
+
+``run_ism`` here has the same argument meaning, record semantics and error behaviour, and
+executes on the B200 through ``libqoc_b200.so`` (include/qoc_gpu.h).  There is no CPU path:
+if the native library is missing the call fails loudly (see ``_native``).
+
+Controls are numpy arrays of shape (C, K) -- the reference's C x K sample matrix
+(controls.hpp:33-60) -- or (B, C, K) for a batch of independent problems.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import abi
+from .models import HamiltonianModel
+
+
+# ----------------------------------------------------------------------------------------
+# Exceptions mirroring the reference's exception types (SURVEY §8(b) conventions).
+# ----------------------------------------------------------------------------------------
+class InvalidArgument(ValueError):
+    """std::invalid_argument"""
+
+
+class LogicError(Exception):
+    """std::logic_error"""
+
+
+class QocRuntimeError(RuntimeError):
+    """std::runtime_error (e.g. decomposition errors, controls.cpp:16-18)"""
+
+
+class DeviceError(RuntimeError):
+    """CUDA / NCCL failure"""
+
+
+def raise_for(code: int, msg: str) -> None:
+    if code == abi.QOC_OK:
+        return
+    exc = {abi.QOC_EINVAL: InvalidArgument, abi.QOC_ELOGIC: LogicError,
+           abi.QOC_ERUNTIME: QocRuntimeError}.get(code, DeviceError)
+    raise exc(msg or f"qoc error {code}")
+
+
+# ----------------------------------------------------------------------------------------
+# Problem / config types
+# ----------------------------------------------------------------------------------------
+@dataclass(frozen=True)
+class TimeGrid:
+    """Uniform step grid (controls.hpp:14-25)."""
+    t_start: float
+    dt: float
+    steps: int
+
+    @staticmethod
+    def over(t0: float, t1: float, steps: int) -> "TimeGrid":  # controls.cpp:55-59
+        if steps <= 0:
+            raise QocRuntimeError("TimeGrid: steps must be positive")
+        if not t1 > t0:
+            raise QocRuntimeError("TimeGrid: t_end must exceed t_start")
+        return TimeGrid(float(t0), (t1 - t0) / steps, int(steps))
+
+    def node(self, j: int) -> float:
+        return self.t_start + self.dt * j
+
+
+@dataclass
+class ControlProblem:
+    """objective.hpp:18-24: model, grid, initial and target states, per-step penalty."""
+    model: HamiltonianModel
+    grid: TimeGrid
+    initial: np.ndarray            # (d,) or (B, d) complex
+    target: np.ndarray             # (d,) or (B, d) complex
+    penalty: Optional[np.ndarray] = None   # (K,) alpha_j, None = 0
+
+    @property
+    def batch(self) -> int:
+        return self.model.batch
+
+
+@dataclass
+class IsmConfig:
+    """ism.hpp:12-39 (plus the decomposition choice)."""
+    subintervals: int = 1
+    workers: int = 1
+    eta: float = 1e-3
+    max_outer: int = 50
+    variant: str = "interpolated"      # or "split"
+    plan: str = "assembled"            # or "direct"
+    compute_error: bool = True
+    log_exact_objective: bool = False
+    checkpoint_stride: int = 0
+    partition: str = "balanced"        # "uniform" = Decomposition::uniform; "explicit"
+    node_index: Optional[Sequence[int]] = None
+
+
+@dataclass
+class SolverSpec:
+    """optimizers.hpp:9-30; the constant-step gradient kind is the hot path."""
+    kind: str = "gradient"
+    step_size: float = 1.0
+    inner_iterations: int = 1
+    naive_nonlinear_adjoint: bool = False
+    checkpoint_stride: int = 0
+
+
+@dataclass
+class IterationStat:
+    """runtime.hpp:44-63."""
+    iteration: int
+    objective: float
+    exact_objective: Optional[float] = None
+    error: Optional[float] = None
+    task_values: list = field(default_factory=list)
+    device_seconds: float = 0.0
+
+
+@dataclass
+class RunRecord:
+    """runtime.hpp:65-75."""
+    subintervals: int = 1
+    workers: int = 1
+    solver: str = "gradient"
+    variant: str = "interpolated"
+    plan: str = "assembled"
+    iterations: list = field(default_factory=list)
+    aborted: bool = False
+    abort_reason: str = ""
+
+    def objectives(self) -> np.ndarray:
+        return np.array([it.objective for it in self.iterations])
+
+
+@dataclass
+class IsmRun:
+    """ism.hpp:74-77: the optimized control (C, K) and the run record."""
+    control: np.ndarray
+    record: RunRecord
+
+
+# ----------------------------------------------------------------------------------------
+# Packing into the C ABI (shared with the test-side oracle wrapper).
+# ----------------------------------------------------------------------------------------
+def _states(a, B: int, d: int, what: str) -> np.ndarray:
+    a = np.asarray(a, dtype=np.complex128)
+    if a.ndim == 2 and a.shape[1] == 1 and B == 1 and a.shape[0] == d:
+        a = a[:, 0]
+    if a.ndim == 1:
+        a = np.broadcast_to(a[None], (B, a.shape[0]))
+    if a.shape != (B, d):
+        raise InvalidArgument(f"{what} state has shape {a.shape}, expected ({B}, {d})")
+    return np.ascontiguousarray(a)
+
+
+def pack_problem(p: ControlProblem) -> abi.PackedProblem:
+    if p.model is None:
+        raise InvalidArgument("problem has no model")
+    m = p.model
+    s = abi.ProblemV1()
+    keep: list = []
+    s.abi_version = abi.QOC_ABI_VERSION
+    s.kind = m.kind
+    s.dim = m.state_dim()
+    s.channels = m.channels()
+    s.steps = p.grid.steps
+    s.batch = m.batch
+    s.t_start = p.grid.t_start
+    s.dt = p.grid.dt
+    s.ip_weight = m.ip_weight()
+    m.pack_into(s, keep)
+    ini = abi.cplx(_states(p.initial, m.batch, s.dim, "initial"))
+    tgt = abi.cplx(_states(p.target, m.batch, s.dim, "target"))
+    keep += [ini, tgt]
+    s.initial, s.target = abi.dptr(ini), abi.dptr(tgt)
+    if p.penalty is not None:
+        pen = np.ascontiguousarray(np.broadcast_to(np.asarray(p.penalty, dtype=np.float64), (p.grid.steps,)))
+        keep.append(pen)
+        s.penalty = abi.dptr(pen)
+    return abi.PackedProblem(s, keep)
+
+
+def controls_to_abi(u, B: int, Cn: int, K: int) -> np.ndarray:
+    """(C, K) or (B, C, K) samples -> [B][K][C] contiguous (column-major C x K per problem)."""
+    u = np.asarray(u, dtype=np.float64)
+    if u.ndim == 2:
+        u = np.broadcast_to(u[None], (B,) + u.shape)
+    if u.shape != (B, Cn, K):
+        raise InvalidArgument(f"control has shape {u.shape}, expected ({B}, {Cn}, {K}) "
+                              "(initial control grid/channel count does not match the problem)")
+    return np.ascontiguousarray(np.swapaxes(u, 1, 2)).reshape(-1)
+
+
+def controls_from_abi(flat: np.ndarray, B: int, Cn: int, K: int) -> np.ndarray:
+    return np.ascontiguousarray(np.swapaxes(flat.reshape(B, K, Cn), 1, 2))
+
+
+_VARIANTS = {"interpolated": abi.VARIANT_INTERPOLATED, "split": abi.VARIANT_SPLIT}
+_PLANS = {"assembled": abi.PLAN_ASSEMBLED, "direct": abi.PLAN_DIRECT}
+_PARTS = {"balanced": abi.PARTITION_BALANCED, "uniform": abi.PARTITION_UNIFORM,
+          "explicit": abi.PARTITION_EXPLICIT}
+_SOLVERS = {"gradient": abi.SOLVER_GRADIENT, "monotonic": abi.SOLVER_MONOTONIC,
+            "newton": abi.SOLVER_NEWTON}
+
+
+def pack_config(cfg: IsmConfig):
+    c = abi.IsmConfigV1()
+    c.subintervals, c.workers, c.max_outer = cfg.subintervals, cfg.workers, cfg.max_outer
+    try:
+        c.variant, c.plan = _VARIANTS[cfg.variant], _PLANS[cfg.plan]
+        c.partition = _PARTS[cfg.partition]
+    except KeyError as e:
+        raise InvalidArgument(f"unknown option {e}") from None
+    c.compute_error = int(cfg.compute_error)
+    c.log_exact_objective = int(cfg.log_exact_objective)
+    c.checkpoint_stride = cfg.checkpoint_stride
+    c.eta = cfg.eta
+    keep = None
+    if cfg.node_index is not None:
+        keep = np.ascontiguousarray(cfg.node_index, dtype=np.int32)
+        c.node_index = abi.iptr(keep)
+        c.partition = abi.PARTITION_EXPLICIT
+    return c, keep
+
+
+def pack_solver(sv: SolverSpec):
+    s = abi.SolverV1()
+    if sv.kind not in _SOLVERS:
+        raise InvalidArgument(f"unknown solver {sv.kind}")
+    s.kind = _SOLVERS[sv.kind]
+    s.inner_iterations = sv.inner_iterations
+    s.naive_nonlinear_adjoint = int(sv.naive_nonlinear_adjoint)
+    s.checkpoint_stride = sv.checkpoint_stride
+    s.step_size = sv.step_size
+    return s
+
+
+def unpack_records(recs: np.ndarray, tvals: np.ndarray, status, cfg: IsmConfig,
+                   solver: SolverSpec, b: int) -> RunRecord:
+    st = status[b]
+    n = st.iterations_recorded
+    rec = RunRecord(subintervals=cfg.subintervals, workers=cfg.workers, solver=solver.kind,
+                    variant=cfg.variant, plan=cfg.plan, aborted=bool(st.aborted),
+                    abort_reason=st.abort_reason.decode())
+    for k in range(n):
+        r = recs[b, k]
+        rec.iterations.append(IterationStat(
+            iteration=int(r["iteration"]), objective=float(r["objective"]),
+            exact_objective=float(r["exact_objective"]) if r["has_exact_objective"] else None,
+            error=float(r["error"]) if r["has_error"] else None,
+            task_values=[float(v) for v in tvals[b, k]],
+            device_seconds=float(r["device_seconds"])))
+    return rec
+
+
+def run_buffers(p: ControlProblem, cfg: IsmConfig):
+    B, L = p.batch, cfg.subintervals
+    cap = max(cfg.max_outer, 0) + 1
+    recs = np.zeros((B, cap), dtype=abi.REC_DTYPE)
+    tvals = np.full((B, cap, max(L, 1)), np.nan)
+    status = (abi.RunStatusV1 * B)()
+    return cap, recs, tvals, status
+
+
+def _validate(p: ControlProblem, cfg: IsmConfig) -> None:
+    if cfg.variant == "interpolated" and not p.model.is_linear():
+        raise InvalidArgument("interpolated waypoints require linear one-step flows; use the split "
+                              "variant for split-step states")
+
+
+# ----------------------------------------------------------------------------------------
+# The device entry points.
+# ----------------------------------------------------------------------------------------
+def run_ism_batch(p: ControlProblem, u0, cfg: IsmConfig, solver: SolverSpec,
+                  ctx=None) -> list[IsmRun]:
+    """run_ism for every problem of a batched ControlProblem, in one device call."""
+    from . import _native
+    _validate(p, cfg)
+    packed = pack_problem(p)
+    B, Cn, K = p.batch, p.model.channels(), p.grid.steps
+    u_in = controls_to_abi(u0, B, Cn, K)
+    u_out = np.empty_like(u_in)
+    c, keep = pack_config(cfg)
+    s = pack_solver(solver)
+    cap, recs, tvals, status = run_buffers(p, cfg)
+    ctx = ctx or _native.default_context()
+    code = ctx.lib.qoc_ism_run(ctx.handle, packed.ref, C.byref(c), C.byref(s), abi.dptr(u_in),
+                               abi.dptr(u_out), recs.ctypes.data_as(C.c_void_p), cap,
+                               abi.dptr(tvals), status)
+    raise_for(code, ctx.last_error())
+    u = controls_from_abi(u_out, B, Cn, K)
+    return [IsmRun(u[b], unpack_records(recs, tvals, status, cfg, solver, b)) for b in range(B)]
+
+
+def run_ism(p: ControlProblem, u0, cfg: IsmConfig, solver: SolverSpec, ctx=None) -> IsmRun:
+    """ism.hpp:80-81 -- single-problem solve on the device."""
+    if p.batch != 1:
+        raise InvalidArgument("run_ism takes one problem; use run_ism_batch")
+    return run_ism_batch(p, u0, cfg, solver, ctx)[0]
+
+
+def propagate_final(p: ControlProblem, u, ctx=None) -> np.ndarray:
+    """propagation.cpp:194-200, on the device: (B, d) final states."""
+    from . import _native
+    packed = pack_problem(p)
+    B, Cn, K, d = p.batch, p.model.channels(), p.grid.steps, p.model.state_dim()
+    u_in = controls_to_abi(u, B, Cn, K)
+    out = np.empty(2 * B * d)
+    ctx = ctx or _native.default_context()
+    raise_for(ctx.lib.qoc_propagate_final(ctx.handle, packed.ref, abi.dptr(u_in), abi.dptr(out)),
+              ctx.last_error())
+    return out.view(np.complex128).reshape(B, d)
+
+
+def objective_gradient(p: ControlProblem, u, form: str = "tracking", naive: bool = False, ctx=None):
+    """evaluate_objective + objective_gradient (objective.cpp:93-129) on the device.
+    Returns (values (B,), gradients (B, C, K))."""
+    from . import _native
+    packed = pack_problem(p)
+    B, Cn, K = p.batch, p.model.channels(), p.grid.steps
+    u_in = controls_to_abi(u, B, Cn, K)
+    val = np.empty(B)
+    grad = np.empty_like(u_in)
+    f = abi.FORM_OVERLAP if form == "overlap" else abi.FORM_TRACKING
+    ctx = ctx or _native.default_context()
+    raise_for(ctx.lib.qoc_objective_gradient(ctx.handle, packed.ref, abi.dptr(u_in), f, int(naive),
+                                             abi.dptr(val), abi.dptr(grad)), ctx.last_error())
+    return val, controls_from_abi(grad, B, Cn, K)
+
+
+def evaluate_objective(p: ControlProblem, u, form: str = "tracking", ctx=None) -> np.ndarray:
+    from . import _native
+    packed = pack_problem(p)
+    B, Cn, K = p.batch, p.model.channels(), p.grid.steps
+    u_in = controls_to_abi(u, B, Cn, K)
+    val = np.empty(B)
+    f = abi.FORM_OVERLAP if form == "overlap" else abi.FORM_TRACKING
+    ctx = ctx or _native.default_context()
+    raise_for(ctx.lib.qoc_objective_gradient(ctx.handle, packed.ref, abi.dptr(u_in), f, 0,
+                                             abi.dptr(val), None), ctx.last_error())
+    return val
+
+
+def assemble_propagator(p: ControlProblem, u, ctx=None) -> np.ndarray:
+    """propagation.cpp:236-249 on the device: (B, d, d) products of the one-step maps."""
+    from . import _native
+    packed = pack_problem(p)
+    B, Cn, K, d = p.batch, p.model.channels(), p.grid.steps, p.model.state_dim()
+    u_in = controls_to_abi(u, B, Cn, K)
+    out = np.empty(2 * B * d * d)
+    ctx = ctx or _native.default_context()
+    raise_for(ctx.lib.qoc_assemble_propagator(ctx.handle, packed.ref, abi.dptr(u_in), abi.dptr(out)),
+              ctx.last_error())
+    return np.swapaxes(out.view(np.complex128).reshape(B, d, d), 1, 2)
+
+
+def balanced_nodes(K: int, L: int) -> list[int]:
+    """The balanced decomposition: first K mod L parts get ceil(K/L) steps."""
+    base, extra = divmod(K, L)
+    nodes = [0]
+    for n in range(L):
+        nodes.append(nodes[-1] + base + (1 if n < extra else 0))
+    return nodes
+
+
+def fidelity_history(run: IsmRun, split: bool = False) -> np.ndarray:
+    """F_k per SURVEY §8(d): 1 + objective (interpolated, alpha = 0) or exact_objective."""
+    its = run.record.iterations
+    if split:
+        return np.array([it.exact_objective if it.exact_objective is not None else math.nan for it in its])
+    return np.array([1.0 + it.objective for it in its])

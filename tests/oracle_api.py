@@ -1,0 +1,218 @@
+"""ctypes wrapper of the CPU oracle (oracle/_build/liboracle.so) -- TEST INFRASTRUCTURE.
+
+The oracle restates the reference's ISM path on the CPU (oracle/oracle.cpp).  It takes the
+same packed qoc_problem_v1 as the device library, so a test packs a problem once and feeds
+both sides.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+from paper_1603_01237_b200 import abi
+from paper_1603_01237_b200 import ism as I
+
+ROOT = Path(__file__).resolve().parents[1]
+LIBPATH = ROOT / "oracle" / "_build" / "liboracle.so"
+REFERENCE, STRUCTURED = 0, 1
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not LIBPATH.exists():
+            subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True)
+        _lib = C.CDLL(str(LIBPATH))
+        _lib.oracle_ism_run.restype = C.c_int32
+    return _lib
+
+
+def _err():
+    return C.create_string_buffer(512)
+
+
+def _check(code, err):
+    I.raise_for(code, err.value.decode())
+
+
+def ism_run(p: I.ControlProblem, u0, cfg: I.IsmConfig, solver: I.SolverSpec,
+            arith: int = STRUCTURED, threads: int | None = None) -> list[I.IsmRun]:
+    packed = I.pack_problem(p)
+    B, Cn, K = p.batch, p.model.channels(), p.grid.steps
+    u_in = I.controls_to_abi(u0, B, Cn, K)
+    u_out = np.empty_like(u_in)
+    c, keep = I.pack_config(cfg)
+    s = I.pack_solver(solver)
+    cap, recs, tvals, status = I.run_buffers(p, cfg)
+    err = _err()
+    threads = threads or os.cpu_count() or 1
+    code = lib().oracle_ism_run(packed.ref, C.byref(c), C.byref(s), abi.dptr(u_in), abi.dptr(u_out),
+                                recs.ctypes.data_as(C.c_void_p), C.c_int32(cap), abi.dptr(tvals),
+                                status, C.c_int32(arith), C.c_int32(threads), err, C.c_size_t(512))
+    _check(code, err)
+    u = I.controls_from_abi(u_out, B, Cn, K)
+    return [I.IsmRun(u[b], I.unpack_records(recs, tvals, status, cfg, solver, b)) for b in range(B)]
+
+
+def propagate_final(p, u, arith=STRUCTURED):
+    packed = I.pack_problem(p)
+    B, d = p.batch, p.model.state_dim()
+    u_in = I.controls_to_abi(u, B, p.model.channels(), p.grid.steps)
+    out = np.empty(2 * B * d)
+    err = _err()
+    _check(lib().oracle_propagate_final(packed.ref, abi.dptr(u_in), abi.dptr(out), C.c_int32(arith),
+                                        err, C.c_size_t(512)), err)
+    return out.view(np.complex128).reshape(B, d)
+
+
+def propagate(p, u, arith=STRUCTURED):
+    packed = I.pack_problem(p)
+    B, d, K = p.batch, p.model.state_dim(), p.grid.steps
+    u_in = I.controls_to_abi(u, B, p.model.channels(), K)
+    out = np.empty(2 * B * (K + 1) * d)
+    err = _err()
+    _check(lib().oracle_propagate(packed.ref, abi.dptr(u_in), abi.dptr(out), C.c_int32(arith), err,
+                                  C.c_size_t(512)), err)
+    return out.view(np.complex128).reshape(B, K + 1, d)
+
+
+def objective_gradient(p, u, form="tracking", naive=False, stride=0, arith=STRUCTURED):
+    packed = I.pack_problem(p)
+    B, Cn, K = p.batch, p.model.channels(), p.grid.steps
+    u_in = I.controls_to_abi(u, B, Cn, K)
+    val = np.empty(B)
+    grad = np.empty_like(u_in)
+    f = abi.FORM_OVERLAP if form == "overlap" else abi.FORM_TRACKING
+    err = _err()
+    _check(lib().oracle_objective_gradient(packed.ref, abi.dptr(u_in), C.c_int32(f), C.c_int32(int(naive)),
+                                           C.c_int32(stride), abi.dptr(val), abi.dptr(grad),
+                                           C.c_int32(arith), err, C.c_size_t(512)), err)
+    return val, I.controls_from_abi(grad, B, Cn, K)
+
+
+def assemble_propagator(p, u, arith=STRUCTURED):
+    packed = I.pack_problem(p)
+    B, d = p.batch, p.model.state_dim()
+    u_in = I.controls_to_abi(u, B, p.model.channels(), p.grid.steps)
+    out = np.empty(2 * B * d * d)
+    err = _err()
+    _check(lib().oracle_assemble_propagator(packed.ref, abi.dptr(u_in), abi.dptr(out), C.c_int32(arith),
+                                            err, C.c_size_t(512)), err)
+    return np.swapaxes(out.view(np.complex128).reshape(B, d, d), 1, 2)
+
+
+def step(p, u_col, dt, state, adjoint=False, psi_j=None, naive=False, arith=STRUCTURED):
+    packed = I.pack_problem(p)
+    d = p.model.state_dim()
+    uc = np.ascontiguousarray(np.asarray(u_col, dtype=np.float64).reshape(-1))
+    sin = abi.cplx(np.asarray(state).reshape(-1))
+    pj = abi.cplx(np.asarray(psi_j).reshape(-1)) if psi_j is not None else None
+    out = np.empty(2 * d)
+    err = _err()
+    _check(lib().oracle_step(packed.ref, abi.dptr(uc), C.c_double(dt), abi.dptr(sin), abi.dptr(pj),
+                             C.c_int32(int(adjoint)), C.c_int32(int(naive)), abi.dptr(out),
+                             C.c_int32(arith), err, C.c_size_t(512)), err)
+    return out.view(np.complex128).copy()
+
+
+def dft(x, inverse=False):
+    xi = abi.cplx(x)
+    out = np.empty_like(xi)
+    assert lib().oracle_dft(C.c_int32(len(x)), abi.dptr(xi), abi.dptr(out), C.c_int32(int(inverse))) == 0
+    return out.view(np.complex128).copy()
+
+
+def verify_decomposition(p, u, parts, arith=STRUCTURED):
+    packed = I.pack_problem(p)
+    u_in = I.controls_to_abi(u, 1, p.model.channels(), p.grid.steps)
+    fm, gm = C.c_double(), C.c_double()
+    err = _err()
+    _check(lib().oracle_verify_decomposition(packed.ref, abi.dptr(u_in), C.c_int32(parts), C.byref(fm),
+                                             C.byref(gm), C.c_int32(arith), err, C.c_size_t(512)), err)
+    return fm.value, gm.value
+
+
+def boundary_sweep(p, u, nodes, arith=STRUCTURED):
+    packed = I.pack_problem(p)
+    d = p.model.state_dim()
+    u_in = I.controls_to_abi(u, 1, p.model.channels(), p.grid.steps)
+    L = len(nodes) - 1
+    ni = np.ascontiguousarray(nodes, dtype=np.int32)
+    ps = np.empty(2 * (L + 1) * d)
+    cs = np.empty(2 * (L + 1) * d)
+    err = _err()
+    _check(lib().oracle_boundary_sweep(packed.ref, abi.dptr(u_in), C.c_int32(L), abi.iptr(ni), abi.dptr(ps),
+                                       abi.dptr(cs), C.c_int32(arith), err, C.c_size_t(512)), err)
+    return ps.view(np.complex128).reshape(L + 1, d), cs.view(np.complex128).reshape(L + 1, d)
+
+
+def dense_fixture(seed, dim=4, steps=16, channels=2, quadratic=False, alpha=0.1, duration=1.0,
+                  control_amplitude=0.8, random_penalty=False):
+    """fixtures::dense_fixture (fixtures.hpp:66-112), vector kind, same mt19937 draws."""
+    dd = dim * dim
+    h0 = np.empty(2 * dd)
+    lin = np.empty(2 * dd * channels)
+    quad = np.empty(2 * dd * channels) if quadratic else np.empty(2)
+    ini, tgt = np.empty(2 * dim), np.empty(2 * dim)
+    pen = np.empty(steps)
+    ctl = np.empty(channels * steps)
+    lib().oracle_dense_fixture(C.c_uint32(seed), dim, steps, channels, int(quadratic), C.c_double(alpha),
+                               int(random_penalty), C.c_double(control_amplitude), abi.dptr(h0),
+                               abi.dptr(lin), abi.dptr(quad), abi.dptr(ini), abi.dptr(tgt),
+                               abi.dptr(pen), abi.dptr(ctl))
+
+    def mats(buf, n):
+        return np.swapaxes(buf.view(np.complex128).reshape(n, dim, dim), 1, 2)
+
+    from paper_1603_01237_b200.models import DenseModel
+    model = DenseModel(mats(h0, 1)[0], mats(lin, channels), mats(quad, channels) if quadratic else None)
+    grid = I.TimeGrid.over(0.0, duration, steps)
+    problem = I.ControlProblem(model, grid, ini.view(np.complex128).copy(), tgt.view(np.complex128).copy(),
+                               pen)
+    control = ctl.reshape(steps, channels).T.copy()
+    return problem, control
+
+
+def strang_fixture(seed, points=24, x_min=-8.0, x_max=8.0, distance=6.0, kappa=1.0, steps=12,
+                   duration=0.5, alpha=0.05, control_amplitude=0.9):
+    """fixtures::strang_fixture (fixtures.hpp:208-234)."""
+    from paper_1603_01237_b200.models import CondensateModel
+    ini, tgt, ctl = np.empty(2 * points), np.empty(2 * points), np.empty(steps)
+    lib().oracle_strang_fixture(C.c_uint32(seed), points, C.c_double(x_min), C.c_double(x_max), steps,
+                                C.c_double(control_amplitude), abi.dptr(ini), abi.dptr(tgt), abi.dptr(ctl))
+    model = CondensateModel(points, x_min, x_max, abi.POT_TRAP, [distance], kappa)
+    grid = I.TimeGrid.over(0.0, duration, steps)
+    problem = I.ControlProblem(model, grid, ini.view(np.complex128).copy(), tgt.view(np.complex128).copy(),
+                               np.full(steps, alpha))
+    return problem, ctl.reshape(1, steps)
+
+
+class Rng:
+    """std::mt19937-driven draws of the reference tests (random_cvec/state/hermitian)."""
+
+    def __init__(self, seed):
+        self.buf = C.create_string_buffer(5000)
+        self.seed = seed
+        self.fresh = True
+
+    def _draw(self, what, n, scale, size):
+        out = np.empty(2 * size)
+        lib().oracle_rng(self.buf, int(self.fresh), C.c_uint32(self.seed), what, n, C.c_double(scale),
+                         abi.dptr(out))
+        self.fresh = False
+        return out.view(np.complex128).copy()
+
+    def cvec(self, n):
+        return self._draw(0, n, 1.0, n)
+
+    def state(self, n):
+        return self._draw(1, n, 1.0, n)
+
+    def hermitian(self, n, scale=1.0):
+        return self._draw(2, n, scale, n * n).reshape(n, n).T.copy()

@@ -1,0 +1,68 @@
+"""Device parity, dense operators: libqoc_b200.so vs the CPU oracle on the reference's own
+seeded fixtures (fixtures.hpp:66-112) and BASELINE config 1."""
+import numpy as np
+import pytest
+
+from paper_1603_01237_b200 import ism as I
+from paper_1603_01237_b200 import problems
+from tests import oracle_api as O
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)
+
+
+@pytest.mark.parametrize("quad", [False, True])
+@pytest.mark.parametrize("dim", [2, 4, 7, 16, 21])
+def test_propagate_gradient_assemble(ctx, quad, dim):
+    p, u = O.dense_fixture(100 + dim + 2 * quad, dim=dim, steps=16, quadratic=quad, random_penalty=True)
+    fin = I.propagate_final(p, u, ctx)
+    ref = O.propagate_final(p, u, O.REFERENCE)
+    assert np.max(np.abs(fin - ref)) < 1e-13
+    for form in ("overlap", "tracking"):
+        v, g = I.objective_gradient(p, u, form, ctx=ctx)
+        vr, gr = O.objective_gradient(p, u, form, arith=O.REFERENCE)
+        assert abs(v[0] - vr[0]) < 1e-13
+        assert np.max(np.abs(g - gr)) < 1e-13
+    M = I.assemble_propagator(p, u, ctx)
+    Mr = O.assemble_propagator(p, u, O.REFERENCE)
+    assert np.max(np.abs(M - Mr)) < 1e-13
+
+
+@pytest.mark.parametrize("parts", [1, 2, 4, 8, 5])
+@pytest.mark.parametrize("plan", ["assembled", "direct"])
+def test_run_ism_matches_oracle(ctx, parts, plan):
+    p, u = O.dense_fixture(2600, random_penalty=True)
+    cfg = I.IsmConfig(subintervals=parts, max_outer=5, eta=0.0, plan=plan)
+    sv = I.SolverSpec(step_size=0.5)
+    g = I.run_ism(p, u, cfg, sv, ctx)
+    r = O.ism_run(p, u, cfg, sv, O.REFERENCE)[0]
+    assert np.max(np.abs(g.control - r.control)) < 1e-12
+    assert len(g.record.iterations) == len(r.record.iterations) == 6
+    for a, b in zip(g.record.iterations, r.record.iterations):
+        assert a.iteration == b.iteration
+        assert abs(a.objective - b.objective) < 1e-12
+        assert (a.error is None) == (b.error is None)
+        if a.error is not None:
+            assert abs(a.error - b.error) < 1e-11 * max(1.0, abs(b.error))
+        assert np.max(np.abs(np.array(a.task_values) - np.array(b.task_values))) < 1e-12
+
+
+def test_spin2_200_iterations(ctx):
+    for rho in (0.1, 10.0):
+        w = problems.spin2(rho=rho)
+        g = I.run_ism(w.problem, w.u0, w.config, w.solver, ctx)
+        r = O.ism_run(w.problem, w.u0, w.config, w.solver, O.REFERENCE)[0]
+        assert rel(g.control, r.control) < 1e-9
+        assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-10
+
+
+def test_batch_subset(ctx):
+    w = problems.batch4096(batch=8, iterations=3)
+    gs = I.run_ism_batch(w.problem, w.u0, w.config, w.solver, ctx)
+    rs = O.ism_run(w.problem, w.u0, w.config, w.solver, O.REFERENCE)
+    for g, r in zip(gs, rs):
+        assert rel(g.control, r.control) < 1e-11
+        assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-11
