@@ -125,6 +125,7 @@ struct DevRun {
   double* rec_tv;       // [B][cap][L]
   int* rec_flags;       // [B][cap] bit 1 = has error, bit 2 = has exact objective
   double* tot_err;      // [B] summed task residual of the current iteration
+  int* err_flags;       // [1] bit 1: a structured solve would have needed pivoting
   int cap;
 };
 

@@ -312,6 +312,8 @@ void alloc_run(const DeviceProblem& dp, int cap, const std::vector<int>& node, b
   R.rec_exact = out.alloc<double>(B * cap);
   R.rec_tv = out.alloc<double>(B * cap * L);
   R.rec_flags = out.alloc<int>(B * cap);
+  R.err_flags = out.alloc<int>(1);
+  ck(cudaMemsetAsync(R.err_flags, 0, sizeof(int), st), "memset");
   ck(cudaMemsetAsync(R.done, 0, sizeof(int) * B, st), "memset");
   ck(cudaMemsetAsync(R.status, 0, sizeof(int) * B, st), "memset");
   ck(cudaMemsetAsync(R.abort_iter, 0, sizeof(int) * B, st), "memset");
@@ -346,6 +348,14 @@ cudaError_t horizon(const DevProblem& P, const DevRun& R, int which, int k, cuda
     case QOC_KIND_STRANG: return strang_horizon(P, R, which, k, st);
   }
   return cudaErrorInvalidValue;
+}
+
+void check_flags(const DevRun& R) {
+  int flags = 0;
+  ck(cudaMemcpy(&flags, R.err_flags, sizeof(int), cudaMemcpyDeviceToHost), "flags");
+  if (flags & 1)
+    fail(QOC_ERUNTIME, "tridiagonal Cayley solve would need a row interchange (dt/2 |H| too large for the "
+                       "structured kind); use QOC_KIND_DENSE");
 }
 
 struct Launcher {
@@ -504,6 +514,7 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
         launch(trailing_values(P, R, st), "trailing");
       }
       ck(cudaStreamSynchronize(st), "run");
+      check_flags(R);
 
       // ---- download
       std::vector<int> n_recs(B), stat(B), abort_iter(B), flags((size_t)B * rec_cap);
@@ -571,6 +582,7 @@ void single_run(qoc_ctx* ctx, const qoc_problem_v1* p, const double* u, int mode
   TaskArgs A{mode, form, 0, 1, 0.0};
   launch(task(dp.P, dr.R, A, 0, st), "task");
   ck(cudaStreamSynchronize(st), "run");
+  check_flags(dr.R);
 }
 }  // namespace
 
