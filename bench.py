@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""bench.py -- ISM hot path (arXiv 1603.01237) on B200: propagation steps/s.
+
+One "step" is one ISM outer iteration over the whole workload: every subinterval task's
+forward sweep, adjoint sweep with the fused gradient + control update, residual sweeps and
+propagator assembly, then the boundary chain and waypoint rebuild (ism.cpp:396-592).
+metric = 2 * K * B * iterations / seconds: one forward and one adjoint
+single-state step per grid step, B independent problems.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload NAME]
+
+Default workload = BASELINE.json configs[1]: the rotor j<=20 (d = 21, tridiagonal), K = 20000,
+L = 128 (32 x 157 + 96 x 156 steps), rho = 0.1/dt.  N > 1 runs N independent replicas of it
+(the path is one small latency-bound problem: "replicas only"); batch4096 shards its
+problems over the ranks instead.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "propagation steps/s (fwd+adjoint, all subintervals); time-to-fidelity 0.999"
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2: every timed iteration starts cold
+
+
+def flops_per_iteration(name: str, w) -> float:
+    """Algorithmic fp64 flops of one outer iteration (SURVEY.md §8(d) model, '+err' variant:
+    forward + adjoint/gradient + assembly + residual forward/adjoint per grid step)."""
+    p = w.problem
+    d, C, K, B = p.model.state_dim(), p.model.channels(), p.grid.steps, p.batch
+    if name == "rotor21":  # tridiagonal: W_tri = 64d, W_g = 24d, W_asm = 41d^2 + 23d
+        per = 4 * 64 * d + 2 * 24 * d + 41 * d * d + 23 * d
+    elif name in ("spin2", "batch4096"):  # dense Cayley
+        w_cay = (8 / 3) * d ** 3 + (4 * C + 20) * d ** 2
+        w_bg = w_cay + 4 * d + C * (8 * d ** 2 + 8 * d)
+        w_asm = (56 / 3) * d ** 3 + (4 * C + 4) * d ** 2
+        per = 2 * w_cay + 2 * w_bg + w_asm
+    else:
+        return float("nan")
+    return per * K * B
+
+
+def fp64_peak():
+    f = ROOT / "profiles" / "fp64_peak.json"
+    if f.exists():
+        j = json.loads(f.read_text())
+        return j["fp64_fma_tflops"], "measured (tools/fp64_peak.cu, profiles/fp64_peak.json)"
+    return 37.2, "nominal 148 SM x 64 DFMA x 2 x 1.965 GHz (no measurement found)"
+
+
+def ncu_traffic(name: str):
+    f = ROOT / "profiles" / f"ncu_{name}.json"
+    if f.exists():
+        j = json.loads(f.read_text())
+        return j.get("dram_bytes_per_launch")
+    return None
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.tmp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.tmp, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        self.tmp.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.tmp.read().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_workload(name: str, iterations: int, rank: int, world: int, rho_fast: bool = True):
+    from paper_1603_01237_b200 import problems
+    if name == "rotor21":
+        w = problems.rotor21(subintervals=128, iterations=iterations)
+    elif name == "spin2":
+        w = problems.spin2(iterations=iterations)
+    elif name == "batch4096":
+        per = 4096 // world
+        w = problems.batch4096(batch=per, iterations=iterations, first=rank * per)
+    elif name == "ising10":
+        w = problems.ising10(iterations=iterations)
+    elif name == "gpe1024":
+        w = problems.gpe1024(iterations=iterations)
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    if rho_fast:
+        w.solver.step_size = w.rho_fast
+    return w
+
+
+def problem_bytes(w) -> int:
+    from paper_1603_01237_b200 import ism as I
+    packed = I.pack_problem(w.problem)
+    return int(sum(a.nbytes for a in packed.keep)) + int(np.asarray(w.u0).nbytes)
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl")
+        else:
+            dist.init_process_group("gloo")
+    return world, rank, local, dist
+
+
+def allmax(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allsum(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+def barrier_sync(dist):
+    try:
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+    except ImportError:
+        pass
+    if dist is not None:
+        dist.barrier()
+
+
+def cpu_reference(name: str, warmup: int, steps: int, sample_iters: int | None = None):
+    """The reference's CPU path: the oracle restatement with reference arithmetic (dense
+    partial-pivot LU per step, like Eigen::PartialPivLU in propagation.cpp:85-106) on all host
+    threads, as WorkerPool does (runtime.cpp:72-90)."""
+    from tests import oracle_api as O
+    from paper_1603_01237_b200 import problems
+    threads = os.cpu_count() or 1
+    if name == "batch4096":
+        sample_b = 16
+        w = problems.batch4096(batch=sample_b, iterations=warmup + steps)
+        desc = f"{sample_b} of 4096 problems (d=16, K=2000, L=128)"
+    else:
+        w = build_workload(name, warmup + steps, 0, 1)
+        desc = f"full {name} workload"
+    if name == "rotor21":  # the reference builds the rotor as a dense model (models.cpp:361-399)
+        from paper_1603_01237_b200.models import TridiagonalModel
+        assert isinstance(w.problem.model, TridiagonalModel)
+        w.problem.model = w.problem.model.to_dense()
+    w.solver.step_size = w.rho_fast
+    w.config.max_outer = warmup + steps
+    t0 = time.perf_counter()
+    runs = O.ism_run(w.problem, w.u0, w.config, w.solver, O.REFERENCE, threads=threads)
+    wall = time.perf_counter() - t0
+    its = runs[0].record.iterations
+    secs = sum(it.device_seconds for it in its[warmup + 1:warmup + steps + 1])
+    p = w.problem
+    work = 2.0 * p.grid.steps * p.batch * steps
+    return {"value": work / secs, "unit": "steps/s", "cores": threads, "kind": "port",
+            "sample": f"{desc}; {steps} timed outer iterations after {warmup} warm-up, dense-LU "
+                      f"reference arithmetic, {threads} threads",
+            "seconds": secs, "wall": wall}
+
+
+def run_reference_arm(args, world, rank, dist):
+    if rank != 0:
+        return 0
+    ref = cpu_reference(args.workload, args.warmup, args.steps)
+    line = {"metric": METRIC, "value": ref["value"], "unit": "steps/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * ref["seconds"] / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload},
+            "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": ref["value"], "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="rotor21",
+                    choices=["rotor21", "spin2", "batch4096", "ising10", "gpe1024"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local, dist = dist_setup()
+    if args.impl == "reference":
+        return run_reference_arm(args, world, rank, dist)
+
+    from paper_1603_01237_b200 import _native, abi
+    from paper_1603_01237_b200 import ism as I
+    from paper_1603_01237_b200 import problems
+
+    K_, W_ = args.steps, args.warmup
+    ctx = _native.default_context(local)
+    w = build_workload(args.workload, W_ + K_, rank, world)
+    p = w.problem
+    # untimed first call (context, module load)
+    w1 = build_workload(args.workload, 1, rank, world)
+    I.run_ism_batch(w1.problem, w1.u0, w1.config, w1.solver, ctx)
+
+    # ---- timed: W warm-up + K timed outer iterations inside one run; per-iteration CUDA events
+    ctx.set_option(abi.OPT_PROFILE, 1)
+    ctx.set_option(abi.OPT_FLUSH_L2_BYTES, L2_FLUSH_BYTES)
+    ctx.profile(reset=True)
+    barrier_sync(dist)
+    with Clocks(local) as clk:
+        runs = I.run_ism_batch(p, w.u0, w.config, w.solver, ctx)
+        barrier_sync(dist)
+    prof = ctx.profile(reset=True)
+    ctx.set_option(abi.OPT_PROFILE, 0)
+    its = runs[0].record.iterations
+    timed = its[W_ + 1:W_ + K_ + 1]
+    assert len(timed) == K_, "run stopped early"
+    t_rank = sum(it.device_seconds for it in timed)
+    t_max = allmax(dist, t_rank)
+    work_rank = 2.0 * p.grid.steps * p.batch * K_
+    work = allsum(dist, work_rank)
+    value = work / t_max
+    launches_per_iter = prof["iteration_launches"] / max(prof["iterations"], 1)
+
+    # ---- roofline of the dominant kernel (per-subinterval task kernel)
+    task_ms = prof["task_ms"] / max(prof["task_launches"], 1)
+    fl = flops_per_iteration(args.workload, w)
+    peak, peak_src = fp64_peak()
+    achieved = fl / (task_ms * 1e-3) / 1e12 if task_ms > 0 else float("nan")
+
+    # ---- end to end through the public API: host buffers in, host results out
+    ctx.set_option(abi.OPT_FLUSH_L2_BYTES, 0)
+    we = build_workload(args.workload, K_, rank, world)
+    barrier_sync(dist)
+    t0 = time.perf_counter()
+    e2e_runs = I.run_ism_batch(we.problem, we.u0, we.config, we.solver, ctx)
+    barrier_sync(dist)
+    e2e_wall = allmax(dist, time.perf_counter() - t0)
+    e2e_value = allsum(dist, 2.0 * we.problem.grid.steps * we.problem.batch * K_) / e2e_wall
+    h2d = problem_bytes(we)
+    d2h = int(np.asarray(e2e_runs[0].control).nbytes * len(e2e_runs)
+              + (K_ + 1) * (abi.REC_DTYPE.itemsize + 8 * we.config.subintervals) * len(e2e_runs))
+
+    # ---- time to fidelity 0.999 (rho = 0.1/dt), device time summed over iterations
+    ttf = None
+    if args.workload in ("rotor21", "spin2", "batch4096") and rank == 0:
+        wt = build_workload(args.workload, 300, 0, 1)
+        if args.workload == "batch4096":
+            wt = problems.batch4096(batch=64, iterations=300)
+            wt.solver.step_size = wt.rho_fast
+        rr = I.run_ism_batch(wt.problem, wt.u0, wt.config, wt.solver, ctx)
+        r0 = rr[0]
+        F = 1.0 + r0.record.objectives()
+        hit = np.nonzero(F >= 0.999)[0]
+        if len(hit):
+            k = int(hit[0])
+            ttf = {"target": 0.999, "iterations": k,
+                   "seconds": float(sum(it.device_seconds for it in r0.record.iterations[:k + 1])),
+                   "rho": wt.solver.step_size, "problem": "problem 0 of 64" if args.workload == "batch4096" else args.workload}
+        else:
+            ttf = {"target": 0.999, "iterations": None, "reached": False, "rho": wt.solver.step_size}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ref = cpu_reference(args.workload, 0, 2)
+        cpu = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        if ttf and ttf.get("iterations"):
+            ttf["cpu_seconds_est"] = ttf["iterations"] * ref["seconds"] / 2 * (
+                4096 / 16 if args.workload == "batch4096" else 1)
+
+    if rank != 0:
+        return 0
+    desc = problems.describe(w)
+    cfg = {"workload": args.workload, "dim": desc["dim"], "channels": desc["channels"],
+           "grid_steps": desc["steps"], "subintervals": desc["subintervals"], "partition": desc["partition"],
+           "batch_per_gpu": p.batch, "step_size": w.solver.step_size, "variant": desc["variant"],
+           "plan": desc["plan"], "parallelism": f"{'batch shards' if args.workload == 'batch4096' else 'replicas'} x{world}",
+           "l2": "flushed between timed iterations (256 MiB memset outside the event brackets)"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": K_, "warmup": W_,
+        "ms_per_step": 1e3 * t_max / K_, "higher_is_better": True,
+        "scaling": "strong" if args.workload == "batch4096" else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d))", "config": cfg,
+        "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": h2d // K_,
+                "d2h_bytes_per_step": d2h // K_, "note": "one run_ism call of K outer iterations from pageable "
+                "host arrays, wall clock incl. upload, bootstrap, trailing evaluation and download"},
+        "gpu_launches": int(round(launches_per_iter * K_)),
+        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(args.workload),
+                     "kernel": "task kernel (per-subinterval sweeps)", "kernel_ms": task_ms,
+                     "flops_per_launch": fl, "peak_source": peak_src,
+                     "share_of_step": prof["task_ms"] / max(prof["task_ms"] + prof["other_ms"], 1e-12)},
+        "time_to_fidelity": ttf,
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -209,6 +209,27 @@ int32_t qoc_assemble_propagator(qoc_ctx* ctx, const qoc_problem_v1* problem, con
 /* Kernel-launch counter of this context (for the bench's gpu_launches claim). */
 int64_t qoc_ctx_launch_count(const qoc_ctx* ctx);
 
+/* Context options.
+ *   QOC_OPT_PROFILE        1 = bracket every kernel launch of qoc_ism_run with CUDA events on
+ *                          the launching stream and accumulate them into qoc_profile_v1.
+ *   QOC_OPT_FLUSH_L2_BYTES >0 = overwrite that many bytes of scratch between outer iterations
+ *                          (outside the per-iteration event brackets) so every iteration
+ *                          starts with a cold L2. */
+enum qoc_ctx_option { QOC_OPT_PROFILE = 1, QOC_OPT_FLUSH_L2_BYTES = 2 };
+int32_t qoc_ctx_set_option(qoc_ctx* ctx, int32_t option, int64_t value);
+
+/* Device-time totals since the last reset (CUDA events on the context stream). */
+typedef struct qoc_profile_v1 {
+  int64_t task_launches;   /* per-subinterval task kernels (the dominant kernel) */
+  double task_ms;
+  int64_t other_launches;  /* coordinator kernels (merge, chain, boundary, ...) */
+  double other_ms;
+  int64_t iterations;      /* outer iterations run */
+  double iteration_ms;     /* summed per-iteration device time (L2 flush excluded) */
+  int64_t iteration_launches; /* kernel launches inside the outer iterations */
+} qoc_profile_v1;
+int32_t qoc_ctx_profile(qoc_ctx* ctx, qoc_profile_v1* out, int32_t reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -38,6 +38,10 @@ def lib():
         L.qoc_ctx_last_error.restype = C.c_char_p
         L.qoc_ctx_launch_count.argtypes = [vp]
         L.qoc_ctx_launch_count.restype = C.c_int64
+        L.qoc_ctx_set_option.argtypes = [vp, i32, C.c_int64]
+        L.qoc_ctx_set_option.restype = i32
+        L.qoc_ctx_profile.argtypes = [vp, C.POINTER(abi.ProfileV1), i32]
+        L.qoc_ctx_profile.restype = i32
         L.qoc_ism_run.argtypes = [vp, vp, vp, vp, dp, dp, vp, i32, dp, vp]
         L.qoc_ism_run.restype = i32
         L.qoc_propagate_final.argtypes = [vp, vp, dp, dp]
@@ -71,6 +75,15 @@ class Context:
 
     def launches(self) -> int:
         return int(self.lib.qoc_ctx_launch_count(self.handle))
+
+    def set_option(self, option: int, value: int) -> None:
+        if self.lib.qoc_ctx_set_option(self.handle, option, int(value)) != abi.QOC_OK:
+            raise RuntimeError(f"qoc_ctx_set_option({option}, {value}) failed")
+
+    def profile(self, reset: bool = False) -> dict:
+        p = abi.ProfileV1()
+        self.lib.qoc_ctx_profile(self.handle, C.byref(p), int(reset))
+        return {f: getattr(p, f) for f, _ in abi.ProfileV1._fields_}
 
     def close(self):
         if self.handle:

@@ -72,6 +72,15 @@ class RunStatusV1(C.Structure):
                 ("abort_reason", C.c_char * 240)]
 
 
+class ProfileV1(C.Structure):
+    _fields_ = [("task_launches", C.c_int64), ("task_ms", C.c_double), ("other_launches", C.c_int64),
+                ("other_ms", C.c_double), ("iterations", C.c_int64), ("iteration_ms", C.c_double),
+                ("iteration_launches", C.c_int64)]
+
+
+OPT_PROFILE, OPT_FLUSH_L2_BYTES = 1, 2
+
+
 class CtxOptsV1(C.Structure):
     _fields_ = [("abi_version", C.c_int32), ("device", C.c_int32), ("reserved", C.c_int32 * 6)]
 

@@ -126,6 +126,11 @@ struct DevRun {
   int* rec_flags;       // [B][cap] bit 1 = has error, bit 2 = has exact objective
   double* tot_err;      // [B] summed task residual of the current iteration
   int* err_flags;       // [1] bit 1: a structured solve would have needed pivoting
+  // propagator-cache engine (pcache.cu)
+  double2* pc;          // [B][L][traj_len][d][d] partial products P_j (row-major)
+  double* chunk_pen;    // [B][L][nchunk]
+  double* chunk_err;    // [B][L][nchunk]
+  double* entry_pay;    // [B][L]
   int cap;
 };
 

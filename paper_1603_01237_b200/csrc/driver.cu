@@ -16,6 +16,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/qoc_gpu.h"
@@ -28,6 +29,12 @@ struct qoc_ctx {
   cudaStream_t stream = nullptr;
   std::string last_error;
   int64_t launches = 0;
+  bool profile = false;
+  int64_t flush_bytes = 0;
+  void* flush_buf = nullptr;
+  qoc_profile_v1 prof{};
+  // event pairs of the current run: (start, stop, is_task)
+  std::vector<std::tuple<cudaEvent_t, cudaEvent_t, bool>> marks;
 };
 
 namespace {
@@ -279,8 +286,24 @@ struct DeviceRun {
   }
 };
 
+// Bytes of the propagator cache (pcache.cu) for a run, or 0 when the engine does not apply.
+size_t pc_bytes(const DevProblem& P, const std::vector<int>& node) {
+  if (!(P.kind == QOC_KIND_DENSE || (P.kind == QOC_KIND_TRIDIAG && P.d <= 30)) || P.d > 32) return 0;
+  int maxlen = 0;
+  for (size_t n = 0; n + 1 < node.size(); ++n) maxlen = std::max(maxlen, node[n + 1] - node[n]);
+  return sizeof(double2) * (size_t)P.B * P.L * (maxlen + 1) * P.d * P.d;
+}
+
+bool use_pcache(const DevProblem& P, const std::vector<int>& node) {
+  const size_t need = pc_bytes(P, node);
+  if (!need) return false;
+  size_t freeb = 0, total = 0;
+  if (cudaMemGetInfo(&freeb, &total) != cudaSuccess) return false;
+  return need < freeb / 10 * 7;
+}
+
 void alloc_run(const DeviceProblem& dp, int cap, const std::vector<int>& node, bool need_prop, bool need_grad,
-               cudaStream_t st, DeviceRun& out) {
+               cudaStream_t st, DeviceRun& out, bool with_pc = false) {
   const DevProblem& P = dp.P;
   DevRun& R = out.R;
   const size_t B = P.B, L = P.L, d = P.d, K = P.K, C = P.C;
@@ -313,6 +336,13 @@ void alloc_run(const DeviceProblem& dp, int cap, const std::vector<int>& node, b
   R.rec_tv = out.alloc<double>(B * cap * L);
   R.rec_flags = out.alloc<int>(B * cap);
   R.err_flags = out.alloc<int>(1);
+  if (with_pc) {
+    R.pc = out.alloc<double2>(pc_bytes(P, node) / sizeof(double2));
+    const int nchunk = pc_nchunk(P, R);
+    R.chunk_pen = out.alloc<double>(B * L * nchunk);
+    R.chunk_err = out.alloc<double>(B * L * nchunk);
+    R.entry_pay = out.alloc<double>(B * L);
+  }
   ck(cudaMemsetAsync(R.err_flags, 0, sizeof(int), st), "memset");
   ck(cudaMemsetAsync(R.done, 0, sizeof(int) * B, st), "memset");
   ck(cudaMemsetAsync(R.status, 0, sizeof(int) * B, st), "memset");
@@ -358,14 +388,52 @@ void check_flags(const DevRun& R) {
                        "structured kind); use QOC_KIND_DENSE");
 }
 
+// Launch wrapper: counts launches and, when profiling, brackets each launch with events.
 struct Launcher {
   qoc_ctx* ctx;
-  void operator()(cudaError_t e, const char* what) {
+  bool in_iteration = false;
+  template <class F>
+  void run(F&& f, const char* what, bool is_task = false) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (ctx->profile) {
+      ck(cudaEventCreate(&a), "event");
+      ck(cudaEventCreate(&b), "event");
+      ck(cudaEventRecord(a, ctx->stream), "event");
+    }
+    const cudaError_t e = f();
+    ++ctx->launches;
+    if (in_iteration) ++ctx->prof.iteration_launches;
+    if (ctx->profile) {
+      ck(cudaEventRecord(b, ctx->stream), "event");
+      ctx->marks.emplace_back(a, b, is_task);
+    }
+    if (e == cudaErrorNotSupported) fail(QOC_ELOGIC, std::string(what) + ": not supported for this model kind");
+    ck(e, what);
+  }
+  void operator()(cudaError_t e, const char* what) {  // already-launched form (no timing)
     ++ctx->launches;
     if (e == cudaErrorNotSupported) fail(QOC_ELOGIC, std::string(what) + ": not supported for this model kind");
     ck(e, what);
   }
 };
+
+void harvest_marks(qoc_ctx* ctx) {
+  for (auto& [a, b, is_task] : ctx->marks) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, a, b) == cudaSuccess) {
+      if (is_task) {
+        ctx->prof.task_ms += ms;
+        ++ctx->prof.task_launches;
+      } else {
+        ctx->prof.other_ms += ms;
+        ++ctx->prof.other_launches;
+      }
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  ctx->marks.clear();
+}
 
 template <class F>
 int32_t guarded(qoc_ctx* ctx, F&& f) {
@@ -415,7 +483,35 @@ void qoc_ctx_destroy(qoc_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->flush_buf) cudaFree(ctx->flush_buf);
   delete ctx;
+}
+
+int32_t qoc_ctx_set_option(qoc_ctx* ctx, int32_t option, int64_t value) {
+  if (!ctx) return QOC_EINVAL;
+  cudaSetDevice(ctx->device);
+  if (option == QOC_OPT_PROFILE) {
+    ctx->profile = value != 0;
+    return QOC_OK;
+  }
+  if (option == QOC_OPT_FLUSH_L2_BYTES) {
+    if (ctx->flush_buf) cudaFree(ctx->flush_buf);
+    ctx->flush_buf = nullptr;
+    ctx->flush_bytes = 0;
+    if (value > 0) {
+      if (cudaMalloc(&ctx->flush_buf, (size_t)value) != cudaSuccess) return QOC_ECUDA;
+      ctx->flush_bytes = value;
+    }
+    return QOC_OK;
+  }
+  return QOC_EINVAL;
+}
+
+int32_t qoc_ctx_profile(qoc_ctx* ctx, qoc_profile_v1* out, int32_t reset) {
+  if (!ctx) return QOC_EINVAL;
+  if (out) *out = ctx->prof;
+  if (reset) ctx->prof = qoc_profile_v1{};
+  return QOC_OK;
 }
 
 const char* qoc_ctx_last_error(const qoc_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
@@ -448,7 +544,8 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
     upload_problem(p, node, st, dp);
     const DevProblem& P = dp.P;
     DeviceRun dr;
-    alloc_run(dp, rec_cap, node, assembled_interp, false, st, dr);
+    const bool pcache = use_pcache(P, node);
+    alloc_run(dp, rec_cap, node, assembled_interp, false, st, dr, pcache);
     const DevRun& R = dr.R;
     ck(cudaMemcpyAsync(R.u, u0, sizeof(double) * B * K * C, cudaMemcpyHostToDevice, st), "u0");
 
@@ -461,10 +558,13 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
     try {
       ck(cudaEventRecord(ev[0], st), "event");
       // ---- bootstrap (ism.cpp:344-393)
+      if (pcache) launch(pc_assemble(P, R, 0, st), "propagator cache");
       if (L > 1) {
         if (assembled_interp) {
-          TaskArgs A{M_ASSEMBLE, QOC_FORM_TRACKING, 1, 1, 0.0};
-          launch(task(P, R, A, 0, st), "assemble");
+          if (!pcache) {
+            TaskArgs A{M_ASSEMBLE, QOC_FORM_TRACKING, 1, 1, 0.0};
+            launch(task(P, R, A, 0, st), "assemble");
+          }
           launch(chain_propagators(P, R, st), "chain");
         } else {
           launch(horizon(P, R, 0, 0, st), "node sweeps");
@@ -483,20 +583,47 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
       if (L > 1 && split && !direct) mode |= M_LAGGED;
       TaskArgs A{mode, form, split ? 0 : 1, std::max(0, solver->inner_iterations), solver->step_size};
       std::vector<int> h_done(B), h_status(B);
+      std::vector<cudaEvent_t> ev_end(max_outer + 2);
+      for (auto& e : ev_end) ck(cudaEventCreate(&e), "event");
       int ran = 0;
+      launch.in_iteration = true;
       for (int k = 1; k <= max_outer; ++k) {
-        launch(task(P, R, A, 0, st), "task");
-        launch(penalty_partials(P, R, 0, st), "penalty");
-        launch(merge_iteration(P, R, k, nullptr, st), "merge");
-        if (L > 1) {
-          if (direct) launch(horizon(P, R, 0, k, st), "node sweeps");
-          else if (split) launch(split_nodes(P, R, st), "split nodes");
-          else launch(chain_propagators(P, R, st), "chain");
-          launch(boundary_update(P, R, k, split, 0, st), "boundary");
+        if (ctx->flush_bytes > 0) {  // cold L2 for every iteration, outside the brackets
+          ck(cudaMemsetAsync(ctx->flush_buf, k & 0xff, (size_t)ctx->flush_bytes, st), "flush");
+          ck(cudaEventRecord(ev[k], st), "event");
         }
-        if (cfg->log_exact_objective) launch(horizon(P, R, 1, k, st), "exact objective");
-        launch(finish_iteration_ex(P, R, k, cfg->compute_error, cfg->eta, cfg->log_exact_objective, st), "finish");
-        ck(cudaEventRecord(ev[k + 1], st), "event");
+        if (pcache) {
+          // gradient + update through the cache, then the assembly sweep at the new control,
+          // then residual / lagged endpoints through the new cache
+          const TaskArgs G{PCM_ENTRY | PCM_GRAD, form, split ? 0 : 1, 1, solver->step_size};
+          launch.run([&] { return pc_eval(P, R, G, 0, st); }, "gradient", true);
+          for (int it = 1; it < std::max(1, solver->inner_iterations); ++it) {
+            launch.run([&] { return pc_assemble(P, R, 0, st); }, "assembly", true);
+            const TaskArgs G2{PCM_GRAD, form, split ? 0 : 1, 1, solver->step_size};
+            launch.run([&] { return pc_eval(P, R, G2, 0, st); }, "gradient", true);
+          }
+          launch.run([&] { return pc_assemble(P, R, 0, st); }, "assembly", true);
+          const int em = (cfg->compute_error ? PCM_ERR : 0) | ((L > 1 && split && !direct) ? PCM_LAG : 0);
+          if (em) {
+            const TaskArgs E{em, form, split ? 0 : 1, 1, 0.0};
+            launch.run([&] { return pc_eval(P, R, E, 0, st); }, "residual", true);
+          }
+        } else {
+          launch.run([&] { return task(P, R, A, 0, st); }, "task", true);
+        }
+        launch.run([&] { return penalty_partials(P, R, 0, st); }, "penalty");
+        launch.run([&] { return merge_iteration(P, R, k, nullptr, st); }, "merge");
+        if (L > 1) {
+          if (direct) launch.run([&] { return horizon(P, R, 0, k, st); }, "node sweeps");
+          else if (split) launch.run([&] { return split_nodes(P, R, st); }, "split nodes");
+          else launch.run([&] { return chain_propagators(P, R, st); }, "chain");
+          launch.run([&] { return boundary_update(P, R, k, split, 0, st); }, "boundary");
+        }
+        if (cfg->log_exact_objective) launch.run([&] { return horizon(P, R, 1, k, st); }, "exact objective");
+        launch.run([&] { return finish_iteration_ex(P, R, k, cfg->compute_error, cfg->eta,
+                                                    cfg->log_exact_objective, st); }, "finish");
+        ck(cudaEventRecord(ev_end[k + 1], st), "event");
+        if (ctx->flush_bytes <= 0) ck(cudaEventRecord(ev[k + 1], st), "event");
         ran = k;
         if (k % 8 == 0 || k == max_outer) {  // early exit once every problem stopped
           ck(cudaMemcpyAsync(h_done.data(), R.done, sizeof(int) * B, cudaMemcpyDeviceToHost, st), "poll");
@@ -507,10 +634,16 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
           if (all) break;
         }
       }
+      launch.in_iteration = false;
       // ---- trailing evaluation (ism.cpp:594-609)
       {
-        TaskArgs T{M_ENTRY, form, split ? 0 : 1, 1, 0.0};
-        launch(task(P, R, T, 1, st), "trailing task");
+        if (pcache) {
+          const TaskArgs T{PCM_ENTRY, form, split ? 0 : 1, 1, 0.0};
+          launch(pc_eval(P, R, T, 1, st), "trailing task");
+        } else {
+          TaskArgs T{M_ENTRY, form, split ? 0 : 1, 1, 0.0};
+          launch(task(P, R, T, 1, st), "trailing task");
+        }
         launch(trailing_values(P, R, st), "trailing");
       }
       ck(cudaStreamSynchronize(st), "run");
@@ -531,7 +664,15 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
         ck(cudaMemcpy(task_values, R.rec_tv, sizeof(double) * (size_t)B * rec_cap * L, cudaMemcpyDeviceToHost),
            "task values");
       std::vector<float> secs(ran + 1, 0.f);
-      for (int k = 0; k <= ran; ++k) ck(cudaEventElapsedTime(&secs[k], ev[k], ev[k + 1]), "elapsed");
+      ck(cudaEventElapsedTime(&secs[0], ev[0], ev[1]), "elapsed");
+      for (int k = 1; k <= ran; ++k) {
+        // iteration k spans [ev[k], ev_end[k+1]] (the L2 flush, if any, precedes ev[k])
+        ck(cudaEventElapsedTime(&secs[k], ev[k], ev_end[k + 1]), "elapsed");
+        ctx->prof.iteration_ms += secs[k];
+      }
+      ctx->prof.iterations += ran;
+      harvest_marks(ctx);
+      for (auto& e : ev_end) cudaEventDestroy(e);
       for (int b = 0; b < B; ++b) {
         qoc_run_status_v1& s = status[b];
         std::memset(&s, 0, sizeof(s));
@@ -560,6 +701,7 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
       }
     } catch (...) {
       cudaStreamSynchronize(st);
+      harvest_marks(ctx);
       destroy_events();
       throw;
     }

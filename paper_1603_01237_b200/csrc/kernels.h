@@ -22,6 +22,12 @@ cudaError_t bitflip_horizon(const DevProblem& P, const DevRun& R, int which, int
 cudaError_t strang_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
 cudaError_t strang_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st);
 
+// propagator-cache engine for the linear kinds (d <= 32)
+int pc_nchunk(const DevProblem& P, const DevRun& R);
+cudaError_t pc_eval(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
+cudaError_t pc_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st);
+constexpr int PCM_ENTRY = 1, PCM_GRAD = 2, PCM_ERR = 4, PCM_LAG = 8, PCM_FINAL = 16, PCM_RAWGRAD = 32;
+
 // glue (kind independent)
 cudaError_t penalty_partials(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st);
 cudaError_t merge_iteration(const DevProblem& P, const DevRun& R, int k, double* tot_err, cudaStream_t st);

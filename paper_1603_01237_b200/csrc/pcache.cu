@@ -1,0 +1,401 @@
+// pcache.cu — propagator-cache engine for the linear kinds (DENSE, TRIDIAG; d <= 32), sm_100a.
+//
+// The reference evaluates each subinterval task with step-by-step sweeps: a forward sweep, an
+// adjoint sweep with the gradient (objective.cpp:38-89), a residual forward/adjoint pair and a
+// d-column assembly sweep (ism.cpp:401-479).  Every one of them is a dependent chain of len
+// Cayley steps.  This engine keeps, per task, the partial products of the one-step maps
+//     P_0 = I,  P_{j+1} = C_j P_j,   C_j = (I + L_j)^-1 (I - L_j)     (propagation.cpp:236-249)
+// and uses two exact identities of the discrete scheme:
+//   forward states   psi_j = P_j phi                                   (propagate, 184-192)
+//   adjoint states   chi_j = C_j^dag ... C_{len-1}^dag seed = P_j chi_0,  chi_0 = P_len^dag seed
+// (C_j is unitary because H(u_j) is Hermitian, so C_j^-dag = C_j).  Given the cache, the
+// entry value, gradient, residual and lagged endpoints are matvecs that are independent
+// across j; the only sequential chain per outer iteration is one assembly sweep at the
+// updated control, which the assembled plan needs for M_n = P_len anyway.
+//
+//   pc_eval_kernel      warp per (task, j-chunk): entry payoff, gradient + in-place ascent
+//                       update (optimizers.cpp:102-107), residual norm partials, lagged
+//                       endpoints, final state / raw gradient for the helper API.
+//   pc_finalize_kernel  index-order reduction of the chunk partials.
+//   dense_pc_assemble   lane group per task: in-register Gauss-Jordan inverse of B_j, then
+//                       P_{j+1} = 2 B_j^-1 P_j - P_j.
+//   tri_pc_assemble     warp per task, lane per column: Thomas elimination per column.
+#include "dense.cuh"
+#include "kernels.h"
+#include "qoc_gpu.h"
+
+namespace qoc {
+
+namespace {
+
+constexpr int PC_ENTRY = 1, PC_GRAD = 2, PC_ERR = 4, PC_LAG = 8, PC_FINAL = 16, PC_RAWGRAD = 32;
+
+template <int D>
+struct PcSmem {
+  double2 phi[D];
+  double2 chi0[D];
+  double2 vec[D];
+  double red[32];
+};
+
+// (dH/du_c ps)_i for this lane's row i, dense operators (row-major, global / L1).
+__device__ __forceinline__ double2 dense_dH_row(const DevProblem& P, int b, int c, double uc, int i,
+                                                const double2* ps_sh) {
+  const int d = P.d;
+  const double2* a = P.lin + (((size_t)b * P.C + c) * d + i) * d;
+  const double2* q = P.has_quad ? P.quad + (((size_t)b * P.C + c) * d + i) * d : nullptr;
+  double2 acc = cx(0.0, 0.0);
+  for (int k = 0; k < d; ++k) {
+    double2 m = a[k];
+    if (q) m = cx(fma(uc, q[k].x, m.x), fma(uc, q[k].y, m.y));
+    acc = cfma(m, ps_sh[k], acc);
+  }
+  return acc;
+}
+
+// Tridiagonal (dH/du_c ps)_i with neighbours by shuffle.
+__device__ __forceinline__ double2 tri_dH_row(const DevProblem& P, int b, int c, double uc, int i, double2 ps) {
+  const int d = P.d, C = P.C;
+  const int nops = 1 + C + (P.has_quad ? C : 0);
+  const double* dg = P.tri_diag + (size_t)b * nops * d;
+  const double2* sb = P.tri_sub + (size_t)b * nops * (d - 1);
+  const double2 up = shfl(ps, (i + 31) & 31);   // ps_{i-1}
+  const double2 dn = shfl(ps, (i + 1) & 31);    // ps_{i+1}
+  if (i >= d) return cx(0.0, 0.0);
+  double g = dg[(1 + c) * d + i];
+  if (P.has_quad) g = fma(uc, dg[(1 + C + c) * d + i], g);
+  double2 h = cx(g * ps.x, g * ps.y);
+  if (i > 0) {
+    double2 s = sb[(size_t)(1 + c) * (d - 1) + i - 1];
+    if (P.has_quad) {
+      const double2 qq = sb[(size_t)(1 + C + c) * (d - 1) + i - 1];
+      s = cx(fma(uc, qq.x, s.x), fma(uc, qq.y, s.y));
+    }
+    h = cfma(s, up, h);
+  }
+  if (i + 1 < d) {
+    double2 s = sb[(size_t)(1 + c) * (d - 1) + i];
+    if (P.has_quad) {
+      const double2 qq = sb[(size_t)(1 + C + c) * (d - 1) + i];
+      s = cx(fma(uc, qq.x, s.x), fma(uc, qq.y, s.y));
+    }
+    h = cfmaconj(s, dn, h);
+  }
+  return h;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// y_i = sum_k M[i][k] v_k (M row-major d x d, v in smem); lanes >= d return 0.
+__device__ __forceinline__ double2 matvec_row(const double2* M, int d, int i, const double2* v) {
+  double2 a = cx(0.0, 0.0), b = cx(0.0, 0.0);
+  if (i < d) {
+    const double2* r = M + (size_t)i * d;
+    int k = 0;
+    for (; k + 1 < d; k += 2) {
+      a = cfma(r[k], v[k], a);
+      b = cfma(r[k + 1], v[k + 1], b);
+    }
+    if (k < d) a = cfma(r[k], v[k], a);
+  }
+  return cadd(a, b);
+}
+// y_i = sum_k conj(M[k][i]) v_k
+__device__ __forceinline__ double2 matvec_adj_row(const double2* M, int d, int i, const double2* v) {
+  double2 a = cx(0.0, 0.0);
+  if (i < d)
+    for (int k = 0; k < d; ++k) a = cfmaconj(M[(size_t)k * d + i], v[k], a);
+  return a;
+}
+
+template <bool TRI>
+__global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, TaskArgs A, int chunk, int nchunk,
+                                                      int ignore_done) {
+  __shared__ PcSmem<32> sm_all[4];
+  const int b = blockIdx.y;
+  if (ignore_done ? R.status[b] : R.done[b]) return;
+  const int warp = threadIdx.x >> 5, i = threadIdx.x & 31;
+  const int item = blockIdx.x * 4 + warp;
+  if (item >= P.L * nchunk) return;
+  PcSmem<32>& S = sm_all[warp];
+  const int n = item / nchunk, ch = item % nchunk;
+  const int d = P.d, C = P.C, mode = A.mode;
+  const int node0 = P.node[n], len = P.node[n + 1] - node0;
+  const int j0 = ch * chunk;
+  const int j1 = min(len, j0 + chunk);
+  const double Kd = (double)P.K;
+  const double weight = A.weighted ? Kd / (double)len : 1.0;
+  const double scale = (double)len / Kd;
+  const double dt = P.dt, w = P.ip_w;
+  double* u = R.u + ((size_t)b * P.K + node0) * C;
+  const size_t dd = (size_t)d * d;
+  const double2* Pc = R.pc + ((size_t)b * P.L + n) * (size_t)R.traj_len * dd;
+  const size_t tix = ((size_t)b * P.L + n) * d;
+  const size_t cix = ((size_t)b * P.L + n) * nchunk + ch;
+  const double2 zero = cx(0.0, 0.0);
+  const double2 phi = i < d ? R.task_init[tix + i] : zero;
+  const double2 targ = i < d ? R.task_targ[tix + i] : zero;
+  S.phi[i] = phi;
+  __syncwarp();
+  const double2* PL = Pc + (size_t)len * dd;
+  const double2 psiL = matvec_row(PL, d, i, S.phi);
+
+  if (mode & (PC_GRAD | PC_ERR | PC_RAWGRAD)) {
+    // chi_0 = P_len^dag seed (objective.cpp:31-34 seed)
+    S.vec[i] = A.form == 0 ? targ : csub(targ, psiL);
+    __syncwarp();
+    S.chi0[i] = matvec_adj_row(PL, d, i, S.vec);
+    __syncwarp();
+  }
+  if (ch == 0) {
+    if (mode & PC_ENTRY) {  // payoff of the task (objective.cpp:22-29)
+      double t = 0.0;
+      if (i < d) t = A.form == 0 ? cconjmul(targ, psiL).x : cabs2(csub(psiL, targ));
+      const double s = warp_sum(t);
+      if (i == 0) R.entry_pay[(size_t)b * P.L + n] = A.form == 0 ? (w * s) : (-0.5 * (w * s));
+    }
+    if ((mode & PC_FINAL) && i < d) R.psi_end[tix + i] = psiL;
+    if (mode & PC_LAG) {  // ism.cpp:424-459 through the cached product
+      S.vec[i] = i < d ? R.psi_nodes[((size_t)b * (P.L + 1) + n) * d + i] : zero;
+      __syncwarp();
+      const double2 pe = matvec_row(PL, d, i, S.vec);
+      __syncwarp();
+      S.vec[i] = i < d ? R.chi_nodes[((size_t)b * (P.L + 1) + n + 1) * d + i] : zero;
+      __syncwarp();
+      const double2 cs = matvec_adj_row(PL, d, i, S.vec);
+      if (i < d) {
+        R.psi_end[tix + i] = pe;
+        R.chi_start[tix + i] = cs;
+      }
+      __syncwarp();
+    }
+  }
+  // penalty of the task window at the current control (before any update of this chunk)
+  double pen = 0.0;
+  for (int j = j0 + i; j < j1; j += 32) {
+    double sq = 0.0;
+    for (int c = 0; c < C; ++c) sq += u[(size_t)j * C + c] * u[(size_t)j * C + c];
+    pen += (P.alpha[node0 + j] * scale) * sq;
+  }
+  pen = warp_sum(pen);
+
+  double err = 0.0;
+  if (mode & (PC_GRAD | PC_ERR | PC_RAWGRAD)) {
+    double2 psa = matvec_row(Pc + (size_t)j0 * dd, d, i, S.phi);
+    double2 cha = matvec_row(Pc + (size_t)j0 * dd, d, i, S.chi0);
+    for (int j = j0; j < j1; ++j) {
+      const double2* Pj1 = Pc + (size_t)(j + 1) * dd;
+      const double2 psb = matvec_row(Pj1, d, i, S.phi);
+      const double2 chb = matvec_row(Pj1, d, i, S.chi0);
+      const double2 ps = cadd(psa, psb), cs = cadd(cha, chb);
+      const double* uj = u + (size_t)j * C;
+      const double aj = P.alpha[node0 + j] * scale;
+      double g[4];
+      double sq = 0.0;
+      for (int c = 0; c < C && c < 4; ++c) {
+        const double uc = uj[c];
+        double2 h;
+        if (TRI) {
+          h = tri_dH_row(P, b, c, uc, i, ps);
+        } else {
+          S.vec[i] = ps;
+          __syncwarp();
+          h = i < d ? dense_dH_row(P, b, c, uc, i, S.vec) : zero;
+          __syncwarp();
+        }
+        const double im = warp_sum(i < d ? cconjmul(cs, h).y : 0.0);
+        g[c] = -aj * dt * uc + 0.25 * dt * (w * im);  // gradient_sweep, objective.cpp:55-57
+        sq += g[c] * g[c];
+      }
+      if (i == 0) {
+        for (int c = 0; c < C && c < 4; ++c) {
+          if (mode & PC_RAWGRAD) R.grad[((size_t)b * P.K + node0 + j) * C + c] = g[c];
+          if (mode & PC_GRAD) u[(size_t)j * C + c] = uj[c] + A.rho * (weight * g[c]);
+        }
+      }
+      err += sqrt(sq);
+      psa = psb;
+      cha = chb;
+    }
+  }
+  if (i == 0) {
+    R.chunk_pen[cix] = pen;
+    R.chunk_err[cix] = err;
+  }
+}
+
+// entry value = weight * (payoff - penalty), residual = sum of chunk partials (index order)
+__global__ void pc_finalize_kernel(DevProblem P, DevRun R, TaskArgs A, int nchunk, int ignore_done) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= P.B * P.L) return;
+  const int b = t / P.L, n = t % P.L;
+  if (ignore_done ? R.status[b] : R.done[b]) return;
+  const int len = P.node[n + 1] - P.node[n];
+  const double weight = A.weighted ? (double)P.K / (double)len : 1.0;
+  double pen = 0.0, err = 0.0;
+  for (int c = 0; c < nchunk; ++c) {
+    pen += R.chunk_pen[(size_t)t * nchunk + c];
+    err += R.chunk_err[(size_t)t * nchunk + c];
+  }
+  if (A.mode & PC_ENTRY) R.entry[t] = weight * (R.entry_pay[t] - 0.5 * P.dt * pen);
+  if (A.mode & PC_ERR) R.err[t] = err;
+}
+
+// ---- dense assembly sweep: lane group of D lanes per task (row per lane) ------------------
+template <int D>
+__global__ void __launch_bounds__(128) dense_pc_assemble_kernel(DevProblem P, DevRun R, int tasks_per_cta,
+                                                                int ignore_done) {
+  using Cfg = DenseCfg<D, 1>;
+  constexpr int NL = Cfg::NL, COLS = Cfg::COLS, TPW = Cfg::TPW;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* ops = reinterpret_cast<double2*>(smem_raw);
+  const int b = blockIdx.y;
+  if (ignore_done ? R.status[b] : R.done[b]) return;
+  const int nops = 1 + P.C + (P.has_quad ? P.C : 0);
+  const int d = P.d;
+  for (int e = threadIdx.x; e < nops * D * D; e += blockDim.x) {
+    const int o = e / (D * D), r = (e / D) % D, c = e % D;
+    double2 v = cx(0.0, 0.0);
+    if (r < d && c < d) {
+      const size_t dd = (size_t)d * d;
+      if (o == 0) v = P.h0[(size_t)b * dd + r * d + c];
+      else if (o <= P.C) v = P.lin[((size_t)b * P.C + (o - 1)) * dd + r * d + c];
+      else v = P.quad[((size_t)b * P.C + (o - 1 - P.C)) * dd + r * d + c];
+    }
+    ops[e] = v;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, l32 = threadIdx.x & 31;
+  const int gid = warp * TPW + l32 / NL, lane = l32 % NL;
+  const int n_raw = blockIdx.x * tasks_per_cta + gid;
+  const bool live_task = n_raw < P.L;
+  if (!__any_sync(0xffffffffu, live_task)) return;
+  const int n = live_task ? n_raw : P.L - 1;
+  const size_t gbytes = sizeof(double2) * (Cfg::PIV + Cfg::VEC + 2 * Cfg::MAT) + sizeof(int) * 2 * D;
+  unsigned char* sp = smem_raw + sizeof(double2) * (size_t)nops * D * D + gbytes * gid;
+  DenseScratch<D, 1> S;
+  S.piv = reinterpret_cast<double2*>(sp);
+  S.vec = S.piv + Cfg::PIV;
+  S.matW = S.vec + Cfg::VEC;
+  S.matP = S.matW + Cfg::MAT;
+  S.perm = reinterpret_cast<int*>(S.matP + Cfg::MAT);
+  DenseLane<D, 1> Ln;
+  Ln.row = lane;
+  Ln.g = 0;
+  const int row = lane, C = P.C;
+  const int node0 = P.node[n], len = P.node[n + 1] - node0;
+  int lenmax = len;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) lenmax = max(lenmax, __shfl_xor_sync(0xffffffffu, lenmax, off));
+  const double half = 0.5 * P.dt;
+  const double* u = R.u + ((size_t)b * P.K + node0) * C;
+  const size_t dd = (size_t)d * d;
+  double2* Pc = R.pc + ((size_t)b * P.L + n) * (size_t)R.traj_len * dd;
+  double2 W[COLS], Pm[COLS];
+#pragma unroll
+  for (int t = 0; t < COLS; ++t) Pm[t] = cx(row == t ? 1.0 : 0.0, 0.0);
+  if (live_task && row < d)
+#pragma unroll
+    for (int t = 0; t < COLS; ++t)
+      if (t < d) Pc[(size_t)row * d + t] = Pm[t];
+  const double* nrm = P.norm1 + (size_t)b * (1 + 2 * C);
+  for (int j = 0; j < lenmax; ++j) {
+    const bool live = j < len;
+    const double* uj = u + (size_t)min(j, len - 1) * C;
+    Ln.build(W, ops, C, P.has_quad, uj, half, false);
+    double bound = nrm[0];
+    for (int c = 0; c < C; ++c) {
+      bound += fabs(uj[c]) * nrm[1 + c];
+      if (P.has_quad) bound += 0.5 * uj[c] * uj[c] * nrm[1 + C + c];
+    }
+    if (__any_sync(0xffffffffu, !(half * bound < 1.0)))
+      Ln.invert_pivot(W, S, lane);
+    else
+      Ln.invert_fast(W, S.piv);
+    double2 Q[COLS];
+#pragma unroll
+    for (int t = 0; t < COLS; ++t) Q[t] = Pm[t];
+    Ln.cayley_matmul(W, Q, S);
+    if (live) {
+#pragma unroll
+      for (int t = 0; t < COLS; ++t) Pm[t] = Q[t];
+      if (live_task && row < d) {
+        double2* dst = Pc + (size_t)(j + 1) * dd + (size_t)row * d;
+#pragma unroll
+        for (int t = 0; t < COLS; ++t)
+          if (t < d) dst[t] = Pm[t];
+      }
+    }
+  }
+  if (live_task && row < d && R.prop) {
+    double2* M = R.prop + ((size_t)b * P.L + n) * dd + (size_t)row * d;
+#pragma unroll
+    for (int t = 0; t < COLS; ++t)
+      if (t < d) M[t] = Pm[t];
+  }
+}
+
+}  // namespace
+
+// ---- tridiagonal assembly sweep (defined in tridiag_kernels.cu) ---------------------------
+cudaError_t tri_pc_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st);
+
+int pc_chunk(const DevProblem& P, const DevRun& R) {
+  (void)P;
+  const int maxlen = R.traj_len - 1;
+  return maxlen <= 32 ? maxlen : 16;
+}
+
+cudaError_t pc_eval(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
+  const int chunk = pc_chunk(P, R);
+  const int nchunk = (R.traj_len - 1 + chunk - 1) / chunk;
+  dim3 grid((P.L * nchunk + 3) / 4, P.B);
+  if (P.kind == QOC_KIND_TRIDIAG)
+    pc_eval_kernel<true><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
+  else
+    pc_eval_kernel<false><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  pc_finalize_kernel<<<(P.B * P.L + 127) / 128, 128, 0, st>>>(P, R, A, nchunk, ignore_done);
+  return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t launch_dense_pc(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st) {
+  using Cfg = DenseCfg<D, 1>;
+  constexpr int TPW = Cfg::TPW;
+  int warps = (P.L + TPW - 1) / TPW;
+  if (warps > 4) warps = 4;
+  const int tpc = warps * TPW;
+  const int nops = 1 + P.C + (P.has_quad ? P.C : 0);
+  const size_t gbytes = sizeof(double2) * (Cfg::PIV + Cfg::VEC + 2 * Cfg::MAT) + sizeof(int) * 2 * D;
+  const size_t smem = sizeof(double2) * (size_t)nops * D * D + gbytes * tpc;
+  auto kern = dense_pc_assemble_kernel<D>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<dim3((P.L + tpc - 1) / tpc, P.B), warps * 32, smem, st>>>(P, R, tpc, ignore_done);
+  return cudaGetLastError();
+}
+
+cudaError_t pc_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st) {
+  if (P.kind == QOC_KIND_TRIDIAG) return tri_pc_assemble(P, R, ignore_done, st);
+  switch (dense_pad(P.d)) {
+    case 2: return launch_dense_pc<2>(P, R, ignore_done, st);
+    case 4: return launch_dense_pc<4>(P, R, ignore_done, st);
+    case 8: return launch_dense_pc<8>(P, R, ignore_done, st);
+    case 16: return launch_dense_pc<16>(P, R, ignore_done, st);
+    case 32: return launch_dense_pc<32>(P, R, ignore_done, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+int pc_nchunk(const DevProblem& P, const DevRun& R) {
+  const int chunk = pc_chunk(P, R);
+  return (R.traj_len - 1 + chunk - 1) / chunk;
+}
+
+}  // namespace qoc

@@ -349,7 +349,56 @@ __global__ void __launch_bounds__(32) tridiag_horizon_kernel(DevProblem P, DevRu
   if (!ok && R.err_flags) atomicOr(R.err_flags, 1);
 }
 
+// Assembly sweep of the propagator cache (pcache.cu): lane k carries column k of P_j.
+template <int TD>
+__global__ void __launch_bounds__(32) tri_pc_assemble_kernel(DevProblem P, DevRun R, int ignore_done) {
+  const int n = blockIdx.x, b = blockIdx.y, lane = threadIdx.x;
+  if (ignore_done ? R.status[b] : R.done[b]) return;
+  const int d = P.d, C = P.C;
+  const int nops = 1 + C + (P.has_quad ? C : 0);
+  const TriView T{P.tri_diag + (size_t)b * nops * d, P.tri_sub + (size_t)b * nops * (d - 1), d, C, P.has_quad};
+  const int node0 = P.node[n], len = P.node[n + 1] - node0;
+  const double half = 0.5 * P.dt;
+  const double* u = R.u + ((size_t)b * P.K + node0) * C;
+  const size_t dd = (size_t)d * d;
+  double2* Pc = R.pc + ((size_t)b * P.L + n) * (size_t)R.traj_len * dd;
+  const bool col = lane < d;
+  bool ok = true;
+  double2 x[TD];
+#pragma unroll
+  for (int i = 0; i < TD; ++i) x[i] = cx(i == lane ? 1.0 : 0.0, 0.0);
+  if (col)
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+      if (i < d) Pc[(size_t)i * d + lane] = x[i];
+  for (int j = 0; j < len; ++j) {
+    ok &= cayley_tri<TD>(T, u + (size_t)j * C, half, x);
+    if (col) {
+      double2* dst = Pc + (size_t)(j + 1) * dd;
+#pragma unroll
+      for (int i = 0; i < TD; ++i)
+        if (i < d) dst[(size_t)i * d + lane] = x[i];
+    }
+  }
+  if (col && R.prop) {
+    double2* M = R.prop + ((size_t)b * P.L + n) * dd;
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+      if (i < d) M[(size_t)i * d + lane] = x[i];
+  }
+  if (!ok && R.err_flags) atomicOr(R.err_flags, 1);
+}
+
 }  // namespace
+
+cudaError_t tri_pc_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st) {
+  if (P.d > 30) return cudaErrorNotSupported;
+  if (P.d <= 24)
+    tri_pc_assemble_kernel<24><<<dim3(P.L, P.B), 32, 0, st>>>(P, R, ignore_done);
+  else
+    tri_pc_assemble_kernel<32><<<dim3(P.L, P.B), 32, 0, st>>>(P, R, ignore_done);
+  return cudaGetLastError();
+}
 
 cudaError_t tridiag_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
   if (P.d > 30) return cudaErrorNotSupported;
