@@ -1,0 +1,462 @@
+// bitflip_kernels.cu — ISM task/horizon kernels for spin registers in bit-flip form
+// (QOC_KIND_BITFLIP, d = 2^n, 5 <= n <= 12; BASELINE config 3, the n = 10 Ising chain).
+//
+// H(u) = diag(h0) + V(u),  V(u) = sum_i (ax_i sigma^x_i + ay_i sigma^y_i),
+// ax_i = sum_{c: axis x} u_c coef[c][i],  ay_i = sum_{c: axis y} u_c coef[c][i].
+// The matrix is never formed: V y is n bit-flip gathers per element.  The Cayley step of the
+// reference (propagation.cpp:85-106, (I + sH) y = (I - sH) x, s = +-i dt/2) is solved by the
+// Jacobi-preconditioned fixed point the oracle restates (oracle.cpp BitM::cayley)
+//     y <- (1 + sD)^-1 (r - s V y),    r = x - s H x,
+// i.e. the Neumann series of (I + sH)^-1 around its diagonal.  |1 + sD_i| >= 1, so the
+// iteration contracts by q = dt/2 * sum_i sqrt(ax_i^2 + ay_i^2) per sweep; the sweep count
+// is fixed per step from that a-priori bound (q^(k+1) <= 2^-53) instead of a data-dependent
+// stopping test, so every thread agrees without a reduction.
+//
+// Layout: one CTA of T = min(d, 256) threads per (problem, subinterval) task; thread t holds
+// the E = d/T amplitudes s = t + e*T.  A flip of bit b pairs
+//   b < 5              -> lane t ^ 2^b of the same warp        (shuffle)
+//   5 <= b < log2 T    -> thread t ^ 2^b                        (shared memory, double buffer)
+//   b >= log2 T        -> register slot e ^ 2^(b - log2 T)     (same thread)
+// so one fixed-point sweep costs one __syncthreads.  Spin i <-> bit n-1-i (spin_operator,
+// models.cpp:296-318).  The forward trajectory of a task (len+1 states, 16 KB each at
+// d = 1024) lives in HBM/L2 (R.traj); the adjoint sweep reads it back for the gradient.
+#include "kernels.h"
+
+namespace qoc {
+
+namespace {
+
+constexpr int BF_MAXN = 12;
+constexpr int BF_T = 256;
+
+struct Geo {
+  int n, log2T, T, t, lane, warp, nwarp;
+};
+
+// Calls f(e, spin, bit_of_s, partner_value) for every amplitude slot e and spin.
+template <int E, int LOG2E, class F>
+__device__ __forceinline__ void for_flips(const Geo& G, const double2 (&v)[E], const double2* buf, F&& f) {
+#pragma unroll
+  for (int hb = 0; hb < LOG2E; ++hb) {
+    const int spin = G.n - 1 - (G.log2T + hb);
+#pragma unroll
+    for (int e = 0; e < E; ++e) f(e, spin, (e >> hb) & 1, v[e ^ (1 << hb)]);
+  }
+  for (int b = 0; b < G.log2T; ++b) {
+    const int spin = G.n - 1 - b;
+    const int m = 1 << b;
+    const int one = (G.t & m) != 0;
+    if (m < 32) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) f(e, spin, one, shfl_xor(v[e], m));
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) f(e, spin, one, buf[(G.t ^ m) + e * G.T]);
+    }
+  }
+}
+
+// <s| (a sigma^x + b sigma^y) |s ^ m> = a + (bit(s) ? +i : -i) b   (oracle.cpp BitM::offdiag)
+__device__ __forceinline__ double2 flip_coef(double2 ab, int one) { return cx(ab.x, one ? ab.y : -ab.y); }
+
+struct BfOps {
+  const double* diag;  // [d]
+  const double* coef;  // [C][n]
+  const int* axis;     // [C]
+  int C, n;
+};
+
+// Per-step channel sums (ax_i, ay_i) for spin i, written by threads i < n.
+__device__ __forceinline__ void channel_sums(const BfOps& O, const double* uj, double2* sa) {
+  const int i = threadIdx.x;
+  if (i < O.n) {
+    double ax = 0.0, ay = 0.0;
+    for (int c = 0; c < O.C; ++c) {
+      const double g = uj[c] * O.coef[c * O.n + i];
+      if (O.axis[c] == 0) ax += g;
+      else ay += g;
+    }
+    sa[i] = cx(ax, ay);
+  }
+}
+
+// Sweeps needed for q^(k+1) <= 2^-53; returns -1 when the Neumann series would not contract.
+__device__ __forceinline__ int sweep_count(const double2* sa, int n, double half) {
+  double q = 0.0;
+  for (int i = 0; i < n; ++i) q += sqrt(sa[i].x * sa[i].x + sa[i].y * sa[i].y);
+  q *= half;
+  if (!(q < 0.5)) return -1;
+  if (q <= 0.0) return 0;
+  return (int)ceil(53.0 * 0.6931471805599453 / -log(q));
+}
+
+template <int E, int LOG2E>
+struct Bf {
+  Geo G;
+  double dg[E];      // diagonal of H at this thread's amplitudes
+  double2* buf;      // smem [2][d] exchange
+  double2* sa;       // smem [2][BF_MAXN] per-step channel sums (by step parity)
+  double* red;       // smem [BF_T / 32][4] reduction scratch
+  int par = 0;       // exchange buffer parity
+  int spar = 0;      // channel-sum parity
+
+  __device__ void publish(const double2 (&v)[E]) {
+    par ^= 1;
+    double2* b = buf + par * (G.T * E);
+#pragma unroll
+    for (int e = 0; e < E; ++e) b[G.t + e * G.T] = v[e];
+  }
+  __device__ const double2* cur() const { return buf + par * (G.T * E); }
+
+  // V v (after publish(v) + __syncthreads)
+  __device__ void apply_V(const double2 (&v)[E], const double2* s, double2 (&out)[E]) const {
+#pragma unroll
+    for (int e = 0; e < E; ++e) out[e] = cx(0.0, 0.0);
+    for_flips<E, LOG2E>(G, v, cur(), [&](int e, int spin, int one, double2 pv) {
+      out[e] = cfma(flip_coef(s[spin], one), pv, out[e]);
+    });
+  }
+
+  // x <- (I + sH)^-1 (I - sH) x, s = (0, sh).  Begins with the step's channel sums already
+  // in sa[spar] (see begin_step).  Returns false if the series would not contract.
+  __device__ bool cayley(double2 (&x)[E], double sh, int sweeps) {
+    const double2* s = sa + spar * BF_MAXN;
+    double2 r[E], y[E], vv[E];
+    publish(x);
+    __syncthreads();
+    apply_V(x, s, vv);
+    double2 inv[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const double2 hx = cx(fma(dg[e], x[e].x, vv[e].x), fma(dg[e], x[e].y, vv[e].y));
+      r[e] = cx(x[e].x + sh * hx.y, x[e].y - sh * hx.x);  // x - s H x
+      const double a = sh * dg[e];
+      const double den = 1.0 / fma(a, a, 1.0);
+      inv[e] = cx(den, -a * den);                           // (1 + s D)^-1
+      y[e] = cmul(r[e], inv[e]);
+    }
+    for (int k = 0; k < sweeps; ++k) {
+      publish(y);
+      __syncthreads();
+      apply_V(y, s, vv);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const double2 t = cx(r[e].x + sh * vv[e].y, r[e].y - sh * vv[e].x);  // r - s V y
+        y[e] = cmul(t, inv[e]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = y[e];
+    return sweeps >= 0;
+  }
+
+  // Publishes the channel sums of u_j; must be followed by a __syncthreads before use
+  // (cayley's first publish/sync provides it).
+  __device__ void begin_step(const BfOps& O, const double* uj) {
+    spar ^= 1;
+    channel_sums(O, uj, sa + spar * BF_MAXN);
+  }
+
+  // Deterministic block sum of up to 4 values (fixed warp order).
+  __device__ void block_sum(double (&v)[4], int nv) {
+    for (int q = 0; q < nv; ++q) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
+    }
+    __syncthreads();
+    if (G.lane == 0)
+      for (int q = 0; q < nv; ++q) red[G.warp * 4 + q] = v[q];
+    __syncthreads();
+    for (int q = 0; q < nv; ++q) {
+      double s = 0.0;
+      for (int w = 0; w < G.nwarp; ++w) s += red[w * 4 + q];
+      v[q] = s;
+    }
+  }
+
+  // Im <cs, A_c ps> for every channel (A_c = sum_i coef[c][i] sigma^{axis_c}_i), block-summed.
+  // ps must be published (and synced) by the caller.
+  __device__ void grad_terms(const BfOps& O, const double2 (&cs)[E], const double2 (&ps)[E], double (&out)[4]) {
+    double2 acc[4] = {cx(0.0, 0.0), cx(0.0, 0.0), cx(0.0, 0.0), cx(0.0, 0.0)};
+    for_flips<E, LOG2E>(G, ps, cur(), [&](int e, int spin, int one, double2 pv) {
+      for (int c = 0; c < O.C && c < 4; ++c) {
+        const double g = O.coef[c * O.n + spin];
+        const double2 a = O.axis[c] == 0 ? cx(g, 0.0) : flip_coef(cx(0.0, g), one);
+        acc[c] = cfmaconj(cs[e], cmul(a, pv), acc[c]);
+      }
+    });
+    for (int c = 0; c < 4; ++c) out[c] = acc[c].y;
+    block_sum(out, O.C < 4 ? O.C : 4);
+  }
+};
+
+template <int E, int LOG2E>
+__device__ __forceinline__ Bf<E, LOG2E> make_bf(const DevProblem& P, int b, unsigned char* smem) {
+  Bf<E, LOG2E> F;
+  F.G.n = P.nspins;
+  F.G.T = P.d / E;
+  F.G.log2T = P.nspins - LOG2E;
+  F.G.t = threadIdx.x;
+  F.G.lane = threadIdx.x & 31;
+  F.G.warp = threadIdx.x >> 5;
+  F.G.nwarp = F.G.T >> 5;
+  F.buf = reinterpret_cast<double2*>(smem);
+  F.sa = F.buf + 2 * P.d;
+  F.red = reinterpret_cast<double*>(F.sa + 2 * BF_MAXN);
+#pragma unroll
+  for (int e = 0; e < E; ++e) F.dg[e] = P.bf_diag[(size_t)b * P.d + F.G.t + e * F.G.T];
+  return F;
+}
+
+__host__ __device__ constexpr size_t bf_smem(int d) {
+  return sizeof(double2) * (2 * (size_t)d + 2 * BF_MAXN) + sizeof(double) * (BF_T / 32) * 4;
+}
+
+template <int E>
+__device__ __forceinline__ void load_state(double2 (&x)[E], const double2* src, int t, int T) {
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = src[t + e * T];
+}
+template <int E>
+__device__ __forceinline__ void store_state(const double2 (&x)[E], double2* dst, int t, int T) {
+#pragma unroll
+  for (int e = 0; e < E; ++e) dst[t + e * T] = x[e];
+}
+
+template <int E, int LOG2E>
+__global__ void __launch_bounds__(BF_T) bitflip_task_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done) {
+  const int n = blockIdx.x, b = blockIdx.y;
+  if (ignore_done ? R.status[b] : R.done[b]) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  Bf<E, LOG2E> F = make_bf<E, LOG2E>(P, b, smem);
+  const int d = P.d, C = P.C, t = F.G.t, T = F.G.T;
+  const BfOps O{P.bf_diag + (size_t)b * d, P.bf_coef + (size_t)b * C * P.nspins, P.bf_axis, C, P.nspins};
+  const int node0 = P.node[n], len = P.node[n + 1] - node0;
+  const double Kd = (double)P.K;
+  const double weight = A.weighted ? Kd / (double)len : 1.0;
+  const double scale = (double)len / Kd;
+  const double half = 0.5 * P.dt, dt = P.dt, w = P.ip_w;
+  double* u = R.u + ((size_t)b * P.K + node0) * C;
+  double2* traj = R.traj + ((size_t)b * P.L + n) * (size_t)R.traj_len * d;
+  const size_t tix = ((size_t)b * P.L + n) * d;
+  const int mode = A.mode;
+  bool ok = true;
+  double2 x[E], chi[E], cn[E], ps[E], tg[E];
+  load_state<E>(tg, R.task_targ + tix, t, T);
+
+  auto step = [&](double2 (&v)[E], const double* uj, double sh) {
+    F.begin_step(O, uj);
+    __syncthreads();
+    const int sweeps = sweep_count(F.sa + F.spar * BF_MAXN, O.n, half);
+    ok &= F.cayley(v, sh, sweeps < 0 ? 0 : sweeps) && sweeps >= 0;
+  };
+  // forward sweep from `init`, optionally recording the trajectory
+  auto forward = [&](double2 (&v)[E], bool rec, double* pen) {
+    if (rec) store_state<E>(v, traj, t, T);
+    for (int j = 0; j < len; ++j) {
+      const double* uj = u + (size_t)j * C;
+      step(v, uj, half);
+      if (rec) store_state<E>(v, traj + (size_t)(j + 1) * d, t, T);
+      if (pen) {
+        double sq = 0.0;
+        for (int c = 0; c < C; ++c) sq += uj[c] * uj[c];
+        *pen += (P.alpha[node0 + j] * scale) * sq;
+      }
+    }
+  };
+  // adjoint sweep with the gradient of objective.cpp:48-60 at every step; `act(j, g)`
+  auto adjoint = [&](double2 (&c0)[E], auto&& act) {
+    for (int j = len - 1; j >= 0; --j) {
+      const double* uj = u + (size_t)j * C;
+      double uold[4];
+      for (int c = 0; c < C && c < 4; ++c) uold[c] = uj[c];
+#pragma unroll
+      for (int e = 0; e < E; ++e) cn[e] = c0[e];
+      step(cn, uj, -half);
+      double2 cs[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const double2 a = traj[(size_t)j * d + t + e * T], bb = traj[(size_t)(j + 1) * d + t + e * T];
+        ps[e] = cadd(a, bb);
+        cs[e] = cadd(cn[e], c0[e]);
+      }
+      F.publish(ps);
+      __syncthreads();
+      double im[4];
+      F.grad_terms(O, cs, ps, im);
+      const double aj = P.alpha[node0 + j] * scale;
+      double g[4];
+      for (int c = 0; c < C && c < 4; ++c) g[c] = -aj * dt * uold[c] + 0.25 * dt * (w * im[c]);
+      act(j, uold, g);
+#pragma unroll
+      for (int e = 0; e < E; ++e) c0[e] = cn[e];
+    }
+  };
+
+  // ---------------- phase 1: sweeps at the current control -------------------------
+  if (mode & (M_ENTRY | M_UPDATE | M_FINAL | M_GRAD)) {
+    const bool need_traj = (mode & (M_UPDATE | M_GRAD)) != 0;
+    const int iters = (mode & M_UPDATE) ? A.inner : 1;
+    for (int it = 0; it < iters; ++it) {
+      load_state<E>(x, R.task_init + tix, t, T);
+      double pen = 0.0;
+      forward(x, need_traj, &pen);
+      if (it == 0 && (mode & M_ENTRY)) {
+        double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int e = 0; e < E; ++e) s[0] += A.form == 0 ? cconjmul(tg[e], x[e]).x : cabs2(csub(x[e], tg[e]));
+        F.block_sum(s, 1);
+        const double payoff = A.form == 0 ? (w * s[0]) : (-0.5 * (w * s[0]));
+        if (t == 0) R.entry[(size_t)b * P.L + n] = weight * (payoff - 0.5 * dt * pen);
+      }
+      if (it == 0 && (mode & M_FINAL)) store_state<E>(x, R.psi_end + tix, t, T);
+      if (mode & (M_UPDATE | M_GRAD)) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) chi[e] = A.form == 0 ? tg[e] : csub(tg[e], x[e]);  // objective.cpp:31-34
+        adjoint(chi, [&](int j, const double* uold, const double* g) {
+          if (t == 0) {
+            for (int c = 0; c < C && c < 4; ++c) {
+              if (mode & M_GRAD) R.grad[((size_t)b * P.K + node0 + j) * C + c] = g[c];
+              if (mode & M_UPDATE) u[(size_t)j * C + c] = uold[c] + A.rho * (weight * g[c]);
+            }
+          }
+          __syncthreads();  // the updated u_j is read by every thread at the next sweep
+        });
+      }
+    }
+  }
+
+  // ---------------- phase 2: sweeps at the updated control -------------------------
+  if (mode & M_ERROR) {
+    load_state<E>(x, R.task_init + tix, t, T);
+    forward(x, true, nullptr);
+#pragma unroll
+    for (int e = 0; e < E; ++e) chi[e] = A.form == 0 ? tg[e] : csub(tg[e], x[e]);
+    double err = 0.0;
+    adjoint(chi, [&](int, const double*, const double* g) {
+      double sq = 0.0;
+      for (int c = 0; c < C && c < 4; ++c) sq += g[c] * g[c];
+      err += sqrt(sq);
+    });
+    if (t == 0) R.err[(size_t)b * P.L + n] = err;
+  }
+  if (mode & M_LAGGED) {  // ism.cpp:424-459
+    load_state<E>(x, R.psi_nodes + ((size_t)b * (P.L + 1) + n) * d, t, T);
+    forward(x, false, nullptr);
+    store_state<E>(x, R.psi_end + tix, t, T);
+    load_state<E>(chi, R.chi_nodes + ((size_t)b * (P.L + 1) + n + 1) * d, t, T);
+    for (int j = len - 1; j >= 0; --j) step(chi, u + (size_t)j * C, -half);
+    store_state<E>(chi, R.chi_start + tix, t, T);
+  }
+  if (!ok && t == 0 && R.err_flags) atomicOr(R.err_flags, 2);
+}
+
+// node_sweeps (ism.cpp:35-84) / exact payoff (objective.cpp:93-100) over the full horizon.
+// blockIdx.y = 0: forward nodes psi_n (which = 0) or the exact payoff (which = 1);
+// blockIdx.y = 1: adjoint nodes chi_n seeded with the target (ism.cpp:72), which = 0 only.
+template <int E, int LOG2E>
+__global__ void __launch_bounds__(BF_T) bitflip_horizon_kernel(DevProblem P, DevRun R, int which, int k) {
+  const int b = blockIdx.x, dir = blockIdx.y;
+  if (R.done[b] || R.status[b]) return;
+  if (which == 1 && dir == 1) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  Bf<E, LOG2E> F = make_bf<E, LOG2E>(P, b, smem);
+  const int d = P.d, C = P.C, t = F.G.t, T = F.G.T;
+  const BfOps O{P.bf_diag + (size_t)b * d, P.bf_coef + (size_t)b * C * P.nspins, P.bf_axis, C, P.nspins};
+  const double half = 0.5 * P.dt;
+  const double* u = R.u + (size_t)b * P.K * C;
+  const size_t nb = (size_t)b * (P.L + 1) * d;
+  bool ok = true;
+  double2 x[E];
+  auto step = [&](const double* uj, double sh) {
+    F.begin_step(O, uj);
+    __syncthreads();
+    const int sweeps = sweep_count(F.sa + F.spar * BF_MAXN, O.n, half);
+    ok &= F.cayley(x, sh, sweeps < 0 ? 0 : sweeps) && sweeps >= 0;
+  };
+  if (dir == 0) {
+    load_state<E>(x, P.init + (size_t)b * d, t, T);
+    if (which == 0) store_state<E>(x, R.psi_nodes + nb, t, T);
+    int nxt = 1;
+    for (int j = 0; j < P.K; ++j) {
+      step(u + (size_t)j * C, half);
+      if (which == 0 && nxt <= P.L && P.node[nxt] == j + 1) {
+        store_state<E>(x, R.psi_nodes + nb + (size_t)nxt * d, t, T);
+        ++nxt;
+      }
+    }
+    if (which == 1) {
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int e = 0; e < E; ++e) s[0] += cconjmul(P.targ[(size_t)b * d + t + e * T], x[e]).x;
+      F.block_sum(s, 1);
+      if (t == 0) {
+        double pen = 0.0;
+        for (int n = 0; n < P.L; ++n) pen += R.pen[(size_t)b * P.L + n];
+        R.rec_exact[(size_t)b * R.cap + k] = P.ip_w * s[0] - 0.5 * P.dt * pen;
+      }
+    }
+  } else {
+    load_state<E>(x, P.targ + (size_t)b * d, t, T);
+    store_state<E>(x, R.chi_nodes + nb + (size_t)P.L * d, t, T);
+    int prev = P.L - 1;
+    for (int j = P.K - 1; j >= 0; --j) {
+      step(u + (size_t)j * C, -half);
+      if (prev >= 0 && P.node[prev] == j) {
+        store_state<E>(x, R.chi_nodes + nb + (size_t)prev * d, t, T);
+        --prev;
+      }
+    }
+  }
+  if (!ok && t == 0 && R.err_flags) atomicOr(R.err_flags, 2);
+}
+
+template <int E, int LOG2E>
+cudaError_t launch_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
+  const size_t smem = bf_smem(P.d);
+  auto kern = bitflip_task_kernel<E, LOG2E>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<dim3(P.L, P.B), P.d / E, smem, st>>>(P, R, A, ignore_done);
+  return cudaGetLastError();
+}
+
+template <int E, int LOG2E>
+cudaError_t launch_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
+  const size_t smem = bf_smem(P.d);
+  auto kern = bitflip_horizon_kernel<E, LOG2E>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<dim3(P.B, 2), P.d / E, smem, st>>>(P, R, which, k);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// d = 2^n: T = min(d, 256) threads, E = d / T amplitudes per thread.
+cudaError_t bitflip_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
+  if (A.mode & M_ASSEMBLE) return cudaErrorNotSupported;  // the driver runs the direct plan
+  if (P.C > 4) return cudaErrorNotSupported;
+  switch (P.nspins) {
+    case 5: case 6: case 7: case 8: return launch_task<1, 0>(P, R, A, ignore_done, st);
+    case 9: return launch_task<2, 1>(P, R, A, ignore_done, st);
+    case 10: return launch_task<4, 2>(P, R, A, ignore_done, st);
+    case 11: return launch_task<8, 3>(P, R, A, ignore_done, st);
+    case 12: return launch_task<16, 4>(P, R, A, ignore_done, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+cudaError_t bitflip_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
+  if (P.C > 4) return cudaErrorNotSupported;
+  switch (P.nspins) {
+    case 5: case 6: case 7: case 8: return launch_horizon<1, 0>(P, R, which, k, st);
+    case 9: return launch_horizon<2, 1>(P, R, which, k, st);
+    case 10: return launch_horizon<4, 2>(P, R, which, k, st);
+    case 11: return launch_horizon<8, 3>(P, R, which, k, st);
+    case 12: return launch_horizon<16, 4>(P, R, which, k, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+}  // namespace qoc

@@ -212,8 +212,8 @@ void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaS
     }
     case QOC_KIND_BITFLIP: {
       if (!p->h0 || !p->bf_axis || !p->bf_coef) fail(QOC_EINVAL, "bit-flip model needs h0/axis/coef");
-      if (p->nspins < 1 || p->nspins > 12 || (1 << p->nspins) != d)
-        fail(QOC_EINVAL, "bit-flip dim must be 2^nspins (nspins <= 12)");
+      if (p->nspins < 5 || p->nspins > 12 || (1 << p->nspins) != d)
+        fail(QOC_EINVAL, "bit-flip dim must be 2^nspins (5 <= nspins <= 12)");
       P.nspins = p->nspins;
       P.bf_diag = out.keep<double>(upload(p->h0, (size_t)B * d, st));
       P.bf_axis = out.keep<int>(upload(p->bf_axis, (size_t)C, st));
@@ -386,6 +386,8 @@ void check_flags(const DevRun& R) {
   if (flags & 1)
     fail(QOC_ERUNTIME, "tridiagonal Cayley solve would need a row interchange (dt/2 |H| too large for the "
                        "structured kind); use QOC_KIND_DENSE");
+  if (flags & 2)
+    fail(QOC_ERUNTIME, "bit-flip Cayley solve would not converge (dt/2 sum_i |V_i(u)| >= 1/2)");
 }
 
 // Launch wrapper: counts launches and, when profiling, brackets each launch with events.
@@ -535,7 +537,10 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
     if (rec_cap < cfg->max_outer + 1) fail(QOC_EINVAL, "rec_cap must be >= max_outer + 1");
     const std::vector<int> node = decomposition(p->steps, cfg->subintervals, cfg->partition, cfg->node_index);
     const int L = cfg->subintervals, B = p->batch, C = p->channels, K = p->steps;
-    const bool direct = cfg->plan == QOC_PLAN_DIRECT;
+    // The bit-flip kind never forms its d x d one-step matrices (16 MB each at d = 1024): its
+    // boundary refresh always runs as direct node sweeps, which agree with the assembled
+    // chain to rounding (ism_test.cpp:248-265).
+    const bool direct = cfg->plan == QOC_PLAN_DIRECT || p->kind == QOC_KIND_BITFLIP;
     const bool assembled_interp = L > 1 && !split && !direct;
     cudaStream_t st = ctx->stream;
     Launcher launch{ctx};
@@ -763,6 +768,8 @@ int32_t qoc_assemble_propagator(qoc_ctx* ctx, const qoc_problem_v1* p, const dou
     if (!u || !prop_out) fail(QOC_EINVAL, "null argument");
     if (p->kind == QOC_KIND_STRANG)
       fail(QOC_ELOGIC, "no dense one-step matrices to assemble for this propagator kind");
+    if (p->kind == QOC_KIND_BITFLIP)
+      fail(QOC_ELOGIC, "the bit-flip kind does not assemble d x d propagators; use QOC_KIND_DENSE");
     DeviceProblem dp;
     DeviceRun dr;
     single_run(ctx, p, u, M_ASSEMBLE, QOC_FORM_TRACKING, true, false, dp, dr);

@@ -55,7 +55,7 @@ __device__ __forceinline__ void bands_at(const TriView& T, const double* u, int 
 // x <- (I + sH)^-1 (I - sH) x,  s = (0, sh); x holds d <= TD entries.
 // Returns false when partial pivoting would have interchanged rows.
 template <int TD>
-__device__ __forceinline__ bool cayley_tri(const TriView& T, const double* u, double sh, double2 (&x)[TD]) {
+__device__ __forceinline__ bool cayley_tri_inl(const TriView& T, const double* u, double sh, double2 (&x)[TD]) {
   const int d = T.d;
   double2 uinv[TD];
   bool ok = true;
@@ -105,6 +105,14 @@ __device__ __forceinline__ bool cayley_tri(const TriView& T, const double* u, do
     }
   }
   return ok;
+}
+
+// Out-of-line copy for the multi-sweep task/horizon kernels: inlining the unrolled solve at
+// every call site made ptxas time explode; the state round-trips through local memory
+// (L1-resident) there, while the hot assembly sweep below keeps the inlined form.
+template <int TD>
+__device__ __noinline__ bool cayley_tri(const TriView& T, const double* u, double sh, double2 (&x)[TD]) {
+  return cayley_tri_inl<TD>(T, u, sh, x);
 }
 
 // Im sum_i conj(cs_i) (dH/du_c ps)_i with ps_i = p0[i] + p1[i] read from the trajectory.
@@ -372,7 +380,7 @@ __global__ void __launch_bounds__(32) tri_pc_assemble_kernel(DevProblem P, DevRu
     for (int i = 0; i < TD; ++i)
       if (i < d) Pc[(size_t)i * d + lane] = x[i];
   for (int j = 0; j < len; ++j) {
-    ok &= cayley_tri<TD>(T, u + (size_t)j * C, half, x);
+    ok &= cayley_tri_inl<TD>(T, u + (size_t)j * C, half, x);
     if (col) {
       double2* dst = Pc + (size_t)(j + 1) * dd;
 #pragma unroll

@@ -1,0 +1,62 @@
+"""Device parity, bit-flip spin registers (QOC_KIND_BITFLIP, BASELINE config 3): the sm_100a
+Neumann/Jacobi Cayley kernels vs the CPU oracle (structured arithmetic, itself pinned against
+the dense-LU reference arithmetic in test_oracle_kats.py)."""
+import numpy as np
+import pytest
+
+from paper_1603_01237_b200 import ism as I
+from paper_1603_01237_b200 import problems
+from tests import oracle_api as O
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)
+
+
+# nspins 5..12 cover every amplitudes-per-thread instantiation (E = 1, 2, 4, 8, 16)
+@pytest.mark.parametrize("nspins", [5, 8, 9, 10, 11, 12])
+def test_propagate_and_gradient(ctx, nspins):
+    w = problems.ising10(nspins=nspins, steps=24, T=0.18)
+    u = w.u0
+    fin = I.propagate_final(w.problem, u, ctx)
+    ref = O.propagate_final(w.problem, u, O.STRUCTURED)
+    assert np.max(np.abs(fin - ref)) < 1e-13
+    for form in ("overlap", "tracking"):
+        v, g = I.objective_gradient(w.problem, u, form, ctx=ctx)
+        vr, gr = O.objective_gradient(w.problem, u, form, arith=O.STRUCTURED)
+        assert abs(v[0] - vr[0]) < 1e-13
+        assert np.max(np.abs(g - gr)) < 1e-13
+
+
+def test_matches_dense_lu_reference_arithmetic(ctx):
+    w = problems.ising10(nspins=6, steps=30, T=0.3)
+    fin = I.propagate_final(w.problem, w.u0, ctx)
+    ref = O.propagate_final(w.problem, w.u0, O.REFERENCE)  # Eigen-style dense partial-pivot LU
+    assert np.max(np.abs(fin - ref)) < 1e-13
+
+
+@pytest.mark.parametrize("parts,plan", [(1, "assembled"), (4, "assembled"), (7, "direct"), (16, "direct")])
+def test_run_ism_small_register(ctx, parts, plan):
+    w = problems.ising10(nspins=6, steps=64, T=0.5, iterations=4, subintervals=parts, rho=2.0)
+    w.config.plan = plan
+    g = I.run_ism(w.problem, w.u0, w.config, w.solver, ctx)
+    r = O.ism_run(w.problem, w.u0, w.config, w.solver, O.STRUCTURED)[0]
+    assert rel(g.control, r.control) < 1e-11
+    assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-11
+    for a, b in zip(g.record.iterations[1:], r.record.iterations[1:]):
+        assert abs(a.error - b.error) < 1e-10 * max(1.0, abs(b.error))
+
+
+@pytest.mark.slow
+def test_ising10_config3_iterations(ctx):
+    # BASELINE config 3 at full size (d = 1024, K = 4000, L = 256), a few iterations
+    for rho_fast in (False, True):
+        w = problems.ising10(iterations=2)
+        if rho_fast:
+            w.solver.step_size = w.rho_fast
+        g = I.run_ism(w.problem, w.u0, w.config, w.solver, ctx)
+        r = O.ism_run(w.problem, w.u0, w.config, w.solver, O.STRUCTURED)[0]
+        assert rel(g.control, r.control) < 1e-9
+        assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-10
