@@ -223,7 +223,7 @@ void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaS
     case QOC_KIND_STRANG: {
       if (!p->kinetic || !p->grid_x) fail(QOC_EINVAL, "condensate model needs kinetic/grid");
       if (C != 1) fail(QOC_EINVAL, "single control channel expected");
-      if (d > 4096) fail(QOC_ELOGIC, "split-step device kernels support d <= 4096");
+      if (d > 2048) fail(QOC_ELOGIC, "split-step device kernels support d <= 2048");
       const bool pow2 = (d & (d - 1)) == 0;
       if (!pow2 && d > 256) fail(QOC_ELOGIC, "split-step device kernels need a power-of-two grid above 256 points");
       // kinetic_half_phase (propagation.cpp:33-40): polar(1, sign * 0.5 * dt * k)

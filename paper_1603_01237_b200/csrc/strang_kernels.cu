@@ -1,0 +1,395 @@
+// strang_kernels.cu — split-step (Strang) condensate kernels (QOC_KIND_STRANG; BASELINE
+// config 4, the 1024-point Gross-Pitaevskii lattice, and the reference's 50-point trap preset).
+//
+// One CTA of 256 threads per (problem, subinterval) task.  The state and three work vectors
+// live in shared memory; every kinetic half step is
+//     spectral(psi, phase) = idft(phase . dft(psi))          (propagation.cpp:27-31)
+// evaluated as two unnormalised transforms with the 1/n of the two unitary 1/sqrt(n) factors
+// folded into the phase multiply.  Powers of two use an in-place radix-2 decimation-in-time
+// FFT in shared memory (bit-reversed scatter fused with the phase multiply, twiddles staged
+// once per CTA); other sizes (<= 256 points, e.g. the reference's 50-point preset) use the
+// direct O(n^2) sum of linalg.cpp:37-50 against a precomputed DFT matrix.
+//
+// Forward step (strang_step, propagation.cpp:131-139): kinetic half phase, potential +
+// kappa |psi_a|^2 phase, kinetic half phase.  Backward stage (strang_backward_stage,
+// propagation.cpp:146-170): recompute the midpoint from the stored forward state psi_j,
+// chi_b = kinetic-adjoint(chi_{j+1}), the real-linear transpose
+//     chi_a = conj(p) chi_b + q conj(chi_b),  p = flow (1 - i dt kappa |psi_a|^2),
+//     q = -i dt kappa flow psi_a^2
+// (or conj(flow) chi_b for the naive adjoint), chi_j = kinetic-adjoint(chi_a), and the
+// gradient dt dx Im sum conj(chi_b) dV/du psi_b (objective.cpp:72-84).  The forward
+// trajectory of a task lives in HBM (R.traj); node sweeps over the whole horizon reuse the
+// problem's trajectory workspace (L * traj_len >= K + 1 states).
+#include <math.h>
+
+#include "../../include/qoc_gpu.h"
+#include "kernels.h"
+
+namespace qoc {
+
+namespace {
+
+constexpr int ST_T = 256;
+constexpr int ST_MAXD = 2048;
+
+struct StrangCtx {
+  int d, log2d;
+  bool pow2;
+  double inv_n;
+  const double2* tw;     // smem [d/2] (pow2) -- exp(-2 pi i k / d)
+  const double2* dftm;   // global [d][d] (direct DFT)
+  double2 *A, *B, *S, *Q;  // smem work vectors [d]
+  double* red;           // smem [ST_T / 32]
+};
+
+// dst = DFT_sign(pre . src) unnormalised (sign -1 forward, +1 inverse); pre may be null.
+// src and dst are distinct shared-memory vectors.  Ends with a __syncthreads.
+__device__ void transform(const StrangCtx& X, const double2* src, double2* dst, int sign, const double2* pre,
+                          double scale) {
+  const int d = X.d, t = threadIdx.x;
+  if (X.pow2) {
+    for (int i = t; i < d; i += ST_T) {
+      double2 v = src[i];
+      if (pre) v = cmul(v, pre[i]);
+      if (scale != 1.0) v = cscale(v, scale);
+      const int r = X.log2d ? (int)(__brev((unsigned)i) >> (32 - X.log2d)) : 0;
+      dst[r] = v;
+    }
+    __syncthreads();
+    for (int s = 1; s <= X.log2d; ++s) {
+      const int half = 1 << (s - 1);
+      const int tstride = d >> s;  // twiddle index step for this stage
+      for (int q = t; q < (d >> 1); q += ST_T) {
+        const int k = q & (half - 1);
+        const int i0 = ((q >> (s - 1)) << s) + k;
+        const int i1 = i0 + half;
+        double2 w = X.tw[k * tstride];
+        if (sign > 0) w.y = -w.y;
+        const double2 lo = dst[i0];
+        const double2 hi = cmul(w, dst[i1]);
+        dst[i0] = cadd(lo, hi);
+        dst[i1] = csub(lo, hi);
+      }
+      __syncthreads();
+    }
+  } else {
+    for (int k = t; k < d; k += ST_T) {
+      double2 acc = cx(0.0, 0.0);
+      const double2* row = X.dftm + (size_t)k * d;
+      for (int m = 0; m < d; ++m) {
+        double2 v = src[m];
+        if (pre) v = cmul(v, pre[m]);
+        double2 w = row[m];
+        if (sign > 0) w.y = -w.y;
+        acc = cfma(v, w, acc);
+      }
+      dst[k] = scale != 1.0 ? cscale(acc, scale) : acc;
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ double block_sum(const StrangCtx& X, double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) X.red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < ST_T / 32; ++w) s += X.red[w];
+  return s;
+}
+
+// V(x_i, u) and dV/du (models.cpp:95-127; cos^2 lattice of BASELINE config 4)
+__device__ __forceinline__ double potential(const DevProblem& P, double x, double u) {
+  if (P.potential == QOC_POT_TRAP) {
+    const double ld = u * P.pp[0];
+    const double ax = fabs(x);
+    if (ax > 0.25 * ld) {
+      const double r = ax - 0.5 * ld;
+      return 0.5 * r * r;
+    }
+    return 0.5 * (0.125 * ld * ld - x * x);
+  }
+  const double cs = cos(P.pp[2] * (x - u));
+  return 0.5 * P.pp[0] * x * x + P.pp[1] * cs * cs;
+}
+__device__ __forceinline__ double potential_du(const DevProblem& P, double x, double u) {
+  if (P.potential == QOC_POT_TRAP) {
+    const double dd = P.pp[0], ld = u * dd;
+    const double ax = fabs(x);
+    return (ax > 0.25 * ld) ? -0.5 * dd * (ax - 0.5 * ld) : 0.125 * u * dd * dd;
+  }
+  return P.pp[1] * P.pp[2] * sin(2.0 * P.pp[2] * (x - u));
+}
+
+// psi (in X.A) -> strang_step(psi); uses B, S.
+__device__ void strang_forward(const StrangCtx& X, const DevProblem& P, double u, double dt) {
+  transform(X, X.A, X.B, -1, nullptr, 1.0);
+  transform(X, X.B, X.S, +1, P.kin_fwd, X.inv_n);  // psi_a
+  for (int i = threadIdx.x; i < X.d; i += ST_T) {
+    const double2 pa = X.S[i];
+    const double w = potential(P, P.grid_x[i], u) + P.kappa * cabs2(pa);
+    double s, c;
+    sincos(-dt * w, &s, &c);
+    X.S[i] = cmul(cx(c, s), pa);  // psi_b
+  }
+  __syncthreads();
+  transform(X, X.S, X.B, -1, nullptr, 1.0);
+  transform(X, X.B, X.A, +1, P.kin_fwd, X.inv_n);
+}
+
+// chi_{j+1} (in X.A), psi_j (in X.Q) -> chi_j (in X.A); returns Im sum conj(chi_b) dV psi_b.
+__device__ double strang_backward(const StrangCtx& X, const DevProblem& P, double u, double dt, bool naive,
+                                  bool want_grad) {
+  const int d = X.d;
+  transform(X, X.Q, X.B, -1, nullptr, 1.0);
+  transform(X, X.B, X.S, +1, P.kin_fwd, X.inv_n);  // psi_a in S
+  transform(X, X.A, X.B, -1, nullptr, 1.0);
+  transform(X, X.B, X.A, +1, P.kin_adj, X.inv_n);  // chi_b in A
+  double g = 0.0;
+  for (int i = threadIdx.x; i < d; i += ST_T) {
+    const double2 pa = X.S[i], cb = X.A[i];
+    const double xi = P.grid_x[i];
+    const double dens = cabs2(pa);
+    const double w = potential(P, xi, u) + P.kappa * dens;
+    double s, c;
+    sincos(-dt * w, &s, &c);
+    const double2 flow = cx(c, s);
+    const double2 pb = cmul(flow, pa);
+    if (want_grad) g += potential_du(P, xi, u) * cconjmul(cb, pb).y;
+    double2 ca;
+    if (naive) {
+      ca = cconjmul(flow, cb);
+    } else {
+      const double kd = dt * P.kappa;
+      const double2 p = cmul(flow, cx(1.0, -kd * dens));           // flow (1 - i dt kappa dens)
+      const double2 q = cmul(cx(0.0, -kd), cmul(flow, cmul(pa, pa)));  // -i dt kappa flow pa^2
+      ca = cadd(cconjmul(p, cb), cmul(q, cconj(cb)));
+    }
+    X.B[i] = ca;
+  }
+  __syncthreads();
+  transform(X, X.B, X.S, -1, nullptr, 1.0);
+  transform(X, X.S, X.A, +1, P.kin_adj, X.inv_n);
+  return want_grad ? block_sum(X, g) : 0.0;
+}
+
+__device__ __forceinline__ StrangCtx make_ctx(const DevProblem& P, unsigned char* smem) {
+  StrangCtx X;
+  const int d = P.d;
+  X.d = d;
+  X.pow2 = (d & (d - 1)) == 0;
+  X.log2d = X.pow2 ? __ffs(d) - 1 : 0;
+  X.inv_n = 1.0 / (double)d;
+  double2* base = reinterpret_cast<double2*>(smem);
+  X.A = base;
+  X.B = base + d;
+  X.S = base + 2 * d;
+  X.Q = base + 3 * d;
+  double2* tw = base + 4 * d;
+  X.dftm = P.twiddle;
+  if (X.pow2) {
+    for (int k = threadIdx.x; k < d / 2; k += ST_T) tw[k] = P.twiddle[k];
+    X.tw = tw;
+    X.red = reinterpret_cast<double*>(tw + (d / 2 > 0 ? d / 2 : 1));
+  } else {
+    X.tw = nullptr;
+    X.red = reinterpret_cast<double*>(tw);
+  }
+  __syncthreads();
+  return X;
+}
+
+size_t strang_smem(int d) {
+  const bool pow2 = (d & (d - 1)) == 0;
+  return sizeof(double2) * (4 * (size_t)d + (pow2 ? (d / 2 > 0 ? d / 2 : 1) : 0)) + sizeof(double) * (ST_T / 32);
+}
+
+__device__ __forceinline__ void load_vec(double2* dst, const double2* src, int d) {
+  for (int i = threadIdx.x; i < d; i += ST_T) dst[i] = src[i];
+  __syncthreads();
+}
+__device__ __forceinline__ void store_vec(double2* dst, const double2* src, int d) {
+  for (int i = threadIdx.x; i < d; i += ST_T) dst[i] = src[i];
+}
+
+__global__ void __launch_bounds__(ST_T) strang_task_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done) {
+  const int n = blockIdx.x, b = blockIdx.y;
+  if (ignore_done ? R.status[b] : R.done[b]) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const StrangCtx X = make_ctx(P, smem);
+  const int d = P.d, t = threadIdx.x;
+  const int node0 = P.node[n], len = P.node[n + 1] - node0;
+  const double Kd = (double)P.K;
+  const double weight = A.weighted ? Kd / (double)len : 1.0;
+  const double scale = (double)len / Kd;
+  const double dt = P.dt, w = P.ip_w;
+  const bool naive = (A.mode & (1 << 10)) != 0;
+  double* u = R.u + ((size_t)b * P.K + node0);  // C == 1
+  double2* traj = R.traj + ((size_t)b * P.L + n) * (size_t)R.traj_len * d;
+  const size_t tix = ((size_t)b * P.L + n) * d;
+  const int mode = A.mode;
+
+  auto forward = [&](bool rec, double* pen) {  // state in X.A
+    if (rec) store_vec(traj, X.A, d);
+    for (int j = 0; j < len; ++j) {
+      strang_forward(X, P, u[j], dt);
+      if (rec) store_vec(traj + (size_t)(j + 1) * d, X.A, d);
+      if (pen) *pen += (P.alpha[node0 + j] * scale) * (u[j] * u[j]);
+    }
+  };
+  // adjoint from the seed in X.A along the stored trajectory; act(j, uold, g)
+  auto adjoint = [&](bool grad, auto&& act) {
+    for (int j = len - 1; j >= 0; --j) {
+      const double uold = u[j];
+      __syncthreads();
+      for (int i = t; i < d; i += ST_T) X.Q[i] = traj[(size_t)j * d + i];
+      __syncthreads();
+      const double im = strang_backward(X, P, uold, dt, naive, grad);
+      const double g = -(P.alpha[node0 + j] * scale) * dt * uold + dt * (w * im);
+      act(j, uold, g);
+    }
+  };
+  auto seed = [&](int form) {  // adjoint_seed (objective.cpp:31-34), from the final state in A
+    for (int i = t; i < d; i += ST_T) {
+      const double2 tg = R.task_targ[tix + i];
+      X.A[i] = form == 0 ? tg : csub(tg, X.A[i]);
+    }
+    __syncthreads();
+  };
+
+  if (mode & (M_ENTRY | M_UPDATE | M_FINAL | M_GRAD)) {
+    const bool need_traj = (mode & (M_UPDATE | M_GRAD)) != 0;
+    const int iters = (mode & M_UPDATE) ? A.inner : 1;
+    for (int it = 0; it < iters; ++it) {
+      load_vec(X.A, R.task_init + tix, d);
+      double pen = 0.0;
+      forward(need_traj, &pen);
+      if (it == 0 && (mode & M_ENTRY)) {
+        double s = 0.0;
+        for (int i = t; i < d; i += ST_T) {
+          const double2 tg = R.task_targ[tix + i];
+          s += A.form == 0 ? cconjmul(tg, X.A[i]).x : cabs2(csub(X.A[i], tg));
+        }
+        s = block_sum(X, s);
+        const double payoff = A.form == 0 ? (w * s) : (-0.5 * (w * s));
+        if (t == 0) R.entry[(size_t)b * P.L + n] = weight * (payoff - 0.5 * dt * pen);
+      }
+      if (it == 0 && (mode & M_FINAL)) store_vec(R.psi_end + tix, X.A, d);
+      if (mode & (M_UPDATE | M_GRAD)) {
+        __syncthreads();
+        seed(A.form);
+        adjoint(true, [&](int j, double uold, double g) {
+          if (t == 0) {
+            if (mode & M_GRAD) R.grad[(size_t)b * P.K + node0 + j] = g;
+            if (mode & M_UPDATE) u[j] = uold + A.rho * (weight * g);
+          }
+          __syncthreads();
+        });
+      }
+    }
+  }
+  if (mode & M_ERROR) {
+    __syncthreads();
+    load_vec(X.A, R.task_init + tix, d);
+    forward(true, nullptr);
+    __syncthreads();
+    seed(A.form);
+    double err = 0.0;
+    adjoint(true, [&](int, double, double g) { err += fabs(g); });
+    if (t == 0) R.err[(size_t)b * P.L + n] = err;
+  }
+  if (mode & M_LAGGED) {  // ism.cpp:424-459 (strang branch): trajectory from psi_nodes[n]
+    __syncthreads();
+    load_vec(X.A, R.psi_nodes + ((size_t)b * (P.L + 1) + n) * d, d);
+    forward(true, nullptr);
+    __syncthreads();
+    store_vec(R.psi_end + tix, X.A, d);
+    __syncthreads();
+    load_vec(X.A, R.chi_nodes + ((size_t)b * (P.L + 1) + n + 1) * d, d);
+    adjoint(false, [&](int, double, double) {});
+    __syncthreads();
+    store_vec(R.chi_start + tix, X.A, d);
+  }
+}
+
+// node_sweeps (ism.cpp:35-84; strang: forward trajectory kept for the nonlinear adjoint) and
+// the exact payoff (which = 1).  One CTA per problem; the trajectory uses the problem's task
+// workspace (L * traj_len >= K + 1 states).
+__global__ void __launch_bounds__(ST_T) strang_horizon_kernel(DevProblem P, DevRun R, int which, int k) {
+  const int b = blockIdx.x;
+  if (R.done[b] || R.status[b]) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const StrangCtx X = make_ctx(P, smem);
+  const int d = P.d, t = threadIdx.x;
+  const double dt = P.dt;
+  const double* u = R.u + (size_t)b * P.K;
+  double2* traj = R.traj + (size_t)b * P.L * R.traj_len * d;
+  const size_t nb = (size_t)b * (P.L + 1) * d;
+  load_vec(X.A, P.init + (size_t)b * d, d);
+  if (which == 0) {
+    store_vec(R.psi_nodes + nb, X.A, d);
+    store_vec(traj, X.A, d);
+  }
+  int nxt = 1;
+  for (int j = 0; j < P.K; ++j) {
+    strang_forward(X, P, u[j], dt);
+    if (which == 0) {
+      store_vec(traj + (size_t)(j + 1) * d, X.A, d);
+      if (nxt <= P.L && P.node[nxt] == j + 1) {
+        store_vec(R.psi_nodes + nb + (size_t)nxt * d, X.A, d);
+        ++nxt;
+      }
+    }
+  }
+  if (which == 1) {
+    double s = 0.0;
+    for (int i = t; i < d; i += ST_T) s += cconjmul(P.targ[(size_t)b * d + i], X.A[i]).x;
+    s = block_sum(X, s);
+    if (t == 0) {
+      double pen = 0.0;
+      for (int n = 0; n < P.L; ++n) pen += R.pen[(size_t)b * P.L + n];
+      R.rec_exact[(size_t)b * R.cap + k] = P.ip_w * s - 0.5 * P.dt * pen;
+    }
+    return;
+  }
+  __syncthreads();
+  load_vec(X.A, P.targ + (size_t)b * d, d);
+  store_vec(R.chi_nodes + nb + (size_t)P.L * d, X.A, d);
+  int prev = P.L - 1;
+  for (int j = P.K - 1; j >= 0; --j) {
+    __syncthreads();
+    for (int i = t; i < d; i += ST_T) X.Q[i] = traj[(size_t)j * d + i];
+    __syncthreads();
+    strang_backward(X, P, u[j], dt, false, false);
+    if (prev >= 0 && P.node[prev] == j) {
+      store_vec(R.chi_nodes + nb + (size_t)prev * d, X.A, d);
+      --prev;
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t strang_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
+  if (A.mode & M_ASSEMBLE) return cudaErrorNotSupported;
+  if (P.C != 1 || P.d > ST_MAXD) return cudaErrorNotSupported;
+  const size_t smem = strang_smem(P.d);
+  cudaError_t e = cudaFuncSetAttribute(strang_task_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  strang_task_kernel<<<dim3(P.L, P.B), ST_T, smem, st>>>(P, R, A, ignore_done);
+  return cudaGetLastError();
+}
+
+cudaError_t strang_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
+  if (P.C != 1 || P.d > ST_MAXD) return cudaErrorNotSupported;
+  const size_t smem = strang_smem(P.d);
+  cudaError_t e = cudaFuncSetAttribute(strang_horizon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  strang_horizon_kernel<<<P.B, ST_T, smem, st>>>(P, R, which, k);
+  return cudaGetLastError();
+}
+
+}  // namespace qoc

@@ -2,6 +2,4 @@
 #include "kernels.h"
 
 namespace qoc {
-cudaError_t strang_task(const DevProblem&, const DevRun&, const TaskArgs&, int, cudaStream_t) { return cudaErrorNotSupported; }
-cudaError_t strang_horizon(const DevProblem&, const DevRun&, int, int, cudaStream_t) { return cudaErrorNotSupported; }
 }  // namespace qoc

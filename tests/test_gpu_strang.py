@@ -1,0 +1,89 @@
+"""Device parity, split-step condensates (QOC_KIND_STRANG, BASELINE config 4 and the
+reference's condensate preset): the sm_100a shared-memory FFT kernels vs the CPU oracle."""
+import numpy as np
+import pytest
+
+from paper_1603_01237_b200 import abi
+from paper_1603_01237_b200 import ism as I
+from paper_1603_01237_b200 import problems
+from paper_1603_01237_b200.models import CondensateModel
+from tests import oracle_api as O
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)
+
+
+def lattice_problem(points, steps=16, T=0.05, seed=7):
+    m = CondensateModel(points, -16.0, 16.0, abi.POT_LATTICE, [1.0, 5.0, 1.0], 10.0)
+    rng = np.random.default_rng(seed)
+    psi = np.exp(-0.5 * m.x ** 2) * (1 + 0.1 * rng.standard_normal(points)) + 0j
+    psi /= np.sqrt(m.dx) * np.linalg.norm(psi)
+    tgt = psi * m.x
+    tgt /= np.sqrt(m.dx) * np.linalg.norm(tgt)
+    grid = I.TimeGrid.over(0.0, T, steps)
+    u = 0.3 * rng.standard_normal((1, steps))
+    return I.ControlProblem(m, grid, psi, tgt.astype(complex), np.full(steps, 0.01)), u
+
+
+@pytest.mark.parametrize("which", ["fixture24", "lattice64", "lattice1024", "lattice2048"])
+def test_propagate_and_gradient(ctx, which):
+    if which == "fixture24":  # direct DFT path (non power of two), trap potential
+        p, u = O.strang_fixture(31)
+    else:
+        p, u = lattice_problem(int(which[7:]))
+    fin = I.propagate_final(p, u, ctx)
+    ref = O.propagate_final(p, u)
+    assert np.max(np.abs(fin - ref)) < 1e-12
+    for naive in (False, True):
+        for form in ("overlap", "tracking"):
+            v, g = I.objective_gradient(p, u, form, naive=naive, ctx=ctx)
+            vr, gr = O.objective_gradient(p, u, form, naive=naive)
+            assert abs(v[0] - vr[0]) < 1e-12
+            assert np.max(np.abs(g - gr)) < 1e-11 * max(1.0, np.max(np.abs(gr)))
+
+
+@pytest.mark.parametrize("parts", [1, 4, 7])
+def test_split_run_matches_oracle(ctx, parts):
+    p, u = O.strang_fixture(3000)
+    cfg = I.IsmConfig(subintervals=parts, max_outer=5, eta=0.0, variant="split", log_exact_objective=True)
+    sv = I.SolverSpec(step_size=0.3)
+    g = I.run_ism(p, u, cfg, sv, ctx)
+    r = O.ism_run(p, u, cfg, sv)[0]
+    assert rel(g.control, r.control) < 1e-10
+    assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-10
+    for a, b in zip(g.record.iterations[1:], r.record.iterations[1:]):
+        assert abs(a.exact_objective - b.exact_objective) < 1e-10
+        assert abs(a.error - b.error) < 1e-9 * max(1.0, abs(b.error))
+
+
+def test_kat8_condensate_preset_on_device(ctx):
+    # acceptance_main.cpp:439-485: 10 iterations, N = 4, rho = 0.1 -> exact payoff >= -0.742728295
+    w = problems.condensate_preset(subintervals=4, iterations=10)
+    v0 = I.evaluate_objective(w.problem, w.u0, "overlap", ctx)[0]
+    g = I.run_ism(w.problem, w.u0, w.config, w.solver, ctx)
+    pay = [it.exact_objective for it in g.record.iterations if it.exact_objective is not None]
+    assert len(pay) == 10
+    prev = v0
+    for v in pay:
+        assert v > prev
+        prev = v
+    assert pay[-1] >= -0.742728295 - 1e-6
+    r = O.ism_run(w.problem, w.u0, w.config, w.solver)[0]
+    assert rel(g.control, r.control) < 1e-9
+
+
+@pytest.mark.slow
+def test_gpe1024_config4(ctx):
+    # BASELINE config 4 at full size (1024 points, K = 10000, L = 64), two iterations
+    w = problems.gpe1024(iterations=2)
+    w.solver.step_size = w.rho_fast
+    g = I.run_ism(w.problem, w.u0, w.config, w.solver, ctx)
+    r = O.ism_run(w.problem, w.u0, w.config, w.solver)[0]
+    assert rel(g.control, r.control) < 1e-9
+    assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-10
+    ex_g = [it.exact_objective for it in g.record.iterations[1:]]
+    ex_r = [it.exact_objective for it in r.record.iterations[1:]]
+    assert np.max(np.abs(np.array(ex_g) - np.array(ex_r))) < 1e-10
