@@ -357,11 +357,28 @@ __global__ void __launch_bounds__(32) tridiag_horizon_kernel(DevProblem P, DevRu
   if (!ok && R.err_flags) atomicOr(R.err_flags, 1);
 }
 
-// Assembly sweep of the propagator cache (pcache.cu): lane k carries column k of P_j.
+// Assembly sweep of the propagator cache (pcache.cu): P_{j+1} = C_j P_j, lane k carries
+// column k of P_j.  The LU factors of B_j = I + s H(u_j) depend on u_j only, so they are
+// computed step-parallel (lane q factors step j0 + q of a 32-step chunk, into shared memory)
+// and the sequential sweep over j only applies the factored solve: per step and column one
+// tridiagonal matvec (I - sH) x, one forward and one backward substitution -- no band
+// recomputation and no global loads on the dependent chain.
+constexpr int TRI_CHUNK = 32;
+
+template <int TD>
+struct TriFactors {
+  double dg[TRI_CHUNK][TD];       // H(u_j) diagonal
+  double2 sb[TRI_CHUNK][TD + 1];  // H(u_j) entry (i, i-1); row d (and 0) zero
+  double2 lf[TRI_CHUNK][TD];      // elimination multipliers l_i = a_i / u_{i-1}
+  double2 ui[TRI_CHUNK][TD];      // 1 / u_i
+};
+
 template <int TD>
 __global__ void __launch_bounds__(32) tri_pc_assemble_kernel(DevProblem P, DevRun R, int ignore_done) {
   const int n = blockIdx.x, b = blockIdx.y, lane = threadIdx.x;
   if (ignore_done ? R.status[b] : R.done[b]) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TriFactors<TD>& F = *reinterpret_cast<TriFactors<TD>*>(smem_raw);
   const int d = P.d, C = P.C;
   const int nops = 1 + C + (P.has_quad ? C : 0);
   const TriView T{P.tri_diag + (size_t)b * nops * d, P.tri_sub + (size_t)b * nops * (d - 1), d, C, P.has_quad};
@@ -379,13 +396,68 @@ __global__ void __launch_bounds__(32) tri_pc_assemble_kernel(DevProblem P, DevRu
 #pragma unroll
     for (int i = 0; i < TD; ++i)
       if (i < d) Pc[(size_t)i * d + lane] = x[i];
-  for (int j = 0; j < len; ++j) {
-    ok &= cayley_tri_inl<TD>(T, u + (size_t)j * C, half, x);
-    if (col) {
-      double2* dst = Pc + (size_t)(j + 1) * dd;
+  for (int j0 = 0; j0 < len; j0 += TRI_CHUNK) {
+    const int cnt = min(TRI_CHUNK, len - j0);
+    __syncwarp();
+    if (lane < cnt) {  // factor B_j = I + sH(u_j), s = i*half (oracle.cpp TriM::cayley)
+      const double* uj = u + (size_t)(j0 + lane) * C;
+      double2 uinv_prev = cx(0.0, 0.0);
+      for (int i = 0; i < d; ++i) {
+        double dg;
+        double2 sb;
+        bands_at(T, uj, i, dg, sb);
+        F.dg[lane][i] = dg;
+        F.sb[lane][i] = sb;
+        double2 ui = cx(1.0, half * dg);
+        double2 lf = cx(0.0, 0.0);
+        if (i > 0) {
+          const double2 a = cx(-half * sb.y, half * sb.x);      // s sb_i
+          ok = ok && !(cabs2(a) * cabs2(uinv_prev) > 1.0);     // |a_i| > |u_{i-1}| would pivot
+          lf = cmul(a, uinv_prev);
+          ui = cfms(lf, cx(half * sb.y, half * sb.x), ui);     // - l_i * s conj(sb_i)
+        }
+        uinv_prev = crcp(ui);
+        F.lf[lane][i] = lf;
+        F.ui[lane][i] = uinv_prev;
+      }
+      F.sb[lane][d] = cx(0.0, 0.0);
+    }
+    __syncwarp();
+    for (int q = 0; q < cnt; ++q) {
+      const double* fdg = F.dg[q];
+      const double2* fsb = F.sb[q];
+      const double2* flf = F.lf[q];
+      const double2* fui = F.ui[q];
+      double2 r[TD];
 #pragma unroll
-      for (int i = 0; i < TD; ++i)
-        if (i < d) dst[(size_t)i * d + lane] = x[i];
+      for (int i = 0; i < TD; ++i) {
+        if (i < d) {
+          const double2 sbi = fsb[i], sbn = fsb[i + 1];
+          double2 h = cx(fdg[i] * x[i].x, fdg[i] * x[i].y);
+          if (i > 0) h = cfma(sbi, x[i - 1], h);
+          if (i + 1 < d) h = cfmaconj(sbn, x[i + 1], h);
+          double2 ri = cx(x[i].x + half * h.y, x[i].y - half * h.x);  // x - s H x
+          if (i > 0) ri = cfms(flf[i], r[i - 1], ri);
+          r[i] = ri;
+        }
+      }
+#pragma unroll
+      for (int i = TD - 1; i >= 0; --i) {
+        if (i < d) {
+          double2 v = r[i];
+          if (i + 1 < d) {
+            const double2 sbn = fsb[i + 1];
+            v = cfms(cx(half * sbn.y, half * sbn.x), x[i + 1], v);  // c_i = s conj(sb_{i+1})
+          }
+          x[i] = cmul(v, fui[i]);
+        }
+      }
+      if (col) {
+        double2* dst = Pc + (size_t)(j0 + q + 1) * dd;
+#pragma unroll
+        for (int i = 0; i < TD; ++i)
+          if (i < d) dst[(size_t)i * d + lane] = x[i];
+      }
     }
   }
   if (col && R.prop) {
@@ -394,17 +466,27 @@ __global__ void __launch_bounds__(32) tri_pc_assemble_kernel(DevProblem P, DevRu
     for (int i = 0; i < TD; ++i)
       if (i < d) M[(size_t)i * d + lane] = x[i];
   }
-  if (!ok && R.err_flags) atomicOr(R.err_flags, 1);
+  ok = __all_sync(0xffffffffu, ok);
+  if (!ok && lane == 0 && R.err_flags) atomicOr(R.err_flags, 1);
 }
 
 }  // namespace
 
 cudaError_t tri_pc_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st) {
   if (P.d > 30) return cudaErrorNotSupported;
-  if (P.d <= 24)
-    tri_pc_assemble_kernel<24><<<dim3(P.L, P.B), 32, 0, st>>>(P, R, ignore_done);
-  else
-    tri_pc_assemble_kernel<32><<<dim3(P.L, P.B), 32, 0, st>>>(P, R, ignore_done);
+  if (P.d <= 24) {
+    auto k = tri_pc_assemble_kernel<24>;
+    const int smem = (int)sizeof(TriFactors<24>);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    k<<<dim3(P.L, P.B), 32, smem, st>>>(P, R, ignore_done);
+  } else {
+    auto k = tri_pc_assemble_kernel<32>;
+    const int smem = (int)sizeof(TriFactors<32>);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    k<<<dim3(P.L, P.B), 32, smem, st>>>(P, R, ignore_done);
+  }
   return cudaGetLastError();
 }
 
