@@ -12,12 +12,14 @@
 // is fixed per step from that a-priori bound (q^(k+1) <= 2^-53) instead of a data-dependent
 // stopping test, so every thread agrees without a reduction.
 //
-// Layout: one CTA of T = min(d, 256) threads per (problem, subinterval) task; thread t holds
-// the E = d/T amplitudes s = t + e*T.  A flip of bit b pairs
-//   b < 5              -> lane t ^ 2^b of the same warp        (shuffle)
-//   5 <= b < log2 T    -> thread t ^ 2^b                        (shared memory, double buffer)
+// Layout: one CTA of T = min(d, 512) threads per (problem, subinterval) task; thread t
+// holds the E = d/T amplitudes s = t + e*T (all compile-time: one instantiation per n).  A flip of bit b pairs
+//   b < log2 T         -> thread t ^ 2^b      (shared memory, double buffer; one LDS.128 per
+//                                               partner -- cheaper than 4 SHFL for a double2)
 //   b >= log2 T        -> register slot e ^ 2^(b - log2 T)     (same thread)
-// so one fixed-point sweep costs one __syncthreads.  Spin i <-> bit n-1-i (spin_operator,
+// so one fixed-point sweep costs one __syncthreads.  d = 1024 runs two amplitudes per
+// thread on 16 warps (98 registers, no spills); the per-spin coefficients of a step live in
+// registers across all its sweeps, so a sweep is n LDS.128 + n complex FMAs per amplitude.  Spin i <-> bit n-1-i (spin_operator,
 // models.cpp:296-318).  The forward trajectory of a task (len+1 states, 16 KB each at
 // d = 1024) lives in HBM/L2 (R.traj); the adjoint sweep reads it back for the gradient.
 #include "kernels.h"
@@ -27,34 +29,7 @@ namespace qoc {
 namespace {
 
 constexpr int BF_MAXN = 12;
-constexpr int BF_T = 256;
-
-struct Geo {
-  int n, log2T, T, t, lane, warp, nwarp;
-};
-
-// Calls f(e, spin, bit_of_s, partner_value) for every amplitude slot e and spin.
-template <int E, int LOG2E, class F>
-__device__ __forceinline__ void for_flips(const Geo& G, const double2 (&v)[E], const double2* buf, F&& f) {
-#pragma unroll
-  for (int hb = 0; hb < LOG2E; ++hb) {
-    const int spin = G.n - 1 - (G.log2T + hb);
-#pragma unroll
-    for (int e = 0; e < E; ++e) f(e, spin, (e >> hb) & 1, v[e ^ (1 << hb)]);
-  }
-  for (int b = 0; b < G.log2T; ++b) {
-    const int spin = G.n - 1 - b;
-    const int m = 1 << b;
-    const int one = (G.t & m) != 0;
-    if (m < 32) {
-#pragma unroll
-      for (int e = 0; e < E; ++e) f(e, spin, one, shfl_xor(v[e], m));
-    } else {
-#pragma unroll
-      for (int e = 0; e < E; ++e) f(e, spin, one, buf[(G.t ^ m) + e * G.T]);
-    }
-  }
-}
+constexpr int BF_T = 512;
 
 // <s| (a sigma^x + b sigma^y) |s ^ m> = a + (bit(s) ? +i : -i) b   (oracle.cpp BitM::offdiag)
 __device__ __forceinline__ double2 flip_coef(double2 ab, int one) { return cx(ab.x, one ? ab.y : -ab.y); }
@@ -66,66 +41,84 @@ struct BfOps {
   int C, n;
 };
 
-// Per-step channel sums (ax_i, ay_i) for spin i, written by threads i < n.
-__device__ __forceinline__ void channel_sums(const BfOps& O, const double* uj, double2* sa) {
-  const int i = threadIdx.x;
-  if (i < O.n) {
-    double ax = 0.0, ay = 0.0;
-    for (int c = 0; c < O.C; ++c) {
-      const double g = uj[c] * O.coef[c * O.n + i];
-      if (O.axis[c] == 0) ax += g;
-      else ay += g;
-    }
-    sa[i] = cx(ax, ay);
-  }
-}
-
-// Sweeps needed for q^(k+1) <= 2^-53; returns -1 when the Neumann series would not contract.
-__device__ __forceinline__ int sweep_count(const double2* sa, int n, double half) {
-  double q = 0.0;
-  for (int i = 0; i < n; ++i) q += sqrt(sa[i].x * sa[i].x + sa[i].y * sa[i].y);
-  q *= half;
-  if (!(q < 0.5)) return -1;
-  if (q <= 0.0) return 0;
-  return (int)ceil(53.0 * 0.6931471805599453 / -log(q));
-}
-
-template <int E, int LOG2E>
+// Everything about the register layout is compile-time: N = log2 d spins, T = 2^LOG2T threads,
+// E = 2^LOG2E amplitudes per thread, so every flip loop unrolls, partner addresses are
+// constant offsets and the per-spin coefficients sit in registers for the whole step.
+template <int LOG2E, int LOG2T>
 struct Bf {
-  Geo G;
-  double dg[E];      // diagonal of H at this thread's amplitudes
-  double2* buf;      // smem [2][d] exchange
-  double2* sa;       // smem [2][BF_MAXN] per-step channel sums (by step parity)
-  double* red;       // smem [BF_T / 32][4] reduction scratch
-  int par = 0;       // exchange buffer parity
-  int spar = 0;      // channel-sum parity
+  static constexpr int E = 1 << LOG2E, T = 1 << LOG2T, N = LOG2E + LOG2T, D = E * T;
+  int t, lane, warp;
+  double dg[E];       // diagonal of H at this thread's amplitudes
+  double2 cl[LOG2T];  // low spins (bit b < LOG2T): coefficient signed for this thread's bit
+  double2 ch[LOG2E > 0 ? LOG2E : 1];  // high spins: raw (ax, ay); the sign is a compile-time function of e
+  double2* buf;       // smem [2][D] exchange
+  double2* sa;        // smem [2][N] per-step channel sums (by step parity)
+  int* ssw;           // smem [2] per-step sweep count
+  double* red;        // smem [T / 32][4] reduction scratch
+  int par = 0, spar = 0;
 
   __device__ void publish(const double2 (&v)[E]) {
     par ^= 1;
-    double2* b = buf + par * (G.T * E);
+    double2* b = buf + par * D;
 #pragma unroll
-    for (int e = 0; e < E; ++e) b[G.t + e * G.T] = v[e];
+    for (int e = 0; e < E; ++e) b[t + e * T] = v[e];
   }
-  __device__ const double2* cur() const { return buf + par * (G.T * E); }
+  __device__ const double2* cur() const { return buf + par * D; }
 
   // V v (after publish(v) + __syncthreads)
-  __device__ void apply_V(const double2 (&v)[E], const double2* s, double2 (&out)[E]) const {
+  __device__ void apply_V(const double2 (&v)[E], double2 (&out)[E]) const {
+    const double2* c = cur();
 #pragma unroll
     for (int e = 0; e < E; ++e) out[e] = cx(0.0, 0.0);
-    for_flips<E, LOG2E>(G, v, cur(), [&](int e, int spin, int one, double2 pv) {
-      out[e] = cfma(flip_coef(s[spin], one), pv, out[e]);
-    });
+#pragma unroll
+    for (int hb = 0; hb < LOG2E; ++hb)
+#pragma unroll
+      for (int e = 0; e < E; ++e) out[e] = cfma(flip_coef(ch[hb], (e >> hb) & 1), v[e ^ (1 << hb)], out[e]);
+#pragma unroll
+    for (int b = 0; b < LOG2T; ++b)
+#pragma unroll
+      for (int e = 0; e < E; ++e) out[e] = cfma(cl[b], c[(t ^ (1 << b)) + e * T], out[e]);
   }
 
-  // x <- (I + sH)^-1 (I - sH) x, s = (0, sh).  Begins with the step's channel sums already
-  // in sa[spar] (see begin_step).  Returns false if the series would not contract.
-  __device__ bool cayley(double2 (&x)[E], double sh, int sweeps) {
-    const double2* s = sa + spar * BF_MAXN;
-    double2 r[E], y[E], vv[E];
+  // Step setup: warp 0 forms the channel sums of u_j and the sweep count (q^(k+1) <= 2^-53,
+  // q = dt/2 sum_i |(ax_i, ay_i)|; -1 if the series would not contract); after the barrier
+  // every thread pulls its signed coefficients into registers.  Returns the sweep count.
+  __device__ int begin_step(const BfOps& O, const double* uj, double half) {
+    spar ^= 1;
+    double2* sa_w = sa + spar * N;
+    if (warp == 0) {
+      double nrm = 0.0;
+      if (lane < N) {
+        double ax = 0.0, ay = 0.0;
+        for (int c = 0; c < O.C; ++c) {
+          const double g = uj[c] * O.coef[c * N + lane];
+          if (O.axis[c] == 0) ax += g;
+          else ay += g;
+        }
+        sa_w[lane] = cx(ax, ay);
+        nrm = sqrt(ax * ax + ay * ay);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, off);
+      if (lane == 0) {
+        const double q = half * nrm;
+        ssw[spar] = !(q < 0.5) ? -1 : (q <= 0.0 ? 0 : (int)ceil(53.0 * 0.6931471805599453 / -log(q)));
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < LOG2T; ++b) cl[b] = flip_coef(sa_w[N - 1 - b], (t >> b) & 1);
+#pragma unroll
+    for (int hb = 0; hb < LOG2E; ++hb) ch[hb] = sa_w[N - 1 - (LOG2T + hb)];
+    return ssw[spar];
+  }
+
+  // x <- (I + sH)^-1 (I - sH) x, s = (0, sh), with the coefficients of begin_step.
+  __device__ void cayley(double2 (&x)[E], double sh, int sweeps) {
+    double2 r[E], y[E], vv[E], inv[E];
     publish(x);
     __syncthreads();
-    apply_V(x, s, vv);
-    double2 inv[E];
+    apply_V(x, vv);
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const double2 hx = cx(fma(dg[e], x[e].x, vv[e].x), fma(dg[e], x[e].y, vv[e].y));
@@ -138,23 +131,15 @@ struct Bf {
     for (int k = 0; k < sweeps; ++k) {
       publish(y);
       __syncthreads();
-      apply_V(y, s, vv);
+      apply_V(y, vv);
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const double2 t = cx(r[e].x + sh * vv[e].y, r[e].y - sh * vv[e].x);  // r - s V y
-        y[e] = cmul(t, inv[e]);
+        const double2 tt = cx(r[e].x + sh * vv[e].y, r[e].y - sh * vv[e].x);  // r - s V y
+        y[e] = cmul(tt, inv[e]);
       }
     }
 #pragma unroll
     for (int e = 0; e < E; ++e) x[e] = y[e];
-    return sweeps >= 0;
-  }
-
-  // Publishes the channel sums of u_j; must be followed by a __syncthreads before use
-  // (cayley's first publish/sync provides it).
-  __device__ void begin_step(const BfOps& O, const double* uj) {
-    spar ^= 1;
-    channel_sums(O, uj, sa + spar * BF_MAXN);
   }
 
   // Deterministic block sum of up to 4 values (fixed warp order).
@@ -164,12 +149,12 @@ struct Bf {
       for (int off = 16; off > 0; off >>= 1) v[q] += __shfl_xor_sync(0xffffffffu, v[q], off);
     }
     __syncthreads();
-    if (G.lane == 0)
-      for (int q = 0; q < nv; ++q) red[G.warp * 4 + q] = v[q];
+    if (lane == 0)
+      for (int q = 0; q < nv; ++q) red[warp * 4 + q] = v[q];
     __syncthreads();
     for (int q = 0; q < nv; ++q) {
       double s = 0.0;
-      for (int w = 0; w < G.nwarp; ++w) s += red[w * 4 + q];
+      for (int w = 0; w < T / 32; ++w) s += red[w * 4 + q];
       v[q] = s;
     }
   }
@@ -178,38 +163,45 @@ struct Bf {
   // ps must be published (and synced) by the caller.
   __device__ void grad_terms(const BfOps& O, const double2 (&cs)[E], const double2 (&ps)[E], double (&out)[4]) {
     double2 acc[4] = {cx(0.0, 0.0), cx(0.0, 0.0), cx(0.0, 0.0), cx(0.0, 0.0)};
-    for_flips<E, LOG2E>(G, ps, cur(), [&](int e, int spin, int one, double2 pv) {
-      for (int c = 0; c < O.C && c < 4; ++c) {
-        const double g = O.coef[c * O.n + spin];
-        const double2 a = O.axis[c] == 0 ? cx(g, 0.0) : flip_coef(cx(0.0, g), one);
-        acc[c] = cfmaconj(cs[e], cmul(a, pv), acc[c]);
+    const double2* c = cur();
+    auto add = [&](int e, int spin, int one, double2 pv) {
+      for (int ch_ = 0; ch_ < O.C && ch_ < 4; ++ch_) {
+        const double g = O.coef[ch_ * N + spin];
+        const double2 a = O.axis[ch_] == 0 ? cx(g, 0.0) : flip_coef(cx(0.0, g), one);
+        acc[ch_] = cfmaconj(cs[e], cmul(a, pv), acc[ch_]);
       }
-    });
-    for (int c = 0; c < 4; ++c) out[c] = acc[c].y;
+    };
+#pragma unroll
+    for (int hb = 0; hb < LOG2E; ++hb)
+#pragma unroll
+      for (int e = 0; e < E; ++e) add(e, N - 1 - (LOG2T + hb), (e >> hb) & 1, ps[e ^ (1 << hb)]);
+#pragma unroll
+    for (int b = 0; b < LOG2T; ++b)
+#pragma unroll
+      for (int e = 0; e < E; ++e) add(e, N - 1 - b, (t >> b) & 1, c[(t ^ (1 << b)) + e * T]);
+    for (int q = 0; q < 4; ++q) out[q] = acc[q].y;
     block_sum(out, O.C < 4 ? O.C : 4);
   }
 };
 
-template <int E, int LOG2E>
-__device__ __forceinline__ Bf<E, LOG2E> make_bf(const DevProblem& P, int b, unsigned char* smem) {
-  Bf<E, LOG2E> F;
-  F.G.n = P.nspins;
-  F.G.T = P.d / E;
-  F.G.log2T = P.nspins - LOG2E;
-  F.G.t = threadIdx.x;
-  F.G.lane = threadIdx.x & 31;
-  F.G.warp = threadIdx.x >> 5;
-  F.G.nwarp = F.G.T >> 5;
+template <int LOG2E, int LOG2T>
+__device__ __forceinline__ Bf<LOG2E, LOG2T> make_bf(const DevProblem& P, int b, unsigned char* smem) {
+  using F_ = Bf<LOG2E, LOG2T>;
+  F_ F;
+  F.t = threadIdx.x;
+  F.lane = threadIdx.x & 31;
+  F.warp = threadIdx.x >> 5;
   F.buf = reinterpret_cast<double2*>(smem);
-  F.sa = F.buf + 2 * P.d;
-  F.red = reinterpret_cast<double*>(F.sa + 2 * BF_MAXN);
+  F.sa = F.buf + 2 * F_::D;
+  F.red = reinterpret_cast<double*>(F.sa + 2 * F_::N);
+  F.ssw = reinterpret_cast<int*>(F.red + (F_::T / 32) * 4);
 #pragma unroll
-  for (int e = 0; e < E; ++e) F.dg[e] = P.bf_diag[(size_t)b * P.d + F.G.t + e * F.G.T];
+  for (int e = 0; e < F_::E; ++e) F.dg[e] = P.bf_diag[(size_t)b * P.d + F.t + e * F_::T];
   return F;
 }
 
 __host__ __device__ constexpr size_t bf_smem(int d) {
-  return sizeof(double2) * (2 * (size_t)d + 2 * BF_MAXN) + sizeof(double) * (BF_T / 32) * 4;
+  return sizeof(double2) * (2 * (size_t)d + 2 * BF_MAXN) + sizeof(double) * (BF_T / 32) * 4 + 2 * sizeof(int);
 }
 
 template <int E>
@@ -223,13 +215,16 @@ __device__ __forceinline__ void store_state(const double2 (&x)[E], double2* dst,
   for (int e = 0; e < E; ++e) dst[t + e * T] = x[e];
 }
 
-template <int E, int LOG2E>
-__global__ void __launch_bounds__(BF_T) bitflip_task_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done) {
+template <int LOG2E, int LOG2T>
+__global__ void __launch_bounds__(1 << LOG2T) bitflip_task_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done) {
+  using F_ = Bf<LOG2E, LOG2T>;
+  constexpr int E = 1 << LOG2E, T = 1 << LOG2T;
+  using Vec = double2[1 << LOG2E];
   const int n = blockIdx.x, b = blockIdx.y;
   if (ignore_done ? R.status[b] : R.done[b]) return;
   extern __shared__ __align__(16) unsigned char smem[];
-  Bf<E, LOG2E> F = make_bf<E, LOG2E>(P, b, smem);
-  const int d = P.d, C = P.C, t = F.G.t, T = F.G.T;
+  F_ F = make_bf<LOG2E, LOG2T>(P, b, smem);
+  const int d = P.d, C = P.C, t = F.t;
   const BfOps O{P.bf_diag + (size_t)b * d, P.bf_coef + (size_t)b * C * P.nspins, P.bf_axis, C, P.nspins};
   const int node0 = P.node[n], len = P.node[n + 1] - node0;
   const double Kd = (double)P.K;
@@ -244,14 +239,13 @@ __global__ void __launch_bounds__(BF_T) bitflip_task_kernel(DevProblem P, DevRun
   double2 x[E], chi[E], cn[E], ps[E], tg[E];
   load_state<E>(tg, R.task_targ + tix, t, T);
 
-  auto step = [&](double2 (&v)[E], const double* uj, double sh) {
-    F.begin_step(O, uj);
-    __syncthreads();
-    const int sweeps = sweep_count(F.sa + F.spar * BF_MAXN, O.n, half);
-    ok &= F.cayley(v, sh, sweeps < 0 ? 0 : sweeps) && sweeps >= 0;
+  auto step = [&](Vec& v, const double* uj, double sh) {
+    const int sweeps = F.begin_step(O, uj, half);
+    ok &= sweeps >= 0;
+    F.cayley(v, sh, sweeps < 0 ? 0 : sweeps);
   };
   // forward sweep from `init`, optionally recording the trajectory
-  auto forward = [&](double2 (&v)[E], bool rec, double* pen) {
+  auto forward = [&](Vec& v, bool rec, double* pen) {
     if (rec) store_state<E>(v, traj, t, T);
     for (int j = 0; j < len; ++j) {
       const double* uj = u + (size_t)j * C;
@@ -265,7 +259,7 @@ __global__ void __launch_bounds__(BF_T) bitflip_task_kernel(DevProblem P, DevRun
     }
   };
   // adjoint sweep with the gradient of objective.cpp:48-60 at every step; `act(j, g)`
-  auto adjoint = [&](double2 (&c0)[E], auto&& act) {
+  auto adjoint = [&](Vec& c0, auto&& act) {
     for (int j = len - 1; j >= 0; --j) {
       const double* uj = u + (size_t)j * C;
       double uold[4];
@@ -354,14 +348,16 @@ __global__ void __launch_bounds__(BF_T) bitflip_task_kernel(DevProblem P, DevRun
 // node_sweeps (ism.cpp:35-84) / exact payoff (objective.cpp:93-100) over the full horizon.
 // blockIdx.y = 0: forward nodes psi_n (which = 0) or the exact payoff (which = 1);
 // blockIdx.y = 1: adjoint nodes chi_n seeded with the target (ism.cpp:72), which = 0 only.
-template <int E, int LOG2E>
-__global__ void __launch_bounds__(BF_T) bitflip_horizon_kernel(DevProblem P, DevRun R, int which, int k) {
+template <int LOG2E, int LOG2T>
+__global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_kernel(DevProblem P, DevRun R, int which, int k) {
+  using F_ = Bf<LOG2E, LOG2T>;
+  constexpr int E = 1 << LOG2E, T = 1 << LOG2T;
   const int b = blockIdx.x, dir = blockIdx.y;
   if (R.done[b] || R.status[b]) return;
   if (which == 1 && dir == 1) return;
   extern __shared__ __align__(16) unsigned char smem[];
-  Bf<E, LOG2E> F = make_bf<E, LOG2E>(P, b, smem);
-  const int d = P.d, C = P.C, t = F.G.t, T = F.G.T;
+  F_ F = make_bf<LOG2E, LOG2T>(P, b, smem);
+  const int d = P.d, C = P.C, t = F.t;
   const BfOps O{P.bf_diag + (size_t)b * d, P.bf_coef + (size_t)b * C * P.nspins, P.bf_axis, C, P.nspins};
   const double half = 0.5 * P.dt;
   const double* u = R.u + (size_t)b * P.K * C;
@@ -369,10 +365,9 @@ __global__ void __launch_bounds__(BF_T) bitflip_horizon_kernel(DevProblem P, Dev
   bool ok = true;
   double2 x[E];
   auto step = [&](const double* uj, double sh) {
-    F.begin_step(O, uj);
-    __syncthreads();
-    const int sweeps = sweep_count(F.sa + F.spar * BF_MAXN, O.n, half);
-    ok &= F.cayley(x, sh, sweeps < 0 ? 0 : sweeps) && sweeps >= 0;
+    const int sweeps = F.begin_step(O, uj, half);
+    ok &= sweeps >= 0;
+    F.cayley(x, sh, sweeps < 0 ? 0 : sweeps);
   };
   if (dir == 0) {
     load_state<E>(x, P.init + (size_t)b * d, t, T);
@@ -411,38 +406,41 @@ __global__ void __launch_bounds__(BF_T) bitflip_horizon_kernel(DevProblem P, Dev
   if (!ok && t == 0 && R.err_flags) atomicOr(R.err_flags, 2);
 }
 
-template <int E, int LOG2E>
+template <int LOG2E, int LOG2T>
 cudaError_t launch_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
   const size_t smem = bf_smem(P.d);
-  auto kern = bitflip_task_kernel<E, LOG2E>;
+  auto kern = bitflip_task_kernel<LOG2E, LOG2T>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<dim3(P.L, P.B), P.d / E, smem, st>>>(P, R, A, ignore_done);
+  kern<<<dim3(P.L, P.B), 1 << LOG2T, smem, st>>>(P, R, A, ignore_done);
   return cudaGetLastError();
 }
 
-template <int E, int LOG2E>
+template <int LOG2E, int LOG2T>
 cudaError_t launch_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
   const size_t smem = bf_smem(P.d);
-  auto kern = bitflip_horizon_kernel<E, LOG2E>;
+  auto kern = bitflip_horizon_kernel<LOG2E, LOG2T>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<dim3(P.B, 2), P.d / E, smem, st>>>(P, R, which, k);
+  kern<<<dim3(P.B, 2), 1 << LOG2T, smem, st>>>(P, R, which, k);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-// d = 2^n: T = min(d, 256) threads, E = d / T amplitudes per thread.
+// d = 2^n: T = min(d, 512) threads, E = d / T amplitudes per thread.
 cudaError_t bitflip_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
   if (A.mode & M_ASSEMBLE) return cudaErrorNotSupported;  // the driver runs the direct plan
   if (P.C > 4) return cudaErrorNotSupported;
   switch (P.nspins) {
-    case 5: case 6: case 7: case 8: return launch_task<1, 0>(P, R, A, ignore_done, st);
-    case 9: return launch_task<2, 1>(P, R, A, ignore_done, st);
-    case 10: return launch_task<4, 2>(P, R, A, ignore_done, st);
-    case 11: return launch_task<8, 3>(P, R, A, ignore_done, st);
-    case 12: return launch_task<16, 4>(P, R, A, ignore_done, st);
+    case 5: return launch_task<0, 5>(P, R, A, ignore_done, st);
+    case 6: return launch_task<0, 6>(P, R, A, ignore_done, st);
+    case 7: return launch_task<0, 7>(P, R, A, ignore_done, st);
+    case 8: return launch_task<0, 8>(P, R, A, ignore_done, st);
+    case 9: return launch_task<0, 9>(P, R, A, ignore_done, st);
+    case 10: return launch_task<1, 9>(P, R, A, ignore_done, st);
+    case 11: return launch_task<2, 9>(P, R, A, ignore_done, st);
+    case 12: return launch_task<3, 9>(P, R, A, ignore_done, st);
   }
   return cudaErrorNotSupported;
 }
@@ -450,11 +448,14 @@ cudaError_t bitflip_task(const DevProblem& P, const DevRun& R, const TaskArgs& A
 cudaError_t bitflip_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
   if (P.C > 4) return cudaErrorNotSupported;
   switch (P.nspins) {
-    case 5: case 6: case 7: case 8: return launch_horizon<1, 0>(P, R, which, k, st);
-    case 9: return launch_horizon<2, 1>(P, R, which, k, st);
-    case 10: return launch_horizon<4, 2>(P, R, which, k, st);
-    case 11: return launch_horizon<8, 3>(P, R, which, k, st);
-    case 12: return launch_horizon<16, 4>(P, R, which, k, st);
+    case 5: return launch_horizon<0, 5>(P, R, which, k, st);
+    case 6: return launch_horizon<0, 6>(P, R, which, k, st);
+    case 7: return launch_horizon<0, 7>(P, R, which, k, st);
+    case 8: return launch_horizon<0, 8>(P, R, which, k, st);
+    case 9: return launch_horizon<0, 9>(P, R, which, k, st);
+    case 10: return launch_horizon<1, 9>(P, R, which, k, st);
+    case 11: return launch_horizon<2, 9>(P, R, which, k, st);
+    case 12: return launch_horizon<3, 9>(P, R, which, k, st);
   }
   return cudaErrorNotSupported;
 }

@@ -51,8 +51,9 @@ def test_run_ism_small_register(ctx, parts, plan):
 
 @pytest.mark.slow
 def test_ising10_config3_iterations(ctx):
-    # BASELINE config 3 at full size (d = 1024, K = 4000, L = 256), a few iterations
-    for rho_fast in (False, True):
+    # BASELINE config 3 at full size (d = 1024, K = 4000, L = 256), two iterations at the
+    # time-to-fidelity step rho = 0.1/dt (the literal rho = 0.1 moves the controls ~100x less)
+    for rho_fast in (True,):
         w = problems.ising10(iterations=2)
         if rho_fast:
             w.solver.step_size = w.rho_fast
