@@ -6,6 +6,7 @@
 // (ism.cpp:546-552), the boundary objective (ism.cpp:285-296) and the waypoint rebuild
 // (interpolated_waypoints + make_subproblems, ism.cpp:100-159).  Every reduction runs in a
 // fixed order, so results do not depend on scheduling.
+#include <cuda_pipeline.h>
 #include <math.h>
 
 #include "kernels.h"
@@ -122,57 +123,59 @@ __global__ void chain_kernel(DevProblem P, DevRun R) {
 
 // compose_from_propagators for d <= 32: one warp per (problem, direction) -- blockIdx.y = 0
 // runs psi_{n+1} = M_n psi_n upward, 1 runs chi_n = M_n^dag chi_{n+1} downward; the two chains
-// are independent.  Lane i keeps row i (forward) or column i (adjoint) of M_n in registers
-// and the loads of M_{n+1} are issued before the dependent matvec of step n, so the chain
-// runs at FMA latency instead of L2 latency.
-template <int TD>
+// are independent.  The matrices stream through an S-deep shared-memory ring filled with
+// cp.async S-1 steps ahead of use, so the dependent matvec chain never waits on L2.
+template <int TD, int S>
 __global__ void __launch_bounds__(32) chain_small_kernel(DevProblem P, DevRun R) {
+  extern __shared__ __align__(16) double2 ring[];  // [S][d*d]
   const int b = blockIdx.x, dir = blockIdx.y, lane = threadIdx.x;
   if (R.done[b] || R.status[b]) return;
-  const int d = P.d, L = P.L;
-  const size_t dd = (size_t)d * d;
+  const int d = P.d, L = P.L, dd = d * d;
   double2* psi = R.psi_nodes + (size_t)b * (L + 1) * d;
   double2* chi = R.chi_nodes + (size_t)b * (L + 1) * d;
   const double2* base = R.prop + (size_t)b * L * dd;
   const bool act = lane < d;
   const int li = act ? lane : 0;
-  double2 v = cx(0.0, 0.0), cur[TD], nxt[TD];
-  auto load = [&](int n, double2 (&m)[TD]) {
-    const double2* M = base + (size_t)n * dd;
-#pragma unroll
-    for (int k = 0; k < TD; ++k)
-      if (k < d) m[k] = dir == 0 ? M[(size_t)li * d + k] : M[(size_t)k * d + li];
+  auto idx = [&](int q) { return dir == 0 ? q : L - 1 - q; };
+  auto issue = [&](int q) {
+    if (q < L) {
+      const double2* M = base + (size_t)idx(q) * dd;
+      double2* dst = ring + (q % S) * dd;
+      for (int e = lane; e < dd; e += 32) __pipeline_memcpy_async(dst + e, M + e, sizeof(double2));
+    }
+    __pipeline_commit();
   };
+  double2 v = cx(0.0, 0.0);
   if (dir == 0) {
     if (act) v = P.init[(size_t)b * d + lane];
     if (act) psi[lane] = v;
-    load(0, cur);
-    for (int n = 0; n < L; ++n) {
-      if (n + 1 < L) load(n + 1, nxt);
-      double2 acc = cx(0.0, 0.0);
-#pragma unroll
-      for (int k = 0; k < TD; ++k)
-        if (k < d) acc = cfma(cur[k], shfl(v, k), acc);
-      v = acc;
-      if (act) psi[(size_t)(n + 1) * d + lane] = v;
-#pragma unroll
-      for (int k = 0; k < TD; ++k) cur[k] = nxt[k];
-    }
   } else {
     if (act) v = P.targ[(size_t)b * d + lane];
     if (act) chi[(size_t)L * d + lane] = v;
-    load(L - 1, cur);
-    for (int n = L - 1; n >= 0; --n) {
-      if (n > 0) load(n - 1, nxt);
-      double2 acc = cx(0.0, 0.0);
+  }
+  for (int q = 0; q < S - 1; ++q) issue(q);
+  for (int q = 0; q < L; ++q) {
+    issue(q + S - 1);
+    __pipeline_wait_prior(S - 1);
+    __syncwarp();
+    const double2* M = ring + (q % S) * dd;
+    double2 acc = cx(0.0, 0.0);
+    if (dir == 0) {
 #pragma unroll
       for (int k = 0; k < TD; ++k)
-        if (k < d) acc = cfmaconj(cur[k], shfl(v, k), acc);
-      v = acc;
-      if (act) chi[(size_t)n * d + lane] = v;
+        if (k < d) acc = cfma(M[li * d + k], shfl(v, k), acc);
+    } else {
 #pragma unroll
-      for (int k = 0; k < TD; ++k) cur[k] = nxt[k];
+      for (int k = 0; k < TD; ++k)
+        if (k < d) acc = cfmaconj(M[k * d + li], shfl(v, k), acc);
     }
+    v = acc;
+    const int n = idx(q);
+    if (act) {
+      if (dir == 0) psi[(size_t)(n + 1) * d + lane] = v;
+      else chi[(size_t)n * d + lane] = v;
+    }
+    __syncwarp();  // slot q % S is refilled by the next iteration's issue
   }
 }
 
@@ -304,14 +307,21 @@ cudaError_t merge_iteration(const DevProblem& P, const DevRun& R, int k, double*
   return cudaGetLastError();
 }
 cudaError_t chain_propagators(const DevProblem& P, const DevRun& R, cudaStream_t st) {
+  const size_t dd = sizeof(double2) * P.d * P.d;
   if (P.d <= 8) {
-    chain_small_kernel<8><<<dim3(P.B, 2), 32, 0, st>>>(P, R);
+    chain_small_kernel<8, 8><<<dim3(P.B, 2), 32, 8 * dd, st>>>(P, R);
   } else if (P.d <= 16) {
-    chain_small_kernel<16><<<dim3(P.B, 2), 32, 0, st>>>(P, R);
+    chain_small_kernel<16, 8><<<dim3(P.B, 2), 32, 8 * dd, st>>>(P, R);
   } else if (P.d <= 24) {
-    chain_small_kernel<24><<<dim3(P.B, 2), 32, 0, st>>>(P, R);
+    auto k = chain_small_kernel<24, 8>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * dd));
+    if (e != cudaSuccess) return e;
+    k<<<dim3(P.B, 2), 32, 8 * dd, st>>>(P, R);
   } else if (P.d <= 32) {
-    chain_small_kernel<32><<<dim3(P.B, 2), 32, 0, st>>>(P, R);
+    auto k = chain_small_kernel<32, 4>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * dd));
+    if (e != cudaSuccess) return e;
+    k<<<dim3(P.B, 2), 32, 4 * dd, st>>>(P, R);
   } else {
     const int nt = P.d >= 256 ? 1024 : 256;
     chain_kernel<<<P.B, nt, sizeof(double2) * P.d, st>>>(P, R);

@@ -367,10 +367,9 @@ constexpr int TRI_CHUNK = 32;
 
 template <int TD>
 struct TriFactors {
-  double dg[TRI_CHUNK][TD];       // H(u_j) diagonal
-  double2 sb[TRI_CHUNK][TD + 1];  // H(u_j) entry (i, i-1); row d (and 0) zero
-  double2 lf[TRI_CHUNK][TD];      // elimination multipliers l_i = a_i / u_{i-1}
-  double2 ui[TRI_CHUNK][TD];      // 1 / u_i
+  double2 lf[TRI_CHUNK][TD];  // elimination multipliers l_i = a_i / u_{i-1}
+  double2 cs[TRI_CHUNK][TD];  // super-diagonal c_i = s conj(sb_{i+1})
+  double2 ui[TRI_CHUNK][TD];  // 1 / u_i
 };
 
 template <int TD>
@@ -402,12 +401,13 @@ __global__ void __launch_bounds__(32) tri_pc_assemble_kernel(DevProblem P, DevRu
     if (lane < cnt) {  // factor B_j = I + sH(u_j), s = i*half (oracle.cpp TriM::cayley)
       const double* uj = u + (size_t)(j0 + lane) * C;
       double2 uinv_prev = cx(0.0, 0.0);
+      double dg;
+      double2 sb;
+      bands_at(T, uj, 0, dg, sb);
       for (int i = 0; i < d; ++i) {
-        double dg;
-        double2 sb;
-        bands_at(T, uj, i, dg, sb);
-        F.dg[lane][i] = dg;
-        F.sb[lane][i] = sb;
+        double dgn;
+        double2 sbn;
+        bands_at(T, uj, i + 1, dgn, sbn);  // zero beyond the last row
         double2 ui = cx(1.0, half * dg);
         double2 lf = cx(0.0, 0.0);
         if (i > 0) {
@@ -419,37 +419,28 @@ __global__ void __launch_bounds__(32) tri_pc_assemble_kernel(DevProblem P, DevRu
         uinv_prev = crcp(ui);
         F.lf[lane][i] = lf;
         F.ui[lane][i] = uinv_prev;
+        F.cs[lane][i] = cx(half * sbn.y, half * sbn.x);         // s conj(sb_{i+1})
+        dg = dgn;
+        sb = sbn;
       }
-      F.sb[lane][d] = cx(0.0, 0.0);
     }
     __syncwarp();
+    // C_j x = (I + sH)^-1 (I - sH) x = 2 z - x with (I + sH) z = x: one forward and one
+    // backward substitution per column, no right-hand-side matvec.
     for (int q = 0; q < cnt; ++q) {
-      const double* fdg = F.dg[q];
-      const double2* fsb = F.sb[q];
       const double2* flf = F.lf[q];
+      const double2* fcs = F.cs[q];
       const double2* fui = F.ui[q];
-      double2 r[TD];
+      double2 z[TD];
 #pragma unroll
-      for (int i = 0; i < TD; ++i) {
-        if (i < d) {
-          const double2 sbi = fsb[i], sbn = fsb[i + 1];
-          double2 h = cx(fdg[i] * x[i].x, fdg[i] * x[i].y);
-          if (i > 0) h = cfma(sbi, x[i - 1], h);
-          if (i + 1 < d) h = cfmaconj(sbn, x[i + 1], h);
-          double2 ri = cx(x[i].x + half * h.y, x[i].y - half * h.x);  // x - s H x
-          if (i > 0) ri = cfms(flf[i], r[i - 1], ri);
-          r[i] = ri;
-        }
-      }
+      for (int i = 0; i < TD; ++i)
+        if (i < d) z[i] = i > 0 ? cfms(flf[i], z[i - 1], x[i]) : x[i];
 #pragma unroll
       for (int i = TD - 1; i >= 0; --i) {
         if (i < d) {
-          double2 v = r[i];
-          if (i + 1 < d) {
-            const double2 sbn = fsb[i + 1];
-            v = cfms(cx(half * sbn.y, half * sbn.x), x[i + 1], v);  // c_i = s conj(sb_{i+1})
-          }
-          x[i] = cmul(v, fui[i]);
+          const double2 v = (i + 1 < d) ? cfms(fcs[i], z[i + 1], z[i]) : z[i];
+          z[i] = cmul(v, fui[i]);
+          x[i] = cx(fma(2.0, z[i].x, -x[i].x), fma(2.0, z[i].y, -x[i].y));
         }
       }
       if (col) {
