@@ -159,17 +159,21 @@ __global__ void __launch_bounds__(32) chain_small_kernel(DevProblem P, DevRun R)
     __pipeline_wait_prior(S - 1);
     __syncwarp();
     const double2* M = ring + (q % S) * dd;
-    double2 acc = cx(0.0, 0.0);
+    // four independent partial sums: the dependent DFMA chain per step is d/2, not 2d
+    double2 acc[4] = {cx(0.0, 0.0), cx(0.0, 0.0), cx(0.0, 0.0), cx(0.0, 0.0)};
+    double2 vk[TD];
+#pragma unroll
+    for (int k = 0; k < TD; ++k) vk[k] = shfl(v, k);
     if (dir == 0) {
 #pragma unroll
       for (int k = 0; k < TD; ++k)
-        if (k < d) acc = cfma(M[li * d + k], shfl(v, k), acc);
+        if (k < d) acc[k & 3] = cfma(M[li * d + k], vk[k], acc[k & 3]);
     } else {
 #pragma unroll
       for (int k = 0; k < TD; ++k)
-        if (k < d) acc = cfmaconj(M[k * d + li], shfl(v, k), acc);
+        if (k < d) acc[k & 3] = cfmaconj(M[k * d + li], vk[k], acc[k & 3]);
     }
-    v = acc;
+    v = cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3]));
     const int n = idx(q);
     if (act) {
       if (dir == 0) psi[(size_t)(n + 1) * d + lane] = v;

@@ -345,9 +345,13 @@ __global__ void __launch_bounds__(128) dense_pc_assemble_kernel(DevProblem P, De
 cudaError_t tri_pc_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st);
 
 int pc_chunk(const DevProblem& P, const DevRun& R) {
-  (void)P;
+  // steps per warp: whole short tasks; otherwise enough chunks for ~16 warps per SM
   const int maxlen = R.traj_len - 1;
-  return maxlen <= 32 ? maxlen : 16;
+  if (maxlen <= 32) return maxlen;
+  const long long want = 148LL * 16;
+  const long long tasks = (long long)P.L * P.B;
+  int chunk = (int)((tasks * maxlen + want - 1) / want);
+  return chunk < 4 ? 4 : (chunk > 16 ? 16 : chunk);
 }
 
 cudaError_t pc_eval(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
