@@ -223,25 +223,34 @@ struct DenseLane {
 
   // P <- 2 W P - P  (one step of assemble_propagator)
   __device__ __forceinline__ void cayley_matmul(const double2 (&W)[COLS], double2 (&P)[COLS],
-                                                const DenseScratch<D, G>& s) const {
+                                                const DenseScratch<D, G>& s, bool live = true) const {
 #pragma unroll
     for (int t = 0; t < COLS; ++t) {
-      s.matW[row * D + col(t, g)] = W[t];
+      if (G > 1) s.matW[row * D + col(t, g)] = W[t];
       s.matP[row * D + col(t, g)] = P[t];
     }
     __syncwarp();
     double2 acc[COLS];
 #pragma unroll
     for (int t = 0; t < COLS; ++t) acc[t] = cx(0.0, 0.0);
-#pragma unroll 4
-    for (int k = 0; k < D; ++k) {
-      const double2 w = s.matW[row * D + k];
+    if constexpr (G == 1) {  // the lane's row of the inverse is already in registers
 #pragma unroll
-      for (int t = 0; t < COLS; ++t) acc[t] = cfma(w, s.matP[k * D + col(t, g)], acc[t]);
+      for (int k = 0; k < D; ++k) {
+#pragma unroll
+        for (int t = 0; t < COLS; ++t) acc[t] = cfma(W[k], s.matP[k * D + t], acc[t]);
+      }
+    } else {
+#pragma unroll 4
+      for (int k = 0; k < D; ++k) {
+        const double2 w = s.matW[row * D + k];
+#pragma unroll
+        for (int t = 0; t < COLS; ++t) acc[t] = cfma(w, s.matP[k * D + col(t, g)], acc[t]);
+      }
     }
     __syncwarp();
 #pragma unroll
-    for (int t = 0; t < COLS; ++t) P[t] = cx(2.0 * acc[t].x - P[t].x, 2.0 * acc[t].y - P[t].y);
+    for (int t = 0; t < COLS; ++t)
+      if (live) P[t] = cx(2.0 * acc[t].x - P[t].x, 2.0 * acc[t].y - P[t].y);
   }
 
   // Sum over the D rows of a per-row value (each g block reduces independently).

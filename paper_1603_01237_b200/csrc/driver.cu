@@ -35,6 +35,8 @@ struct qoc_ctx {
   qoc_profile_v1 prof{};
   // event pairs of the current run: (start, stop, is_task)
   std::vector<std::tuple<cudaEvent_t, cudaEvent_t, bool>> marks;
+  void* prob_slots = nullptr;  // Slots* (driver.cu anonymous namespace)
+  void* run_slots = nullptr;
 };
 
 namespace {
@@ -72,6 +74,23 @@ struct DBuf {
   template <class T>
   T* as() const {
     return static_cast<T*>(p);
+  }
+};
+
+// Grow-only device buffers owned by a context: the i-th request of a call reuses slot i when
+// it is large enough, so repeated solves on one context make no cudaMalloc/cudaFree calls.
+struct Slots {
+  std::vector<DBuf> bufs;
+  size_t next = 0;
+  void reset() { next = 0; }
+  void* get(size_t bytes) {
+    bytes = std::max<size_t>(bytes, 1);
+    if (next < bufs.size()) {
+      if (bufs[next].bytes < bytes) bufs[next] = DBuf(bytes);
+    } else {
+      bufs.emplace_back(bytes);
+    }
+    return bufs[next++].p;
   }
 };
 
@@ -116,13 +135,16 @@ std::vector<int> decomposition(int K, int L, int mode, const int32_t* explicit_n
 // Device copy of a problem (operators converted to the kernels' layouts).
 struct DeviceProblem {
   DevProblem P{};
-  std::vector<DBuf> bufs;
+  Slots* slots = nullptr;
+  cudaStream_t st = nullptr;
   int stride = 0;  // state stride of the kind's trajectory workspace
 
-  template <class T>
-  const T* keep(DBuf&& b) {
-    bufs.push_back(std::move(b));
-    return bufs.back().as<T>();
+  // device copy of n host elements, returned as the kernels' element type T
+  template <class T, class H>
+  const T* put(const H* host, size_t n) {
+    void* d = slots->get(sizeof(H) * n);
+    if (n) ck(cudaMemcpyAsync(d, host, sizeof(H) * n, cudaMemcpyHostToDevice, st), "upload");
+    return static_cast<const T*>(d);
   }
 };
 
@@ -148,6 +170,7 @@ void hermitian_check(const double* m, int d, const char* what) {  // models.cpp:
 }
 
 void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaStream_t st, DeviceProblem& out) {
+  out.st = st;
   validate_problem(p);
   DevProblem& P = out.P;
   const int d = p->dim, C = p->channels, B = p->batch, K = p->steps;
@@ -195,10 +218,10 @@ void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaS
           convert(p->quadratic + 2 * dd * ((size_t)b * C + c), quad.data() + 2 * dd * ((size_t)b * C + c),
                   nb + 1 + C + c, "quadratic operator");
       }
-      P.h0 = out.keep<double2>(upload(h0.data(), h0.size(), st));
-      P.lin = out.keep<double2>(upload(lin.data(), lin.size(), st));
-      P.quad = nq ? out.keep<double2>(upload(quad.data(), quad.size(), st)) : nullptr;
-      P.norm1 = out.keep<double>(upload(norms.data(), norms.size(), st));
+      P.h0 = out.put<double2>(h0.data(), h0.size());
+      P.lin = out.put<double2>(lin.data(), lin.size());
+      P.quad = nq ? out.put<double2>(quad.data(), quad.size()) : nullptr;
+      P.norm1 = out.put<double>(norms.data(), norms.size());
       break;
     }
     case QOC_KIND_TRIDIAG: {
@@ -206,8 +229,8 @@ void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaS
       if (d > 32) fail(QOC_ELOGIC, "tridiagonal device kernels support d <= 32");
       P.has_quad = p->tri_has_quadratic != 0;
       const int nops = 1 + C + (P.has_quad ? C : 0);
-      P.tri_diag = out.keep<double>(upload(p->tri_diag, (size_t)B * nops * d, st));
-      P.tri_sub = out.keep<double2>(upload(reinterpret_cast<const double2*>(p->tri_sub), (size_t)B * nops * (d - 1), st));
+      P.tri_diag = out.put<double>(p->tri_diag, (size_t)B * nops * d);
+      P.tri_sub = out.put<double2>(reinterpret_cast<const double2*>(p->tri_sub), (size_t)B * nops * (d - 1));
       break;
     }
     case QOC_KIND_BITFLIP: {
@@ -215,9 +238,9 @@ void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaS
       if (p->nspins < 5 || p->nspins > 12 || (1 << p->nspins) != d)
         fail(QOC_EINVAL, "bit-flip dim must be 2^nspins (5 <= nspins <= 12)");
       P.nspins = p->nspins;
-      P.bf_diag = out.keep<double>(upload(p->h0, (size_t)B * d, st));
-      P.bf_axis = out.keep<int>(upload(p->bf_axis, (size_t)C, st));
-      P.bf_coef = out.keep<double>(upload(p->bf_coef, (size_t)B * C * p->nspins, st));
+      P.bf_diag = out.put<double>(p->h0, (size_t)B * d);
+      P.bf_axis = out.put<int>(p->bf_axis, (size_t)C);
+      P.bf_coef = out.put<double>(p->bf_coef, (size_t)B * C * p->nspins);
       break;
     }
     case QOC_KIND_STRANG: {
@@ -236,8 +259,8 @@ void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaS
         ka[2 * i] = std::cos(aa);
         ka[2 * i + 1] = std::sin(aa);
       }
-      P.kin_fwd = out.keep<double2>(upload(reinterpret_cast<const double2*>(kf.data()), (size_t)d, st));
-      P.kin_adj = out.keep<double2>(upload(reinterpret_cast<const double2*>(ka.data()), (size_t)d, st));
+      P.kin_fwd = out.put<double2>(reinterpret_cast<const double2*>(kf.data()), (size_t)d);
+      P.kin_adj = out.put<double2>(reinterpret_cast<const double2*>(ka.data()), (size_t)d);
       // twiddles of linalg.cpp:26-27 (polar(1, ang * k), ang = -2 pi / n; the inverse
       // transform conjugates) or the direct DFT kernel of linalg.cpp:37-50
       std::vector<double> tw;
@@ -258,8 +281,8 @@ void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaS
             tw[2 * ((size_t)k * d + m) + 1] = std::sin(a);
           }
       }
-      P.twiddle = out.keep<double2>(upload(reinterpret_cast<const double2*>(tw.data()), tw.size() / 2, st));
-      P.grid_x = out.keep<double>(upload(p->grid_x, (size_t)d, st));
+      P.twiddle = out.put<double2>(reinterpret_cast<const double2*>(tw.data()), tw.size() / 2);
+      P.grid_x = out.put<double>(p->grid_x, (size_t)d);
       P.potential = p->potential;
       for (int i = 0; i < 4; ++i) P.pp[i] = p->pot_params[i];
       P.kappa = p->kappa;
@@ -268,21 +291,27 @@ void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaS
     default:
       fail(QOC_EINVAL, "unknown model kind");
   }
-  P.init = out.keep<double2>(upload(reinterpret_cast<const double2*>(p->initial), (size_t)B * d, st));
-  P.targ = out.keep<double2>(upload(reinterpret_cast<const double2*>(p->target), (size_t)B * d, st));
+  P.init = out.put<double2>(reinterpret_cast<const double2*>(p->initial), (size_t)B * d);
+  P.targ = out.put<double2>(reinterpret_cast<const double2*>(p->target), (size_t)B * d);
   std::vector<double> alpha(K, 0.0);
   if (p->penalty) alpha.assign(p->penalty, p->penalty + K);
-  P.alpha = out.keep<double>(upload(alpha.data(), alpha.size(), st));
-  P.node = out.keep<int>(upload(node.data(), node.size(), st));
+  P.alpha = out.put<double>(alpha.data(), alpha.size());
+  P.node = out.put<int>(node.data(), node.size());
+}
+
+Slots* fresh_slots(void*& handle) {
+  if (!handle) handle = new Slots;
+  Slots* sl = static_cast<Slots*>(handle);
+  sl->reset();
+  return sl;
 }
 
 struct DeviceRun {
   DevRun R{};
-  std::vector<DBuf> bufs;
+  Slots* slots = nullptr;
   template <class T>
   T* alloc(size_t n) {
-    bufs.emplace_back(sizeof(T) * std::max<size_t>(n, 1));
-    return bufs.back().as<T>();
+    return static_cast<T*>(slots->get(sizeof(T) * std::max<size_t>(n, 1)));
   }
 };
 
@@ -486,6 +515,8 @@ void qoc_ctx_destroy(qoc_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->flush_buf) cudaFree(ctx->flush_buf);
+  delete static_cast<Slots*>(ctx->prob_slots);
+  delete static_cast<Slots*>(ctx->run_slots);
   delete ctx;
 }
 
@@ -546,9 +577,11 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
     Launcher launch{ctx};
 
     DeviceProblem dp;
+    dp.slots = fresh_slots(ctx->prob_slots);
     upload_problem(p, node, st, dp);
     const DevProblem& P = dp.P;
     DeviceRun dr;
+    dr.slots = fresh_slots(ctx->run_slots);
     const bool pcache = use_pcache(P, node);
     alloc_run(dp, rec_cap, node, assembled_interp, false, st, dr, pcache);
     const DevRun& R = dr.R;
@@ -738,7 +771,9 @@ int32_t qoc_propagate_final(qoc_ctx* ctx, const qoc_problem_v1* p, const double*
     validate_problem(p);
     if (!u || !states_out) fail(QOC_EINVAL, "null argument");
     DeviceProblem dp;
+    dp.slots = fresh_slots(ctx->prob_slots);
     DeviceRun dr;
+    dr.slots = fresh_slots(ctx->run_slots);
     single_run(ctx, p, u, M_FINAL, QOC_FORM_OVERLAP, false, false, dp, dr);
     ck(cudaMemcpy(states_out, dr.R.psi_end, sizeof(double2) * p->batch * p->dim, cudaMemcpyDeviceToHost), "out");
   });
@@ -751,7 +786,9 @@ int32_t qoc_objective_gradient(qoc_ctx* ctx, const qoc_problem_v1* p, const doub
     if (!u) fail(QOC_EINVAL, "null argument");
     if (naive && p->kind != QOC_KIND_STRANG) naive = 0;
     DeviceProblem dp;
+    dp.slots = fresh_slots(ctx->prob_slots);
     DeviceRun dr;
+    dr.slots = fresh_slots(ctx->run_slots);
     int mode = M_ENTRY | (grad_out ? M_GRAD : 0) | (naive ? (1 << 10) : 0);
     single_run(ctx, p, u, mode, form, false, grad_out != nullptr, dp, dr);
     if (value_out) ck(cudaMemcpy(value_out, dr.R.entry, sizeof(double) * p->batch, cudaMemcpyDeviceToHost), "value");
@@ -771,7 +808,9 @@ int32_t qoc_assemble_propagator(qoc_ctx* ctx, const qoc_problem_v1* p, const dou
     if (p->kind == QOC_KIND_BITFLIP)
       fail(QOC_ELOGIC, "the bit-flip kind does not assemble d x d propagators; use QOC_KIND_DENSE");
     DeviceProblem dp;
+    dp.slots = fresh_slots(ctx->prob_slots);
     DeviceRun dr;
+    dr.slots = fresh_slots(ctx->run_slots);
     single_run(ctx, p, u, M_ASSEMBLE, QOC_FORM_TRACKING, true, false, dp, dr);
     const size_t B = p->batch, d = p->dim;
     std::vector<double2> rm(B * d * d);

@@ -316,13 +316,8 @@ __global__ void __launch_bounds__(128) dense_pc_assemble_kernel(DevProblem P, De
       Ln.invert_pivot(W, S, lane);
     else
       Ln.invert_fast(W, S.piv);
-    double2 Q[COLS];
-#pragma unroll
-    for (int t = 0; t < COLS; ++t) Q[t] = Pm[t];
-    Ln.cayley_matmul(W, Q, S);
+    Ln.cayley_matmul(W, Pm, S, live);  // P_{j+1} = 2 B_j^-1 P_j - P_j (kept when past len)
     if (live) {
-#pragma unroll
-      for (int t = 0; t < COLS; ++t) Pm[t] = Q[t];
       if (live_task && row < d) {
         double2* dst = Pc + (size_t)(j + 1) * dd + (size_t)row * d;
 #pragma unroll
