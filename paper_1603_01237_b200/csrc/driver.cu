@@ -652,12 +652,12 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
         launch.run([&] { return penalty_partials(P, R, 0, st); }, "penalty");
         launch.run([&] { return merge_iteration(P, R, k, nullptr, st); }, "merge");
         if (L > 1) {
-          if (direct) launch.run([&] { return horizon(P, R, 0, k, st); }, "node sweeps");
+          if (direct) launch.run([&] { return horizon(P, R, 0, k, st); }, "node sweeps", true);
           else if (split) launch.run([&] { return split_nodes(P, R, st); }, "split nodes");
           else launch.run([&] { return chain_propagators(P, R, st); }, "chain");
           launch.run([&] { return boundary_update(P, R, k, split, 0, st); }, "boundary");
         }
-        if (cfg->log_exact_objective) launch.run([&] { return horizon(P, R, 1, k, st); }, "exact objective");
+        if (cfg->log_exact_objective) launch.run([&] { return horizon(P, R, 1, k, st); }, "exact objective", true);
         launch.run([&] { return finish_iteration_ex(P, R, k, cfg->compute_error, cfg->eta,
                                                     cfg->log_exact_objective, st); }, "finish");
         ck(cudaEventRecord(ev_end[k + 1], st), "event");

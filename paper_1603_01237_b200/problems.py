@@ -263,12 +263,17 @@ def condensate_preset(subintervals: int = 4, iterations: int = 10) -> Workload:
                     0.1 / grid.dt)
 
 
+_GPE_STATES: dict = {}
+
+
 def gpe1024(subintervals: int = 64, iterations: int = 100, rho: float = 0.1, points: int = 1024,
             steps: int = 10000, T: float = 5.0) -> Workload:
     """BASELINE config 4: H = -1/2 d2/dx2 + x^2/2 + 5 cos^2(x - u) + 10|psi|^2 on [-16, 16)."""
     model = CondensateModel(points, -16.0, 16.0, abi.POT_LATTICE, [1.0, 5.0, 1.0], 10.0)
-    psi_i = stationary_state(model, 0.0)
-    psi_t = stationary_state(model, 0.0, excited=1, lower=[psi_i])
+    if points not in _GPE_STATES:  # setup only; memoised per process (~20 s at 1024 points)
+        g = stationary_state(model, 0.0)
+        _GPE_STATES[points] = (g, stationary_state(model, 0.0, excited=1, lower=[g]))
+    psi_i, psi_t = (s.copy() for s in _GPE_STATES[points])
     grid = TimeGrid.over(0.0, T, steps)
     p = ControlProblem(model, grid, psi_i, psi_t, np.zeros(steps))
     cfg = IsmConfig(subintervals=subintervals, workers=8, eta=0.0, max_outer=iterations,
