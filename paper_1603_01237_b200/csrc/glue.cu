@@ -123,27 +123,39 @@ __global__ void chain_kernel(DevProblem P, DevRun R) {
 
 // compose_from_propagators for d <= 32: one warp per (problem, direction) -- blockIdx.y = 0
 // runs psi_{n+1} = M_n psi_n upward, 1 runs chi_n = M_n^dag chi_{n+1} downward; the two chains
-// are independent.  The matrices stream through an S-deep shared-memory ring filled with
-// cp.async S-1 steps ahead of use, so the dependent matvec chain never waits on L2.
+// are independent.  The chain is bound by instruction latency on one warp, so each step is
+// kept to a minimum of instructions: the matrices stream into an S-deep shared-memory ring
+// by TMA bulk copies (one instruction per matrix, issued S-1 steps ahead, completing on
+// per-slot mbarriers) and the state vector is broadcast through shared memory (one LDS.128
+// per element instead of four SHFL).
 template <int TD, int S>
 __global__ void __launch_bounds__(32) chain_small_kernel(DevProblem P, DevRun R) {
-  extern __shared__ __align__(16) double2 ring[];  // [S][d*d]
+  extern __shared__ __align__(128) unsigned char chain_smem[];
   const int b = blockIdx.x, dir = blockIdx.y, lane = threadIdx.x;
   if (R.done[b] || R.status[b]) return;
   const int d = P.d, L = P.L, dd = d * d;
+  const unsigned mbytes = (unsigned)(sizeof(double2) * dd);
+  const unsigned slot = (mbytes + 127u) & ~127u;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(chain_smem);
+  double2* vsh = reinterpret_cast<double2*>(chain_smem + 128);
+  unsigned char* ring = chain_smem + 128 + 16 * 32;
   double2* psi = R.psi_nodes + (size_t)b * (L + 1) * d;
   double2* chi = R.chi_nodes + (size_t)b * (L + 1) * d;
   const double2* base = R.prop + (size_t)b * L * dd;
   const bool act = lane < d;
   const int li = act ? lane : 0;
   auto idx = [&](int q) { return dir == 0 ? q : L - 1 - q; };
+  if (lane == 0) {
+    for (int k = 0; k < S; ++k) mbar_init(&bars[k], 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
   auto issue = [&](int q) {
-    if (q < L) {
-      const double2* M = base + (size_t)idx(q) * dd;
-      double2* dst = ring + (q % S) * dd;
-      for (int e = lane; e < dd; e += 32) __pipeline_memcpy_async(dst + e, M + e, sizeof(double2));
+    if (lane == 0 && q < L) {
+      unsigned long long* bar = &bars[q % S];
+      mbar_expect_tx(bar, mbytes);
+      bulk_g2s(ring + (size_t)(q % S) * slot, base + (size_t)idx(q) * dd, mbytes, bar);
     }
-    __pipeline_commit();
   };
   double2 v = cx(0.0, 0.0);
   if (dir == 0) {
@@ -156,30 +168,27 @@ __global__ void __launch_bounds__(32) chain_small_kernel(DevProblem P, DevRun R)
   for (int q = 0; q < S - 1; ++q) issue(q);
   for (int q = 0; q < L; ++q) {
     issue(q + S - 1);
-    __pipeline_wait_prior(S - 1);
+    vsh[lane] = v;
+    mbar_wait(&bars[q % S], (unsigned)((q / S) & 1));
     __syncwarp();
-    const double2* M = ring + (q % S) * dd;
-    // four independent partial sums: the dependent DFMA chain per step is d/2, not 2d
-    double2 acc[4] = {cx(0.0, 0.0), cx(0.0, 0.0), cx(0.0, 0.0), cx(0.0, 0.0)};
-    double2 vk[TD];
-#pragma unroll
-    for (int k = 0; k < TD; ++k) vk[k] = shfl(v, k);
+    const double2* M = reinterpret_cast<const double2*>(ring + (size_t)(q % S) * slot);
+    double2 acc[2] = {cx(0.0, 0.0), cx(0.0, 0.0)};
     if (dir == 0) {
 #pragma unroll
       for (int k = 0; k < TD; ++k)
-        if (k < d) acc[k & 3] = cfma(M[li * d + k], vk[k], acc[k & 3]);
+        if (k < d) acc[k & 1] = cfma(M[li * d + k], vsh[k], acc[k & 1]);
     } else {
 #pragma unroll
       for (int k = 0; k < TD; ++k)
-        if (k < d) acc[k & 3] = cfmaconj(M[k * d + li], vk[k], acc[k & 3]);
+        if (k < d) acc[k & 1] = cfmaconj(M[k * d + li], vsh[k], acc[k & 1]);
     }
-    v = cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3]));
+    v = cadd(acc[0], acc[1]);
     const int n = idx(q);
     if (act) {
       if (dir == 0) psi[(size_t)(n + 1) * d + lane] = v;
       else chi[(size_t)n * d + lane] = v;
     }
-    __syncwarp();  // slot q % S is refilled by the next iteration's issue
+    __syncwarp();  // slot q % S and vsh are rewritten next iteration
   }
 }
 
@@ -311,21 +320,22 @@ cudaError_t merge_iteration(const DevProblem& P, const DevRun& R, int k, double*
   return cudaGetLastError();
 }
 cudaError_t chain_propagators(const DevProblem& P, const DevRun& R, cudaStream_t st) {
-  const size_t dd = sizeof(double2) * P.d * P.d;
+  const size_t slot = (sizeof(double2) * P.d * P.d + 127) & ~(size_t)127;
+  auto go = [&](auto kern, int S) -> cudaError_t {
+    const size_t smem = 128 + 16 * 32 + S * slot;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<dim3(P.B, 2), 32, smem, st>>>(P, R);
+    return cudaGetLastError();
+  };
   if (P.d <= 8) {
-    chain_small_kernel<8, 8><<<dim3(P.B, 2), 32, 8 * dd, st>>>(P, R);
+    return go(chain_small_kernel<8, 8>, 8);
   } else if (P.d <= 16) {
-    chain_small_kernel<16, 8><<<dim3(P.B, 2), 32, 8 * dd, st>>>(P, R);
+    return go(chain_small_kernel<16, 8>, 8);
   } else if (P.d <= 24) {
-    auto k = chain_small_kernel<24, 8>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * dd));
-    if (e != cudaSuccess) return e;
-    k<<<dim3(P.B, 2), 32, 8 * dd, st>>>(P, R);
+    return go(chain_small_kernel<24, 8>, 8);
   } else if (P.d <= 32) {
-    auto k = chain_small_kernel<32, 4>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * dd));
-    if (e != cudaSuccess) return e;
-    k<<<dim3(P.B, 2), 32, 4 * dd, st>>>(P, R);
+    return go(chain_small_kernel<32, 4>, 4);
   } else {
     const int nt = P.d >= 256 ? 1024 : 256;
     chain_kernel<<<P.B, nt, sizeof(double2) * P.d, st>>>(P, R);
