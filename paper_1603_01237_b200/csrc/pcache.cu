@@ -104,6 +104,29 @@ __device__ __forceinline__ double2 matvec_row(const double2* M, int d, int i, co
   }
   return cadd(a, b);
 }
+// Both y1 = M v1 and y2 = M v2 for this lane's row, the row loaded once with all its loads
+// in flight together (the step loop is HBM-latency-bound, so the loads must not serialise).
+__device__ __forceinline__ void matvec_row2(const double2* M, int d, int i, const double2* v1,
+                                            const double2* v2, double2& y1, double2& y2) {
+  double2 r[32];
+  const double2* row = M + (size_t)(i < d ? i : 0) * d;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) r[k] = k < d ? __ldcs(row + k) : cx(0.0, 0.0);
+  double2 a0 = cx(0.0, 0.0), a1 = cx(0.0, 0.0), b0 = cx(0.0, 0.0), b1 = cx(0.0, 0.0);
+#pragma unroll
+  for (int k = 0; k < 32; k += 2) {
+    if (k < d) {
+      a0 = cfma(r[k], v1[k], a0);
+      b0 = cfma(r[k], v2[k], b0);
+    }
+    if (k + 1 < d) {
+      a1 = cfma(r[k + 1], v1[k + 1], a1);
+      b1 = cfma(r[k + 1], v2[k + 1], b1);
+    }
+  }
+  y1 = i < d ? cadd(a0, a1) : cx(0.0, 0.0);
+  y2 = i < d ? cadd(b0, b1) : cx(0.0, 0.0);
+}
 // y_i = sum_k conj(M[k][i]) v_k
 __device__ __forceinline__ double2 matvec_adj_row(const double2* M, int d, int i, const double2* v) {
   double2 a = cx(0.0, 0.0);
@@ -185,12 +208,12 @@ __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, Ta
 
   double err = 0.0;
   if (mode & (PC_GRAD | PC_ERR | PC_RAWGRAD)) {
-    double2 psa = matvec_row(Pc + (size_t)j0 * dd, d, i, S.phi);
-    double2 cha = matvec_row(Pc + (size_t)j0 * dd, d, i, S.chi0);
+    double2 psa, cha;
+    matvec_row2(Pc + (size_t)j0 * dd, d, i, S.phi, S.chi0, psa, cha);
     for (int j = j0; j < j1; ++j) {
       const double2* Pj1 = Pc + (size_t)(j + 1) * dd;
-      const double2 psb = matvec_row(Pj1, d, i, S.phi);
-      const double2 chb = matvec_row(Pj1, d, i, S.chi0);
+      double2 psb, chb;
+      matvec_row2(Pj1, d, i, S.phi, S.chi0, psb, chb);
       const double2 ps = cadd(psa, psb), cs = cadd(cha, chb);
       const double* uj = u + (size_t)j * C;
       const double aj = P.alpha[node0 + j] * scale;
