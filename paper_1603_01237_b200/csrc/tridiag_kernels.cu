@@ -461,10 +461,202 @@ __global__ void __launch_bounds__(32) tri_pc_assemble_kernel(DevProblem P, DevRu
   if (!ok && lane == 0 && R.err_flags) atomicOr(R.err_flags, 1);
 }
 
+// Twisted ("burn at both ends") variant of the cache sweep: two warps per task, compiled for
+// an exact dimension (the BASELINE rotor, d = 21) so each warp's row loops cover only its half.  Warp 0
+// eliminates rows 0..m-1 top-down (LU), warp 1 rows d-1..m+1 bottom-up (UL), they meet at the
+// middle row m = d/2 through shared memory, then substitute outward concurrently.  The serial
+// dependent chain per step -- the bound of the one-warp kernel -- is halved.  Factors are
+// again computed step-parallel per 32-step chunk (warp 0 the LU side and the reference's
+// pivot check, warp 1 the UL side).  Same Cayley map; rounding differs from the LU sweep at
+// the 1e-16 level (diagonally dominant B, no pivoting on either side).
+template <int TD>
+struct TwistFactors {
+  double2 lf[TRI_CHUNK][TD];   // top: l_i = a_i / u_{i-1} (i = 1..m)
+  double2 ui[TRI_CHUNK][TD];   // top: 1 / u_i (i = 0..m-1)
+  double2 cs[TRI_CHUNK][TD];   // c_i = s conj(sb_{i+1}) (super)
+  double2 as[TRI_CHUNK][TD];   // a_i = s sb_i (sub)
+  double2 kf[TRI_CHUNK][TD];   // bottom: k_i = c_i / w_{i+1} (i = m..d-2)
+  double2 wi[TRI_CHUNK][TD];   // bottom: 1 / w_i (i = m+1..d-1)
+  double2 gm[TRI_CHUNK];       // 1 / gamma_m
+  double2 bm[TRI_CHUNK];       // b_m (middle diagonal)
+  double2 zt[2][32];           // z'_{m-1} per column (top -> middle), double-buffered by step
+  double2 zb[2][32];           // z''_{m+1} per column (bottom -> middle)
+};
+
+template <int TD, int DIM>
+__global__ void __launch_bounds__(64) tri_pc_assemble2_kernel(DevProblem P, DevRun R, int ignore_done) {
+  const int n = blockIdx.x, b = blockIdx.y, lane = threadIdx.x & 31, side = threadIdx.x >> 5;
+  if (ignore_done ? R.status[b] : R.done[b]) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TwistFactors<TD>& F = *reinterpret_cast<TwistFactors<TD>*>(smem_raw);
+  constexpr int d = DIM, m = DIM / 2;  // compile-time: every row loop unrolls to its own half
+  const int C = P.C;
+  const int nops = 1 + C + (P.has_quad ? C : 0);
+  const TriView T{P.tri_diag + (size_t)b * nops * d, P.tri_sub + (size_t)b * nops * (d - 1), d, C, P.has_quad};
+  const int node0 = P.node[n], len = P.node[n + 1] - node0;
+  const double half = 0.5 * P.dt;
+  const double* u = R.u + ((size_t)b * P.K + node0) * C;
+  const size_t dd = (size_t)d * d;
+  double2* Pc = R.pc + ((size_t)b * P.L + n) * (size_t)R.traj_len * dd;
+  const bool col = lane < d;
+  bool ok = true;
+  // rows owned: top [0, m], bottom [m, d-1] (the middle row in both)
+  const int r0 = side == 0 ? 0 : m, r1 = side == 0 ? m : d - 1;
+  double2 x[TD];
+#pragma unroll
+  for (int i = 0; i < TD; ++i) x[i] = cx(i == lane ? 1.0 : 0.0, 0.0);
+  if (col)
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+      if (i < d && i >= r0 && i <= r1 && (side == 0 || i > m)) Pc[(size_t)i * d + lane] = x[i];
+  auto sband = [&](const double* uj, int i, double& dg, double2& sb) { bands_at(T, uj, i, dg, sb); };
+  for (int j0 = 0; j0 < len; j0 += TRI_CHUNK) {
+    const int cnt = min(TRI_CHUNK, len - j0);
+    __syncthreads();
+    if (lane < cnt) {
+      const double* uj = u + (size_t)(j0 + lane) * C;
+      if (side == 0) {
+        // LU top-down over rows 0..m (and the full-LU pivot check of the reference solve)
+        double2 uinv_prev = cx(0.0, 0.0);
+        double dg;
+        double2 sb;
+        sband(uj, 0, dg, sb);
+        for (int i = 0; i < d; ++i) {
+          double dgn;
+          double2 sbn;
+          sband(uj, i + 1, dgn, sbn);
+          const double2 bi = cx(1.0, half * dg);
+          const double2 ci = cx(half * sbn.y, half * sbn.x);  // s conj(sb_{i+1})
+          double2 ui = bi, lf = cx(0.0, 0.0);
+          if (i > 0) {
+            const double2 a = cx(-half * sb.y, half * sb.x);  // s sb_i
+            ok = ok && !(cabs2(a) * cabs2(uinv_prev) > 1.0);
+            lf = cmul(a, uinv_prev);
+            ui = cfms(lf, cx(half * sb.y, half * sb.x), ui);
+          }
+          uinv_prev = crcp(ui);
+          if (i <= m) {
+            F.lf[lane][i] = lf;
+            F.cs[lane][i] = ci;
+            if (i < m) F.ui[lane][i] = uinv_prev;
+            if (i == m) F.bm[lane] = bi;
+          }
+          dg = dgn;
+          sb = sbn;
+        }
+      } else {
+        // UL bottom-up over rows d-1..m
+        double2 winv_next = cx(0.0, 0.0);
+        for (int i = d - 1; i >= m; --i) {
+          double dg, dgn;
+          double2 sb, sbn;
+          sband(uj, i, dg, sb);
+          sband(uj, i + 1, dgn, sbn);
+          const double2 ci = cx(half * sbn.y, half * sbn.x);  // c_i = s conj(sb_{i+1})
+          const double2 ai = cx(-half * sb.y, half * sb.x);   // a_i = s sb_i
+          F.as[lane][i] = ai;
+          double2 kf = cx(0.0, 0.0), wi = cx(1.0, half * dg);
+          if (i + 1 < d) {
+            kf = cmul(ci, winv_next);
+            wi = cfms(kf, F.as[lane][i + 1], wi);  // b_i - k_i a_{i+1}
+          }
+          F.kf[lane][i] = kf;
+          if (i > m) {
+            winv_next = crcp(wi);
+            F.wi[lane][i] = winv_next;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (side == 0 && lane < cnt) {  // gamma_m = b_m - l_m c_{m-1} - k_m a_{m+1}
+      double2 g = F.bm[lane];
+      if (m > 0) g = cfms(F.lf[lane][m], F.cs[lane][m - 1], g);
+      if (m + 1 < d) g = cfms(F.kf[lane][m], F.as[lane][m + 1], g);
+      F.gm[lane] = crcp(g);
+    }
+    __syncthreads();
+    for (int q = 0; q < cnt; ++q) {
+      const int par = q & 1;
+      double2 z[TD];
+      if (side == 0) {
+#pragma unroll
+        for (int i = 0; i < TD; ++i)
+          if (i < m) z[i] = i > 0 ? cfms(F.lf[q][i], z[i - 1], x[i]) : x[i];
+#pragma unroll
+        for (int i = 0; i < TD; ++i)
+          if (i + 1 == m) F.zt[par][lane] = z[i];  // static register index
+      } else {
+#pragma unroll
+        for (int i = TD - 1; i >= 0; --i)
+          if (i < d && i > m) z[i] = (i + 1 < d) ? cfms(F.kf[q][i], z[i + 1], x[i]) : x[i];
+#pragma unroll
+        for (int i = 0; i < TD; ++i)
+          if (i == m + 1 && i < d) F.zb[par][lane] = z[i];
+      }
+      __syncthreads();
+      // middle row (both warps, identical arithmetic)
+      double2 xm = x[0];
+#pragma unroll
+      for (int i = 0; i < TD; ++i)
+        if (i == m) xm = x[i];
+      double2 zm = xm;
+      if (m > 0) zm = cfms(F.lf[q][m], F.zt[par][lane], zm);
+      if (m + 1 < d) zm = cfms(F.kf[q][m], F.zb[par][lane], zm);
+      zm = cmul(zm, F.gm[q]);
+      double2* dst = Pc + (size_t)(j0 + q + 1) * dd;
+      if (side == 0) {
+        double2 zn = zm;
+#pragma unroll
+        for (int i = TD - 1; i >= 0; --i) {
+          if (i < m) {
+            const double2 v = cfms(F.cs[q][i], zn, z[i]);
+            zn = cmul(v, F.ui[q][i]);
+            x[i] = cx(fma(2.0, zn.x, -x[i].x), fma(2.0, zn.y, -x[i].y));
+            if (col) dst[(size_t)i * d + lane] = x[i];
+          }
+        }
+      } else {
+        double2 zp = zm;
+#pragma unroll
+        for (int i = 0; i < TD; ++i) {
+          if (i < d && i > m) {
+            const double2 v = cfms(F.as[q][i], zp, z[i]);
+            zp = cmul(v, F.wi[q][i]);
+            x[i] = cx(fma(2.0, zp.x, -x[i].x), fma(2.0, zp.y, -x[i].y));
+            if (col) dst[(size_t)i * d + lane] = x[i];
+          }
+        }
+      }
+      xm = cx(fma(2.0, zm.x, -xm.x), fma(2.0, zm.y, -xm.y));
+#pragma unroll
+      for (int i = 0; i < TD; ++i)
+        if (i == m) x[i] = xm;
+      if (side == 0 && col) dst[(size_t)m * d + lane] = xm;
+    }
+  }
+  if (col && R.prop) {
+    double2* M = R.prop + ((size_t)b * P.L + n) * dd;
+#pragma unroll
+    for (int i = 0; i < TD; ++i)
+      if (i < d && ((side == 0 && i <= m) || (side == 1 && i > m))) M[(size_t)i * d + lane] = x[i];
+  }
+  ok = __all_sync(0xffffffffu, ok);
+  if (!ok && lane == 0 && side == 0 && R.err_flags) atomicOr(R.err_flags, 1);
+}
+
 }  // namespace
 
 cudaError_t tri_pc_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st) {
   if (P.d > 30) return cudaErrorNotSupported;
+  if (P.d == 21) {
+    auto k = tri_pc_assemble2_kernel<24, 21>;
+    const int smem = (int)sizeof(TwistFactors<24>);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    k<<<dim3(P.L, P.B), 64, smem, st>>>(P, R, ignore_done);
+    return cudaGetLastError();
+  }
   if (P.d <= 24) {
     auto k = tri_pc_assemble_kernel<24>;
     const int smem = (int)sizeof(TriFactors<24>);
