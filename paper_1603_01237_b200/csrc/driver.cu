@@ -27,6 +27,8 @@ using namespace qoc;
 struct qoc_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t aux = nullptr;          // side stream: boundary chain overlapped with the residual
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::string last_error;
   int64_t launches = 0;
   bool profile = false;
@@ -502,7 +504,10 @@ int32_t qoc_ctx_create(const qoc_ctx_opts_v1* opts, qoc_ctx** out) {
   if (prop.major < 10) return QOC_ECUDA;  // built for sm_100a only
   auto* c = new qoc_ctx;
   c->device = dev;
-  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     delete c;
     return QOC_ECUDA;
   }
@@ -514,6 +519,9 @@ void qoc_ctx_destroy(qoc_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->flush_buf) cudaFree(ctx->flush_buf);
   delete static_cast<Slots*>(ctx->prob_slots);
   delete static_cast<Slots*>(ctx->run_slots);
@@ -641,6 +649,14 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
             launch.run([&] { return pc_eval(P, R, G2, 0, st); }, "gradient", true);
           }
           launch.run([&] { return pc_assemble(P, R, 0, st); }, "assembly", true);
+          if (assembled_interp) {
+            // the boundary chain needs only the new propagators: run it on the side stream,
+            // concurrently with the residual sweep, penalty and merge (joined before boundary)
+            ck(cudaEventRecord(ctx->ev_fork, st), "fork");
+            ck(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0), "fork");
+            launch(chain_propagators(P, R, ctx->aux), "chain");
+            ck(cudaEventRecord(ctx->ev_join, ctx->aux), "join");
+          }
           const int em = (cfg->compute_error ? PCM_ERR : 0) | ((L > 1 && split && !direct) ? PCM_LAG : 0);
           if (em) {
             const TaskArgs E{em, form, split ? 0 : 1, 1, 0.0};
@@ -654,6 +670,7 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
         if (L > 1) {
           if (direct) launch.run([&] { return horizon(P, R, 0, k, st); }, "node sweeps", true);
           else if (split) launch.run([&] { return split_nodes(P, R, st); }, "split nodes");
+          else if (pcache) ck(cudaStreamWaitEvent(st, ctx->ev_join, 0), "join");
           else launch.run([&] { return chain_propagators(P, R, st); }, "chain");
           launch.run([&] { return boundary_update(P, R, k, split, 0, st); }, "boundary");
         }
