@@ -90,19 +90,20 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// y_i = sum_k M[i][k] v_k (M row-major d x d, v in smem); lanes >= d return 0.
+// y_i = sum_k M[i][k] v_k (M row-major d x d, v in smem); lanes >= d return 0.  The row is
+// loaded with every load in flight at once (these reads are HBM-latency-bound).
 __device__ __forceinline__ double2 matvec_row(const double2* M, int d, int i, const double2* v) {
+  double2 r[32];
+  const double2* row = M + (size_t)(i < d ? i : 0) * d;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) r[k] = k < d ? row[k] : cx(0.0, 0.0);
   double2 a = cx(0.0, 0.0), b = cx(0.0, 0.0);
-  if (i < d) {
-    const double2* r = M + (size_t)i * d;
-    int k = 0;
-    for (; k + 1 < d; k += 2) {
-      a = cfma(r[k], v[k], a);
-      b = cfma(r[k + 1], v[k + 1], b);
-    }
+#pragma unroll
+  for (int k = 0; k < 32; k += 2) {
     if (k < d) a = cfma(r[k], v[k], a);
+    if (k + 1 < d) b = cfma(r[k + 1], v[k + 1], b);
   }
-  return cadd(a, b);
+  return i < d ? cadd(a, b) : cx(0.0, 0.0);
 }
 // Both y1 = M v1 and y2 = M v2 for this lane's row, the row loaded once with all its loads
 // in flight together (the step loop is HBM-latency-bound, so the loads must not serialise).
@@ -129,10 +130,17 @@ __device__ __forceinline__ void matvec_row2(const double2* M, int d, int i, cons
 }
 // y_i = sum_k conj(M[k][i]) v_k
 __device__ __forceinline__ double2 matvec_adj_row(const double2* M, int d, int i, const double2* v) {
-  double2 a = cx(0.0, 0.0);
-  if (i < d)
-    for (int k = 0; k < d; ++k) a = cfmaconj(M[(size_t)k * d + i], v[k], a);
-  return a;
+  double2 c[32];
+  const int ii = i < d ? i : 0;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) c[k] = k < d ? M[(size_t)k * d + ii] : cx(0.0, 0.0);
+  double2 a = cx(0.0, 0.0), b = cx(0.0, 0.0);
+#pragma unroll
+  for (int k = 0; k < 32; k += 2) {
+    if (k < d) a = cfmaconj(c[k], v[k], a);
+    if (k + 1 < d) b = cfmaconj(c[k + 1], v[k + 1], b);
+  }
+  return i < d ? cadd(a, b) : cx(0.0, 0.0);
 }
 
 template <bool TRI>
