@@ -5,7 +5,7 @@ import subprocess
 import sys
 
 KEYS = {
-    "gpu__time_duration.sum": "duration_ns",
+    "gpu__time_duration.sum": "duration",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_pct",
     "dram__bytes_read.sum": "dram_read",
     "dram__bytes_write.sum": "dram_write",
@@ -25,12 +25,12 @@ STALLS = "smsp__pcsamp_warps_issue_stalled_"
 def brief(path):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr = rows[0]
+    hdr, units = rows[0], dict(zip(rows[0], rows[1]))
     out = []
     for r in rows[2:]:
         d = dict(zip(hdr, r))
         name = d.get("Kernel Name", "?").split("(")[0]
-        vals = {v: d[k] for k, v in KEYS.items() if k in d}
+        vals = {v: (d[k] + (units.get(k) or "")) for k, v in KEYS.items() if k in d}
         stalls = sorted(((k[len(STALLS):], float(d[k].replace(",", "") or 0)) for k in hdr
                          if k.startswith(STALLS) and not k.endswith("not_issued") and d[k]),
                         key=lambda x: -x[1])[:6]
