@@ -337,7 +337,8 @@ def main():
     # ---- time to fidelity 0.999 (rho = 0.1/dt), device time summed over iterations
     ttf = None
     if args.workload in ("rotor21", "spin2", "batch4096") and rank == 0:
-        wt = build_workload(args.workload, 300, 0, 1)
+        # iteration cap of the time-to-fidelity run (the rotor converges slowly at rho = 0.1/dt)
+        wt = build_workload(args.workload, 4000 if args.workload == "rotor21" else 300, 0, 1)
         if args.workload == "batch4096":
             wt = problems.batch4096(batch=64, iterations=300)
             wt.solver.step_size = wt.rho_fast

@@ -38,19 +38,32 @@ struct PcSmem {
   double red[32];
 };
 
-// (dH/du_c ps)_i for this lane's row i, dense operators (row-major, global / L1).
+// (dH/du_c ps)_i for this lane's row i, dense operators (row-major, global / L1); the row is
+// loaded with all loads in flight (DM-wide unrolled) before the dot product.
+template <int DM>
 __device__ __forceinline__ double2 dense_dH_row(const DevProblem& P, int b, int c, double uc, int i,
                                                 const double2* ps_sh) {
   const int d = P.d;
   const double2* a = P.lin + (((size_t)b * P.C + c) * d + i) * d;
   const double2* q = P.has_quad ? P.quad + (((size_t)b * P.C + c) * d + i) * d : nullptr;
-  double2 acc = cx(0.0, 0.0);
-  for (int k = 0; k < d; ++k) {
-    double2 m = a[k];
-    if (q) m = cx(fma(uc, q[k].x, m.x), fma(uc, q[k].y, m.y));
-    acc = cfma(m, ps_sh[k], acc);
+  double2 m[DM];
+#pragma unroll
+  for (int k = 0; k < DM; ++k) m[k] = k < d ? __ldg(a + k) : cx(0.0, 0.0);
+  if (q) {
+#pragma unroll
+    for (int k = 0; k < DM; ++k)
+      if (k < d) {
+        const double2 qq = __ldg(q + k);
+        m[k] = cx(fma(uc, qq.x, m[k].x), fma(uc, qq.y, m[k].y));
+      }
   }
-  return acc;
+  double2 acc0 = cx(0.0, 0.0), acc1 = cx(0.0, 0.0);
+#pragma unroll
+  for (int k = 0; k < DM; k += 2) {
+    if (k < d) acc0 = cfma(m[k], ps_sh[k], acc0);
+    if (k + 1 < d) acc1 = cfma(m[k + 1], ps_sh[k + 1], acc1);
+  }
+  return cadd(acc0, acc1);
 }
 
 // Tridiagonal (dH/du_c ps)_i with neighbours by shuffle.
@@ -92,14 +105,15 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // y_i = sum_k M[i][k] v_k (M row-major d x d, v in smem); lanes >= d return 0.  The row is
 // loaded with every load in flight at once (these reads are HBM-latency-bound).
+template <int DM>
 __device__ __forceinline__ double2 matvec_row(const double2* M, int d, int i, const double2* v) {
-  double2 r[32];
+  double2 r[DM];
   const double2* row = M + (size_t)(i < d ? i : 0) * d;
 #pragma unroll
-  for (int k = 0; k < 32; ++k) r[k] = k < d ? row[k] : cx(0.0, 0.0);
+  for (int k = 0; k < DM; ++k) r[k] = k < d ? row[k] : cx(0.0, 0.0);
   double2 a = cx(0.0, 0.0), b = cx(0.0, 0.0);
 #pragma unroll
-  for (int k = 0; k < 32; k += 2) {
+  for (int k = 0; k < DM; k += 2) {
     if (k < d) a = cfma(r[k], v[k], a);
     if (k + 1 < d) b = cfma(r[k + 1], v[k + 1], b);
   }
@@ -107,15 +121,16 @@ __device__ __forceinline__ double2 matvec_row(const double2* M, int d, int i, co
 }
 // Both y1 = M v1 and y2 = M v2 for this lane's row, the row loaded once with all its loads
 // in flight together (the step loop is HBM-latency-bound, so the loads must not serialise).
+template <int DM>
 __device__ __forceinline__ void matvec_row2(const double2* M, int d, int i, const double2* v1,
                                             const double2* v2, double2& y1, double2& y2) {
-  double2 r[32];
+  double2 r[DM];
   const double2* row = M + (size_t)(i < d ? i : 0) * d;
 #pragma unroll
-  for (int k = 0; k < 32; ++k) r[k] = k < d ? __ldcs(row + k) : cx(0.0, 0.0);
+  for (int k = 0; k < DM; ++k) r[k] = k < d ? __ldcs(row + k) : cx(0.0, 0.0);
   double2 a0 = cx(0.0, 0.0), a1 = cx(0.0, 0.0), b0 = cx(0.0, 0.0), b1 = cx(0.0, 0.0);
 #pragma unroll
-  for (int k = 0; k < 32; k += 2) {
+  for (int k = 0; k < DM; k += 2) {
     if (k < d) {
       a0 = cfma(r[k], v1[k], a0);
       b0 = cfma(r[k], v2[k], b0);
@@ -129,21 +144,22 @@ __device__ __forceinline__ void matvec_row2(const double2* M, int d, int i, cons
   y2 = i < d ? cadd(b0, b1) : cx(0.0, 0.0);
 }
 // y_i = sum_k conj(M[k][i]) v_k
+template <int DM>
 __device__ __forceinline__ double2 matvec_adj_row(const double2* M, int d, int i, const double2* v) {
-  double2 c[32];
+  double2 c[DM];
   const int ii = i < d ? i : 0;
 #pragma unroll
-  for (int k = 0; k < 32; ++k) c[k] = k < d ? M[(size_t)k * d + ii] : cx(0.0, 0.0);
+  for (int k = 0; k < DM; ++k) c[k] = k < d ? M[(size_t)k * d + ii] : cx(0.0, 0.0);
   double2 a = cx(0.0, 0.0), b = cx(0.0, 0.0);
 #pragma unroll
-  for (int k = 0; k < 32; k += 2) {
+  for (int k = 0; k < DM; k += 2) {
     if (k < d) a = cfmaconj(c[k], v[k], a);
     if (k + 1 < d) b = cfmaconj(c[k + 1], v[k + 1], b);
   }
   return i < d ? cadd(a, b) : cx(0.0, 0.0);
 }
 
-template <bool TRI>
+template <bool TRI, int DM>
 __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, TaskArgs A, int chunk, int nchunk,
                                                       int ignore_done) {
   __shared__ PcSmem<32> sm_all[4];
@@ -173,13 +189,13 @@ __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, Ta
   S.phi[i] = phi;
   __syncwarp();
   const double2* PL = Pc + (size_t)len * dd;
-  const double2 psiL = matvec_row(PL, d, i, S.phi);
+  const double2 psiL = matvec_row<DM>(PL, d, i, S.phi);
 
   if (mode & (PC_GRAD | PC_ERR | PC_RAWGRAD)) {
     // chi_0 = P_len^dag seed (objective.cpp:31-34 seed)
     S.vec[i] = A.form == 0 ? targ : csub(targ, psiL);
     __syncwarp();
-    S.chi0[i] = matvec_adj_row(PL, d, i, S.vec);
+    S.chi0[i] = matvec_adj_row<DM>(PL, d, i, S.vec);
     __syncwarp();
   }
   if (ch == 0) {
@@ -193,11 +209,11 @@ __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, Ta
     if (mode & PC_LAG) {  // ism.cpp:424-459 through the cached product
       S.vec[i] = i < d ? R.psi_nodes[((size_t)b * (P.L + 1) + n) * d + i] : zero;
       __syncwarp();
-      const double2 pe = matvec_row(PL, d, i, S.vec);
+      const double2 pe = matvec_row<DM>(PL, d, i, S.vec);
       __syncwarp();
       S.vec[i] = i < d ? R.chi_nodes[((size_t)b * (P.L + 1) + n + 1) * d + i] : zero;
       __syncwarp();
-      const double2 cs = matvec_adj_row(PL, d, i, S.vec);
+      const double2 cs = matvec_adj_row<DM>(PL, d, i, S.vec);
       if (i < d) {
         R.psi_end[tix + i] = pe;
         R.chi_start[tix + i] = cs;
@@ -217,11 +233,11 @@ __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, Ta
   double err = 0.0;
   if (mode & (PC_GRAD | PC_ERR | PC_RAWGRAD)) {
     double2 psa, cha;
-    matvec_row2(Pc + (size_t)j0 * dd, d, i, S.phi, S.chi0, psa, cha);
+    matvec_row2<DM>(Pc + (size_t)j0 * dd, d, i, S.phi, S.chi0, psa, cha);
     for (int j = j0; j < j1; ++j) {
       const double2* Pj1 = Pc + (size_t)(j + 1) * dd;
       double2 psb, chb;
-      matvec_row2(Pj1, d, i, S.phi, S.chi0, psb, chb);
+      matvec_row2<DM>(Pj1, d, i, S.phi, S.chi0, psb, chb);
       const double2 ps = cadd(psa, psb), cs = cadd(cha, chb);
       const double* uj = u + (size_t)j * C;
       const double aj = P.alpha[node0 + j] * scale;
@@ -235,7 +251,7 @@ __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, Ta
         } else {
           S.vec[i] = ps;
           __syncwarp();
-          h = i < d ? dense_dH_row(P, b, c, uc, i, S.vec) : zero;
+          h = i < d ? dense_dH_row<DM>(P, b, c, uc, i, S.vec) : zero;
           __syncwarp();
         }
         const double im = warp_sum(i < d ? cconjmul(cs, h).y : 0.0);
@@ -384,10 +400,14 @@ cudaError_t pc_eval(const DevProblem& P, const DevRun& R, const TaskArgs& A, int
   const int chunk = pc_chunk(P, R);
   const int nchunk = (R.traj_len - 1 + chunk - 1) / chunk;
   dim3 grid((P.L * nchunk + 3) / 4, P.B);
-  if (P.kind == QOC_KIND_TRIDIAG)
-    pc_eval_kernel<true><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
-  else
-    pc_eval_kernel<false><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
+  const bool small = P.d <= 16;  // narrower register arrays -> higher occupancy
+  if (P.kind == QOC_KIND_TRIDIAG) {
+    if (small) pc_eval_kernel<true, 16><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
+    else pc_eval_kernel<true, 32><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
+  } else {
+    if (small) pc_eval_kernel<false, 16><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
+    else pc_eval_kernel<false, 32><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   pc_finalize_kernel<<<(P.B * P.L + 127) / 128, 128, 0, st>>>(P, R, A, nchunk, ignore_done);
