@@ -351,7 +351,9 @@ void alloc_run(const DeviceProblem& dp, int cap, const std::vector<int>& node, b
   R.prop = need_prop ? out.alloc<double2>(B * L * d * d) : nullptr;
   R.psi_end = out.alloc<double2>(B * L * d);
   R.chi_start = out.alloc<double2>(B * L * d);
-  R.traj = out.alloc<double2>(B * L * (size_t)R.traj_len * dp.stride);
+  // the split-step kind runs its residual and lagged sweeps as concurrent CTAs, each with its
+  // own trajectory: two workspaces
+  R.traj = out.alloc<double2>(B * L * (size_t)R.traj_len * dp.stride * (P.kind == QOC_KIND_STRANG ? 2 : 1));
   R.entry = out.alloc<double>(B * L);
   R.err = out.alloc<double>(B * L);
   R.pen = out.alloc<double>(B * L);

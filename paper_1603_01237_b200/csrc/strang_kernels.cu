@@ -228,9 +228,20 @@ __global__ void __launch_bounds__(ST_T) strang_task_kernel(DevProblem P, DevRun 
   const double dt = P.dt, w = P.ip_w;
   const bool naive = (A.mode & (1 << 10)) != 0;
   double* u = R.u + ((size_t)b * P.K + node0);  // C == 1
-  double2* traj = R.traj + ((size_t)b * P.L + n) * (size_t)R.traj_len * d;
+  int mode = A.mode;
+  // phase-2 roles in separate CTAs (blockIdx.z): 0 = residual sweep, 1 = lagged refresh with
+  // the second trajectory workspace
+  size_t toff = 0;
+  if (gridDim.z == 2) {
+    if (blockIdx.z == 0) {
+      mode &= ~M_LAGGED;
+    } else {
+      mode &= ~M_ERROR;
+      toff = (size_t)P.B * P.L * R.traj_len * d;
+    }
+  }
+  double2* traj = R.traj + toff + ((size_t)b * P.L + n) * (size_t)R.traj_len * d;
   const size_t tix = ((size_t)b * P.L + n) * d;
-  const int mode = A.mode;
 
   auto forward = [&](bool rec, double* pen) {  // state in X.A
     if (rec) store_vec(traj, X.A, d);
@@ -379,7 +390,21 @@ cudaError_t strang_task(const DevProblem& P, const DevRun& R, const TaskArgs& A,
   const size_t smem = strang_smem(P.d);
   cudaError_t e = cudaFuncSetAttribute(strang_task_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  strang_task_kernel<<<dim3(P.L, P.B), ST_T, smem, st>>>(P, R, A, ignore_done);
+  // phase 1 (entry value, gradient sweep + update) then phase 2 (residual sweep and lagged
+  // refresh at the updated control, independent of each other: concurrent CTAs)
+  const int p1 = A.mode & (M_ENTRY | M_UPDATE | M_FINAL | M_GRAD), p2 = A.mode & (M_ERROR | M_LAGGED);
+  if (p1) {
+    TaskArgs A1 = A;
+    A1.mode = A.mode & ~(M_ERROR | M_LAGGED);
+    strang_task_kernel<<<dim3(P.L, P.B, 1), ST_T, smem, st>>>(P, R, A1, ignore_done);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (p2) {
+    TaskArgs A2 = A;
+    A2.mode = p2 | (A.mode & (1 << 10));
+    const int roles = (p2 & M_ERROR) && (p2 & M_LAGGED) ? 2 : 1;
+    strang_task_kernel<<<dim3(P.L, P.B, roles), ST_T, smem, st>>>(P, R, A2, ignore_done);
+  }
   return cudaGetLastError();
 }
 
