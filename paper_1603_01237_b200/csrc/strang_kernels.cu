@@ -5,10 +5,11 @@
 // live in shared memory; every kinetic half step is
 //     spectral(psi, phase) = idft(phase . dft(psi))          (propagation.cpp:27-31)
 // evaluated as two unnormalised transforms with the 1/n of the two unitary 1/sqrt(n) factors
-// folded into the phase multiply.  Powers of two use an in-place radix-2 decimation-in-time
-// FFT in shared memory (bit-reversed scatter fused with the phase multiply, twiddles staged
-// once per CTA); other sizes (<= 256 points, e.g. the reference's 50-point preset) use the
-// direct O(n^2) sum of linalg.cpp:37-50 against a precomputed DFT matrix.
+// folded into the phase multiply.  Powers of two use a Stockham radix-4 autosort FFT in
+// shared memory (phase multiply fused into the first stage, twiddles staged once per CTA);
+// other sizes (<= 256 points, e.g. the reference's 50-point preset) use the
+// direct O(n^2) sum of linalg.cpp:37-50 against a precomputed DFT matrix.  (The transform is
+// a Stockham radix-4 FFT; `src` is used as scratch and is clobbered.)
 //
 // Forward step (strang_step, propagation.cpp:131-139): kinetic half phase, potential +
 // kappa |psi_a|^2 phase, kinetic half phase.  Backward stage (strang_backward_stage,
@@ -40,7 +41,23 @@ struct StrangCtx {
   const double2* dftm;   // global [d][d] (direct DFT)
   double2 *A, *B, *S, *Q;  // smem work vectors [d]
   double* red;           // smem [ST_T / 32]
+  double2* kx;           // smem [d] (cos k x_i, sin k x_i) of the lattice potential
 };
+
+// V(x_i, u) and dV/du for grid point i.  The cos^2 lattice uses cos/sin(k(x_i - u)) by angle
+// addition from the per-point table and one sincos(k u) per step (cs = (cos k u, sin k u)).
+struct PotStep {
+  double2 cs;
+};
+__device__ __forceinline__ PotStep pot_step(const DevProblem& P, double u) {
+  PotStep S{cx(1.0, 0.0)};
+  if (P.potential != QOC_POT_TRAP) {
+    double sn, cn;
+    sincos(P.pp[2] * u, &sn, &cn);
+    S.cs = cx(cn, sn);
+  }
+  return S;
+}
 
 // dst = DFT_sign(pre . src) unnormalised (sign -1 forward, +1 inverse); pre may be null.
 // src and dst are distinct shared-memory vectors.  Ends with a __syncthreads.
@@ -48,27 +65,71 @@ __device__ void transform(const StrangCtx& X, const double2* src, double2* dst, 
                           double scale) {
   const int d = X.d, t = threadIdx.x;
   if (X.pow2) {
-    for (int i = t; i < d; i += ST_T) {
-      double2 v = src[i];
-      if (pre) v = cmul(v, pre[i]);
-      if (scale != 1.0) v = cscale(v, scale);
-      const int r = X.log2d ? (int)(__brev((unsigned)i) >> (32 - X.log2d)) : 0;
-      dst[r] = v;
+    // Stockham autosort, radix 4 (plus one radix-2 stage when log2 d is odd): no bit-reversal
+    // pass and half the barriers of radix 2.  Ping-pongs between dst and src (src is scratch
+    // afterwards); the pre-multiply and scale are fused into the first stage's loads.
+    double2* in = const_cast<double2*>(src);
+    double2* out = dst;
+    bool first = true;
+    for (int Ns = 1; Ns < d;) {
+      const int R = (Ns * 4 <= d) ? 4 : 2;
+      const int nb = d / R;
+      for (int j = t; j < nb; j += ST_T) {
+        const int jm = j & (Ns - 1);  // j % Ns
+        double2 v[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (r < R) {
+            double2 x = in[j + r * nb];
+            if (first) {
+              if (pre) x = cmul(x, pre[j + r * nb]);
+              if (scale != 1.0) x = cscale(x, scale);
+            }
+            if (r > 0 && jm != 0) {  // twiddle exp(sign 2 pi i jm r / (Ns R))
+              int k = jm * r * (d / (Ns * R));
+              double2 w;
+              if (k < d / 2) {
+                w = X.tw[k];
+              } else {
+                w = X.tw[k - d / 2];
+                w = cx(-w.x, -w.y);
+              }
+              if (sign > 0) w.y = -w.y;
+              x = cmul(x, w);
+            }
+            v[r] = x;
+          }
+        }
+        const int idxD = (j / Ns) * Ns * R + jm;
+        if (R == 4) {
+          const double2 a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]), a2 = cadd(v[1], v[3]);
+          const double2 dd = csub(v[1], v[3]);
+          const double2 a3 = sign < 0 ? cx(dd.y, -dd.x) : cx(-dd.y, dd.x);  // -+i (v1 - v3)
+          out[idxD] = cadd(a0, a2);
+          out[idxD + Ns] = cadd(a1, a3);
+          out[idxD + 2 * Ns] = csub(a0, a2);
+          out[idxD + 3 * Ns] = csub(a1, a3);
+        } else {
+          out[idxD] = cadd(v[0], v[1]);
+          out[idxD + Ns] = csub(v[0], v[1]);
+        }
+      }
+      __syncthreads();
+      first = false;
+      Ns *= R;
+      double2* tmp = in;
+      in = out;
+      out = tmp;
     }
-    __syncthreads();
-    for (int s = 1; s <= X.log2d; ++s) {
-      const int half = 1 << (s - 1);
-      const int tstride = d >> s;  // twiddle index step for this stage
-      for (int q = t; q < (d >> 1); q += ST_T) {
-        const int k = q & (half - 1);
-        const int i0 = ((q >> (s - 1)) << s) + k;
-        const int i1 = i0 + half;
-        double2 w = X.tw[k * tstride];
-        if (sign > 0) w.y = -w.y;
-        const double2 lo = dst[i0];
-        const double2 hi = cmul(w, dst[i1]);
-        dst[i0] = cadd(lo, hi);
-        dst[i1] = csub(lo, hi);
+    if (in != dst) {  // even number of stages: the result sits in src
+      for (int i = t; i < d; i += ST_T) dst[i] = in[i];
+      __syncthreads();
+    }
+    if (d == 1 && (pre || scale != 1.0)) {  // no stages ran
+      for (int i = t; i < d; i += ST_T) {
+        double2 x = src[i];
+        if (pre) x = cmul(x, pre[i]);
+        dst[i] = cscale(x, scale);
       }
       __syncthreads();
     }
@@ -124,13 +185,31 @@ __device__ __forceinline__ double potential_du(const DevProblem& P, double x, do
   return P.pp[1] * P.pp[2] * sin(2.0 * P.pp[2] * (x - u));
 }
 
+__device__ __forceinline__ double potential_at(const StrangCtx& X, const DevProblem& P, int i, double u,
+                                               const PotStep& S) {
+  const double x = P.grid_x[i];
+  if (P.potential == QOC_POT_TRAP) return potential(P, x, u);
+  const double2 k = X.kx[i];
+  const double c = fma(k.x, S.cs.x, k.y * S.cs.y);  // cos(k(x - u))
+  return 0.5 * P.pp[0] * x * x + P.pp[1] * c * c;
+}
+__device__ __forceinline__ double potential_du_at(const StrangCtx& X, const DevProblem& P, int i, double u,
+                                                  const PotStep& S) {
+  if (P.potential == QOC_POT_TRAP) return potential_du(P, P.grid_x[i], u);
+  const double2 k = X.kx[i];
+  const double c = fma(k.x, S.cs.x, k.y * S.cs.y);   // cos(k(x - u))
+  const double sn = fma(k.y, S.cs.x, -k.x * S.cs.y);  // sin(k(x - u))
+  return 2.0 * P.pp[1] * P.pp[2] * sn * c;           // v0 k sin(2k(x - u))
+}
+
 // psi (in X.A) -> strang_step(psi); uses B, S.
 __device__ void strang_forward(const StrangCtx& X, const DevProblem& P, double u, double dt) {
   transform(X, X.A, X.B, -1, nullptr, 1.0);
   transform(X, X.B, X.S, +1, P.kin_fwd, X.inv_n);  // psi_a
+  const PotStep ps = pot_step(P, u);
   for (int i = threadIdx.x; i < X.d; i += ST_T) {
     const double2 pa = X.S[i];
-    const double w = potential(P, P.grid_x[i], u) + P.kappa * cabs2(pa);
+    const double w = potential_at(X, P, i, u, ps) + P.kappa * cabs2(pa);
     double s, c;
     sincos(-dt * w, &s, &c);
     X.S[i] = cmul(cx(c, s), pa);  // psi_b
@@ -149,16 +228,16 @@ __device__ double strang_backward(const StrangCtx& X, const DevProblem& P, doubl
   transform(X, X.A, X.B, -1, nullptr, 1.0);
   transform(X, X.B, X.A, +1, P.kin_adj, X.inv_n);  // chi_b in A
   double g = 0.0;
+  const PotStep pst = pot_step(P, u);
   for (int i = threadIdx.x; i < d; i += ST_T) {
     const double2 pa = X.S[i], cb = X.A[i];
-    const double xi = P.grid_x[i];
     const double dens = cabs2(pa);
-    const double w = potential(P, xi, u) + P.kappa * dens;
+    const double w = potential_at(X, P, i, u, pst) + P.kappa * dens;
     double s, c;
     sincos(-dt * w, &s, &c);
     const double2 flow = cx(c, s);
     const double2 pb = cmul(flow, pa);
-    if (want_grad) g += potential_du(P, xi, u) * cconjmul(cb, pb).y;
+    if (want_grad) g += potential_du_at(X, P, i, u, pst) * cconjmul(cb, pb).y;
     double2 ca;
     if (naive) {
       ca = cconjmul(flow, cb);
@@ -198,13 +277,20 @@ __device__ __forceinline__ StrangCtx make_ctx(const DevProblem& P, unsigned char
     X.tw = nullptr;
     X.red = reinterpret_cast<double*>(tw);
   }
+  X.kx = reinterpret_cast<double2*>(X.red + ST_T / 32);
+  for (int i = threadIdx.x; i < d; i += ST_T) {
+    double sn, cn;
+    sincos(P.pp[2] * P.grid_x[i], &sn, &cn);
+    X.kx[i] = cx(cn, sn);
+  }
   __syncthreads();
   return X;
 }
 
 size_t strang_smem(int d) {
   const bool pow2 = (d & (d - 1)) == 0;
-  return sizeof(double2) * (4 * (size_t)d + (pow2 ? (d / 2 > 0 ? d / 2 : 1) : 0)) + sizeof(double) * (ST_T / 32);
+  return sizeof(double2) * (4 * (size_t)d + (pow2 ? (d / 2 > 0 ? d / 2 : 1) : 0)) + sizeof(double) * (ST_T / 32) +
+         sizeof(double2) * (size_t)d;
 }
 
 __device__ __forceinline__ void load_vec(double2* dst, const double2* src, int d) {
