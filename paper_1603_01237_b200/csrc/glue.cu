@@ -128,12 +128,13 @@ __global__ void chain_kernel(DevProblem P, DevRun R) {
 // by TMA bulk copies (one instruction per matrix, issued S-1 steps ahead, completing on
 // per-slot mbarriers) and the state vector is broadcast through shared memory (one LDS.128
 // per element instead of four SHFL).
-template <int TD, int S>
+template <int TD, int S, int DIM = 0>
 __global__ void __launch_bounds__(32) chain_small_kernel(DevProblem P, DevRun R) {
   extern __shared__ __align__(128) unsigned char chain_smem[];
   const int b = blockIdx.x, dir = blockIdx.y, lane = threadIdx.x;
   if (R.done[b] || R.status[b]) return;
-  const int d = P.d, L = P.L, dd = d * d;
+  // DIM > 0: dimension fixed at compile time (the rotor, d = 21): no guards in the dot products
+  const int d = DIM > 0 ? DIM : P.d, L = P.L, dd = d * d;
   const unsigned mbytes = (unsigned)(sizeof(double2) * dd);
   const unsigned slot = (mbytes + 127u) & ~127u;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(chain_smem);
@@ -172,17 +173,17 @@ __global__ void __launch_bounds__(32) chain_small_kernel(DevProblem P, DevRun R)
     mbar_wait(&bars[q % S], (unsigned)((q / S) & 1));
     __syncwarp();
     const double2* M = reinterpret_cast<const double2*>(ring + (size_t)(q % S) * slot);
-    double2 acc[2] = {cx(0.0, 0.0), cx(0.0, 0.0)};
+    double2 acc[4] = {cx(0.0, 0.0), cx(0.0, 0.0), cx(0.0, 0.0), cx(0.0, 0.0)};
     if (dir == 0) {
 #pragma unroll
       for (int k = 0; k < TD; ++k)
-        if (k < d) acc[k & 1] = cfma(M[li * d + k], vsh[k], acc[k & 1]);
+        if (k < d) acc[k & 3] = cfma(M[li * d + k], vsh[k], acc[k & 3]);
     } else {
 #pragma unroll
       for (int k = 0; k < TD; ++k)
-        if (k < d) acc[k & 1] = cfmaconj(M[k * d + li], vsh[k], acc[k & 1]);
+        if (k < d) acc[k & 3] = cfmaconj(M[k * d + li], vsh[k], acc[k & 3]);
     }
-    v = cadd(acc[0], acc[1]);
+    v = cadd(cadd(acc[0], acc[1]), cadd(acc[2], acc[3]));
     const int n = idx(q);
     if (act) {
       if (dir == 0) psi[(size_t)(n + 1) * d + lane] = v;
@@ -332,6 +333,8 @@ cudaError_t chain_propagators(const DevProblem& P, const DevRun& R, cudaStream_t
     return go(chain_small_kernel<8, 8>, 8);
   } else if (P.d <= 16) {
     return go(chain_small_kernel<16, 8>, 8);
+  } else if (P.d == 21) {
+    return go(chain_small_kernel<21, 8, 21>, 8);
   } else if (P.d <= 24) {
     return go(chain_small_kernel<24, 8>, 8);
   } else if (P.d <= 32) {
