@@ -143,6 +143,30 @@ __device__ __forceinline__ void matvec_row2(const double2* M, int d, int i, cons
   y1 = i < d ? cadd(a0, a1) : cx(0.0, 0.0);
   y2 = i < d ? cadd(b0, b1) : cx(0.0, 0.0);
 }
+template <int DM>
+__device__ __forceinline__ void load_row(const double2* M, int d, int i, double2 (&r)[DM]) {
+  const double2* row = M + (size_t)(i < d ? i : 0) * d;
+#pragma unroll
+  for (int k = 0; k < DM; ++k) r[k] = k < d ? __ldcs(row + k) : cx(0.0, 0.0);
+}
+template <int DM>
+__device__ __forceinline__ void rows_dot2(const double2 (&r)[DM], int d, int i, const double2* v1,
+                                          const double2* v2, double2& y1, double2& y2) {
+  double2 a0 = cx(0.0, 0.0), a1 = cx(0.0, 0.0), b0 = cx(0.0, 0.0), b1 = cx(0.0, 0.0);
+#pragma unroll
+  for (int k = 0; k < DM; k += 2) {
+    if (k < d) {
+      a0 = cfma(r[k], v1[k], a0);
+      b0 = cfma(r[k], v2[k], b0);
+    }
+    if (k + 1 < d) {
+      a1 = cfma(r[k + 1], v1[k + 1], a1);
+      b1 = cfma(r[k + 1], v2[k + 1], b1);
+    }
+  }
+  y1 = i < d ? cadd(a0, a1) : cx(0.0, 0.0);
+  y2 = i < d ? cadd(b0, b1) : cx(0.0, 0.0);
+}
 // y_i = sum_k conj(M[k][i]) v_k
 template <int DM>
 __device__ __forceinline__ double2 matvec_adj_row(const double2* M, int d, int i, const double2* v) {
@@ -159,7 +183,7 @@ __device__ __forceinline__ double2 matvec_adj_row(const double2* M, int d, int i
   return i < d ? cadd(a, b) : cx(0.0, 0.0);
 }
 
-template <bool TRI, int DM>
+template <bool TRI, int DM, int DIM = 0>
 __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, TaskArgs A, int chunk, int nchunk,
                                                       int ignore_done) {
   __shared__ PcSmem<32> sm_all[4];
@@ -170,7 +194,7 @@ __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, Ta
   if (item >= P.L * nchunk) return;
   PcSmem<32>& S = sm_all[warp];
   const int n = item / nchunk, ch = item % nchunk;
-  const int d = P.d, C = P.C, mode = A.mode;
+  const int d = DIM > 0 ? DIM : P.d, C = P.C, mode = A.mode;  // DIM: compile-time dimension
   const int node0 = P.node[n], len = P.node[n + 1] - node0;
   const int j0 = ch * chunk;
   const int j1 = min(len, j0 + chunk);
@@ -234,10 +258,21 @@ __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, Ta
   if (mode & (PC_GRAD | PC_ERR | PC_RAWGRAD)) {
     double2 psa, cha;
     matvec_row2<DM>(Pc + (size_t)j0 * dd, d, i, S.phi, S.chi0, psa, cha);
+    // compile-time dimension: software pipeline, the row of P_{j+2} is in flight while step j
+    // computes with P_{j+1} (the registers it costs only pay off when d is fixed)
+    constexpr int DP = DIM > 0 ? DM : 1;
+    double2 rcur[DP], rnext[DP];
+    if constexpr (DIM > 0) load_row<DP>(Pc + (size_t)(j0 + 1) * dd, d, i, rcur);
     for (int j = j0; j < j1; ++j) {
-      const double2* Pj1 = Pc + (size_t)(j + 1) * dd;
       double2 psb, chb;
-      matvec_row2<DM>(Pj1, d, i, S.phi, S.chi0, psb, chb);
+      if constexpr (DIM > 0) {
+        if (j + 2 <= j1) load_row<DP>(Pc + (size_t)(j + 2) * dd, d, i, rnext);
+        rows_dot2<DP>(rcur, d, i, S.phi, S.chi0, psb, chb);
+#pragma unroll
+        for (int k = 0; k < DP; ++k) rcur[k] = rnext[k];
+      } else {
+        matvec_row2<DM>(Pc + (size_t)(j + 1) * dd, d, i, S.phi, S.chi0, psb, chb);
+      }
       const double2 ps = cadd(psa, psb), cs = cadd(cha, chb);
       const double* uj = u + (size_t)j * C;
       const double aj = P.alpha[node0 + j] * scale;
@@ -402,7 +437,8 @@ cudaError_t pc_eval(const DevProblem& P, const DevRun& R, const TaskArgs& A, int
   dim3 grid((P.L * nchunk + 3) / 4, P.B);
   const bool small = P.d <= 16;  // narrower register arrays -> higher occupancy
   if (P.kind == QOC_KIND_TRIDIAG) {
-    if (small) pc_eval_kernel<true, 16><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
+    if (P.d == 21) pc_eval_kernel<true, 24, 21><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
+    else if (small) pc_eval_kernel<true, 16><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
     else pc_eval_kernel<true, 32><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
   } else {
     if (small) pc_eval_kernel<false, 16><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
