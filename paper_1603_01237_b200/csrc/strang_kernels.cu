@@ -71,9 +71,10 @@ __device__ void transform(const StrangCtx& X, const double2* src, double2* dst, 
     double2* in = const_cast<double2*>(src);
     double2* out = dst;
     bool first = true;
-    for (int Ns = 1; Ns < d;) {
-      const int R = (Ns * 4 <= d) ? 4 : 2;
-      const int nb = d / R;
+    for (int Ns = 1, lNs = 0; Ns < d;) {
+      const int R = (Ns * 4 <= d) ? 4 : 2, lR = R == 4 ? 2 : 1;
+      const int nb = d >> lR;
+      const int tws = X.log2d - lNs - lR;  // twiddle index = jm * r << tws  (d / (Ns R) = 2^tws)
       for (int j = t; j < nb; j += ST_T) {
         const int jm = j & (Ns - 1);  // j % Ns
         double2 v[4];
@@ -86,7 +87,7 @@ __device__ void transform(const StrangCtx& X, const double2* src, double2* dst, 
               if (scale != 1.0) x = cscale(x, scale);
             }
             if (r > 0 && jm != 0) {  // twiddle exp(sign 2 pi i jm r / (Ns R))
-              int k = jm * r * (d / (Ns * R));
+              const int k = (jm * r) << tws;
               double2 w;
               if (k < d / 2) {
                 w = X.tw[k];
@@ -100,7 +101,7 @@ __device__ void transform(const StrangCtx& X, const double2* src, double2* dst, 
             v[r] = x;
           }
         }
-        const int idxD = (j / Ns) * Ns * R + jm;
+        const int idxD = ((j >> lNs) << (lNs + lR)) + jm;
         if (R == 4) {
           const double2 a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]), a2 = cadd(v[1], v[3]);
           const double2 dd = csub(v[1], v[3]);
@@ -116,7 +117,8 @@ __device__ void transform(const StrangCtx& X, const double2* src, double2* dst, 
       }
       __syncthreads();
       first = false;
-      Ns *= R;
+      Ns <<= lR;
+      lNs += lR;
       double2* tmp = in;
       in = out;
       out = tmp;
