@@ -347,6 +347,7 @@ __global__ void __launch_bounds__(1 << LOG2T) bitflip_task_kernel(DevProblem P, 
 // blockIdx.y = 1: adjoint nodes chi_n seeded with the target (ism.cpp:72), which = 0 only.
 template <int LOG2E, int LOG2T>
 __global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_kernel(DevProblem P, DevRun R, int which, int k) {
+  if (R.kdev) k = *R.kdev;
   using F_ = Bf<LOG2E, LOG2T>;
   constexpr int E = 1 << LOG2E, T = 1 << LOG2T;
   const int b = blockIdx.x, dir = blockIdx.y;

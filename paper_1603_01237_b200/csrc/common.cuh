@@ -159,6 +159,7 @@ struct DevRun {
   double* tot_err;      // [B] summed task residual of the current iteration
   int* err_flags;       // [1] bit 1: a structured solve would have needed pivoting
   // propagator-cache engine (pcache.cu)
+  const int* kdev;      // outer-iteration index read on the device (CUDA-graph replays), or null
   double2* pc;          // [B][L][traj_len][d][d] partial products P_j (row-major)
   double* chunk_pen;    // [B][L][nchunk]
   double* chunk_err;    // [B][L][nchunk]

@@ -281,6 +281,7 @@ __global__ void __launch_bounds__(256) dense_task_kernel(DevProblem P, DevRun R,
 //   which = 1: overlap payoff of the full propagation minus the full penalty -> rec_exact[k]
 template <int D, int G>
 __global__ void __launch_bounds__(32) dense_horizon_kernel(DevProblem P, DevRun R, int which, int k) {
+  if (R.kdev) k = *R.kdev;
   using K_ = DenseKernel<D, G>;
   constexpr int NL = K_::NL, COLS = K_::COLS;
   extern __shared__ __align__(16) unsigned char smem_raw[];

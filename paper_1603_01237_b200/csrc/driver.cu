@@ -37,6 +37,8 @@ struct qoc_ctx {
   qoc_profile_v1 prof{};
   // event pairs of the current run: (start, stop, is_task)
   std::vector<std::tuple<cudaEvent_t, cudaEvent_t, bool>> marks;
+  int* khost = nullptr;        // pinned iteration indices for graph replays
+  size_t khost_n = 0;
   void* prob_slots = nullptr;  // Slots* (driver.cu anonymous namespace)
   void* run_slots = nullptr;
 };
@@ -525,6 +527,7 @@ void qoc_ctx_destroy(qoc_ctx* ctx) {
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->flush_buf) cudaFree(ctx->flush_buf);
+  if (ctx->khost) cudaFreeHost(ctx->khost);
   delete static_cast<Slots*>(ctx->prob_slots);
   delete static_cast<Slots*>(ctx->run_slots);
   delete ctx;
@@ -635,62 +638,130 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
       for (auto& e : ev_end) ck(cudaEventCreate(&e), "event");
       int ran = 0;
       launch.in_iteration = true;
-      for (int k = 1; k <= max_outer; ++k) {
-        if (ctx->flush_bytes > 0) {  // cold L2 for every iteration, outside the brackets
-          ck(cudaMemsetAsync(ctx->flush_buf, k & 0xff, (size_t)ctx->flush_bytes, st), "flush");
-          ck(cudaEventRecord(ev[k], st), "event");
-        }
+      // One outer iteration (ism.cpp:396-592) as a launch sequence on `st` (+ the side stream).
+      auto body = [&](const DevRun& RR, int k) {
         if (pcache) {
           // gradient + update through the cache, then the assembly sweep at the new control,
           // then residual / lagged endpoints through the new cache
           const TaskArgs G{PCM_ENTRY | PCM_GRAD, form, split ? 0 : 1, 1, solver->step_size};
-          launch.run([&] { return pc_eval(P, R, G, 0, st); }, "gradient", true);
+          launch.run([&] { return pc_eval(P, RR, G, 0, st); }, "gradient", true);
           for (int it = 1; it < std::max(1, solver->inner_iterations); ++it) {
-            launch.run([&] { return pc_assemble(P, R, 0, st); }, "assembly", true);
+            launch.run([&] { return pc_assemble(P, RR, 0, st); }, "assembly", true);
             const TaskArgs G2{PCM_GRAD, form, split ? 0 : 1, 1, solver->step_size};
-            launch.run([&] { return pc_eval(P, R, G2, 0, st); }, "gradient", true);
+            launch.run([&] { return pc_eval(P, RR, G2, 0, st); }, "gradient", true);
           }
-          launch.run([&] { return pc_assemble(P, R, 0, st); }, "assembly", true);
+          launch.run([&] { return pc_assemble(P, RR, 0, st); }, "assembly", true);
           if (assembled_interp) {
             // the boundary chain needs only the new propagators: run it on the side stream,
             // concurrently with the residual sweep, penalty and merge (joined before boundary)
             ck(cudaEventRecord(ctx->ev_fork, st), "fork");
             ck(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0), "fork");
-            launch(chain_propagators(P, R, ctx->aux), "chain");
+            launch(chain_propagators(P, RR, ctx->aux), "chain");
             ck(cudaEventRecord(ctx->ev_join, ctx->aux), "join");
           }
           const int em = (cfg->compute_error ? PCM_ERR : 0) | ((L > 1 && split && !direct) ? PCM_LAG : 0);
           if (em) {
             const TaskArgs E{em, form, split ? 0 : 1, 1, 0.0};
-            launch.run([&] { return pc_eval(P, R, E, 0, st); }, "residual", true);
+            launch.run([&] { return pc_eval(P, RR, E, 0, st); }, "residual", true);
           }
         } else {
-          launch.run([&] { return task(P, R, A, 0, st); }, "task", true);
+          launch.run([&] { return task(P, RR, A, 0, st); }, "task", true);
         }
-        launch.run([&] { return penalty_partials(P, R, 0, st); }, "penalty");
-        launch.run([&] { return merge_iteration(P, R, k, nullptr, st); }, "merge");
+        launch.run([&] { return penalty_partials(P, RR, 0, st); }, "penalty");
+        launch.run([&] { return merge_iteration(P, RR, k, nullptr, st); }, "merge");
         if (L > 1) {
-          if (direct) launch.run([&] { return horizon(P, R, 0, k, st); }, "node sweeps", true);
-          else if (split) launch.run([&] { return split_nodes(P, R, st); }, "split nodes");
+          if (direct) launch.run([&] { return horizon(P, RR, 0, k, st); }, "node sweeps", true);
+          else if (split) launch.run([&] { return split_nodes(P, RR, st); }, "split nodes");
           else if (pcache) ck(cudaStreamWaitEvent(st, ctx->ev_join, 0), "join");
-          else launch.run([&] { return chain_propagators(P, R, st); }, "chain");
-          launch.run([&] { return boundary_update(P, R, k, split, 0, st); }, "boundary");
+          else launch.run([&] { return chain_propagators(P, RR, st); }, "chain");
+          launch.run([&] { return boundary_update(P, RR, k, split, 0, st); }, "boundary");
         }
-        if (cfg->log_exact_objective) launch.run([&] { return horizon(P, R, 1, k, st); }, "exact objective", true);
-        launch.run([&] { return finish_iteration_ex(P, R, k, cfg->compute_error, cfg->eta,
+        if (cfg->log_exact_objective) launch.run([&] { return horizon(P, RR, 1, k, st); }, "exact objective", true);
+        launch.run([&] { return finish_iteration_ex(P, RR, k, cfg->compute_error, cfg->eta,
                                                     cfg->log_exact_objective, st); }, "finish");
-        ck(cudaEventRecord(ev_end[k + 1], st), "event");
-        if (ctx->flush_bytes <= 0) ck(cudaEventRecord(ev[k + 1], st), "event");
-        ran = k;
-        if (k % 8 == 0 || k == max_outer) {  // early exit once every problem stopped
-          ck(cudaMemcpyAsync(h_done.data(), R.done, sizeof(int) * B, cudaMemcpyDeviceToHost, st), "poll");
-          ck(cudaMemcpyAsync(h_status.data(), R.status, sizeof(int) * B, cudaMemcpyDeviceToHost, st), "poll");
-          ck(cudaStreamSynchronize(st), "poll");
-          bool all = true;
-          for (int b = 0; b < B; ++b) all = all && (h_done[b] || h_status[b]);
-          if (all) break;
+      };
+      // Long runs replay the iteration as one CUDA graph (captured once; the iteration index
+      // is read from device memory), which removes the per-kernel launch gaps of the small
+      // latency-bound configs.  Profiling mode keeps direct launches (per-launch events).
+      bool use_graph = !ctx->profile && max_outer >= 8;
+      cudaGraphExec_t gexec = nullptr;
+      int* kdev = nullptr;
+      int64_t launches_per_body = 0;
+      DevRun RG = R;
+      if (use_graph) {
+        kdev = dr.alloc<int>(1);
+        RG.kdev = kdev;
+        if ((int)ctx->khost_n < max_outer + 2) {
+          if (ctx->khost) cudaFreeHost(ctx->khost);
+          ctx->khost = nullptr;
+          ctx->khost_n = 0;
+          ck(cudaHostAlloc(reinterpret_cast<void**>(&ctx->khost), sizeof(int) * (max_outer + 2), cudaHostAllocDefault),
+             "pinned iteration index");
+          ctx->khost_n = max_outer + 2;
         }
+        for (int k = 0; k < max_outer + 2; ++k) ctx->khost[k] = k;
       }
+      auto destroy_graph = [&] {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        gexec = nullptr;
+      };
+      try {
+        for (int k = 1; k <= max_outer; ++k) {
+          if (ctx->flush_bytes > 0) {  // cold L2 for every iteration, outside the brackets
+            ck(cudaMemsetAsync(ctx->flush_buf, k & 0xff, (size_t)ctx->flush_bytes, st), "flush");
+            ck(cudaEventRecord(ev[k], st), "event");
+          }
+          if (use_graph) {
+            ck(cudaMemcpyAsync(kdev, ctx->khost + k, sizeof(int), cudaMemcpyHostToDevice, st), "iteration index");
+            if (!gexec) {
+              const int64_t l0 = ctx->launches, i0 = ctx->prof.iteration_launches;
+              cudaGraph_t graph = nullptr;
+              bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+              if (ok) {
+                try {
+                  body(RG, k);
+                } catch (...) {
+                  ok = false;
+                }
+                ok = (cudaStreamEndCapture(st, &graph) == cudaSuccess) && ok && graph;
+                if (ok) ok = cudaGraphInstantiate(&gexec, graph, 0) == cudaSuccess;
+                if (graph) cudaGraphDestroy(graph);
+              }
+              launches_per_body = ctx->launches - l0;  // counted during capture, added per replay
+              ctx->launches = l0;
+              ctx->prof.iteration_launches = i0;
+              if (!ok) {  // capture unsupported here: fall back to direct launches
+                cudaGetLastError();
+                gexec = nullptr;
+                use_graph = false;
+                body(R, k);
+              }
+            }
+            if (use_graph) {
+              ck(cudaGraphLaunch(gexec, st), "graph launch");
+              ctx->launches += launches_per_body;
+              ctx->prof.iteration_launches += launches_per_body;
+            }
+          } else {
+            body(R, k);
+          }
+          ck(cudaEventRecord(ev_end[k + 1], st), "event");
+          if (ctx->flush_bytes <= 0) ck(cudaEventRecord(ev[k + 1], st), "event");
+          ran = k;
+          if (k % 8 == 0 || k == max_outer) {  // early exit once every problem stopped
+            ck(cudaMemcpyAsync(h_done.data(), R.done, sizeof(int) * B, cudaMemcpyDeviceToHost, st), "poll");
+            ck(cudaMemcpyAsync(h_status.data(), R.status, sizeof(int) * B, cudaMemcpyDeviceToHost, st), "poll");
+            ck(cudaStreamSynchronize(st), "poll");
+            bool all = true;
+            for (int b = 0; b < B; ++b) all = all && (h_done[b] || h_status[b]);
+            if (all) break;
+          }
+        }
+      } catch (...) {
+        destroy_graph();
+        throw;
+      }
+      destroy_graph();
       launch.in_iteration = false;
       // ---- trailing evaluation (ism.cpp:594-609)
       {

@@ -60,6 +60,7 @@ __global__ void penalty_kernel(DevProblem P, DevRun R, int ignore_done) {
 
 // Index-order merge of task results (ism.cpp:481-539).
 __global__ void merge_kernel(DevProblem P, DevRun R, int k) {
+  if (R.kdev) k = *R.kdev;  // graph replay: the iteration index lives on the device
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= P.B || R.done[b] || R.status[b]) return;
   double tot = 0.0, esum = 0.0;
@@ -214,6 +215,7 @@ __global__ void split_nodes_kernel(DevProblem P, DevRun R) {
 // Finite checks of the nodes, boundary objective, task rebuild.
 template <int NT>
 __global__ void __launch_bounds__(NT) boundary_kernel(DevProblem P, DevRun R, int k, int split, int boot) {
+  if (R.kdev) k = *R.kdev;  // graph replay: the iteration index lives on the device
   __shared__ double sh[NT];
   __shared__ int bad_sh;
   const int b = blockIdx.x;
@@ -290,6 +292,7 @@ __global__ void single_tasks_kernel(DevProblem P, DevRun R) {
 
 // Record the residual, stop on eta (ism.cpp:586-591).
 __global__ void finish_kernel(DevProblem P, DevRun R, int k, int compute_error, double eta, int log_exact) {
+  if (R.kdev) k = *R.kdev;  // graph replay: the iteration index lives on the device
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= P.B || R.done[b] || R.status[b]) return;
   const size_t r = (size_t)b * R.cap + k;

@@ -418,6 +418,7 @@ __global__ void __launch_bounds__(ST_T) strang_task_kernel(DevProblem P, DevRun 
 // the exact payoff (which = 1).  One CTA per problem; the trajectory uses the problem's task
 // workspace (L * traj_len >= K + 1 states).
 __global__ void __launch_bounds__(ST_T) strang_horizon_kernel(DevProblem P, DevRun R, int which, int k) {
+  if (R.kdev) k = *R.kdev;
   const int b = blockIdx.x;
   if (R.done[b] || R.status[b]) return;
   extern __shared__ __align__(16) unsigned char smem[];

@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(32) tridiag_task_kernel(DevProblem P, DevRun R
 
 template <int TD>
 __global__ void __launch_bounds__(32) tridiag_horizon_kernel(DevProblem P, DevRun R, int which, int k) {
+  if (R.kdev) k = *R.kdev;
   const int b = blockIdx.x, lane = threadIdx.x;
   if (R.done[b] || R.status[b] || lane != 0) return;
   const int d = P.d, C = P.C;
