@@ -478,6 +478,8 @@ struct TwistFactors {
   double2 as[TRI_CHUNK][TD];   // a_i = s sb_i (sub)
   double2 kf[TRI_CHUNK][TD];   // bottom: k_i = c_i / w_{i+1} (i = m..d-2)
   double2 wi[TRI_CHUNK][TD];   // bottom: 1 / w_i (i = m+1..d-1)
+  double2 cu[TRI_CHUNK][TD];   // top: c_i / u_i  (back substitution z_i = z'_i/u_i - (c_i/u_i) z_{i+1})
+  double2 au[TRI_CHUNK][TD];   // bottom: a_i / w_i
   double2 gm[TRI_CHUNK];       // 1 / gamma_m
   double2 bm[TRI_CHUNK];       // b_m (middle diagonal)
   double2 zt[2][32];           // z'_{m-1} per column (top -> middle), double-buffered by step
@@ -539,7 +541,10 @@ __global__ void __launch_bounds__(64) tri_pc_assemble2_kernel(DevProblem P, DevR
           if (i <= m) {
             F.lf[lane][i] = lf;
             F.cs[lane][i] = ci;
-            if (i < m) F.ui[lane][i] = uinv_prev;
+            if (i < m) {
+              F.ui[lane][i] = uinv_prev;
+              F.cu[lane][i] = cmul(ci, uinv_prev);
+            }
             if (i == m) F.bm[lane] = bi;
           }
           dg = dgn;
@@ -565,6 +570,7 @@ __global__ void __launch_bounds__(64) tri_pc_assemble2_kernel(DevProblem P, DevR
           if (i > m) {
             winv_next = crcp(wi);
             F.wi[lane][i] = winv_next;
+            F.au[lane][i] = cmul(ai, winv_next);
           }
         }
       }
@@ -587,6 +593,9 @@ __global__ void __launch_bounds__(64) tri_pc_assemble2_kernel(DevProblem P, DevR
 #pragma unroll
         for (int i = 0; i < TD; ++i)
           if (i + 1 == m) F.zt[par][lane] = z[i];  // static register index
+#pragma unroll
+        for (int i = 0; i < TD; ++i)
+          if (i < m) z[i] = cmul(z[i], F.ui[q][i]);  // z'_i / u_i, off the back-substitution chain
       } else {
 #pragma unroll
         for (int i = TD - 1; i >= 0; --i)
@@ -594,6 +603,9 @@ __global__ void __launch_bounds__(64) tri_pc_assemble2_kernel(DevProblem P, DevR
 #pragma unroll
         for (int i = 0; i < TD; ++i)
           if (i == m + 1 && i < d) F.zb[par][lane] = z[i];
+#pragma unroll
+        for (int i = 0; i < TD; ++i)
+          if (i < d && i > m) z[i] = cmul(z[i], F.wi[q][i]);
       }
       __syncthreads();
       // middle row (both warps, identical arithmetic)
@@ -611,8 +623,7 @@ __global__ void __launch_bounds__(64) tri_pc_assemble2_kernel(DevProblem P, DevR
 #pragma unroll
         for (int i = TD - 1; i >= 0; --i) {
           if (i < m) {
-            const double2 v = cfms(F.cs[q][i], zn, z[i]);
-            zn = cmul(v, F.ui[q][i]);
+            zn = cfms(F.cu[q][i], zn, z[i]);  // one complex FMA per row on the chain
             x[i] = cx(fma(2.0, zn.x, -x[i].x), fma(2.0, zn.y, -x[i].y));
             if (col) dst[(size_t)i * d + lane] = x[i];
           }
@@ -622,8 +633,7 @@ __global__ void __launch_bounds__(64) tri_pc_assemble2_kernel(DevProblem P, DevR
 #pragma unroll
         for (int i = 0; i < TD; ++i) {
           if (i < d && i > m) {
-            const double2 v = cfms(F.as[q][i], zp, z[i]);
-            zp = cmul(v, F.wi[q][i]);
+            zp = cfms(F.au[q][i], zp, z[i]);
             x[i] = cx(fma(2.0, zp.x, -x[i].x), fma(2.0, zp.y, -x[i].y));
             if (col) dst[(size_t)i * d + lane] = x[i];
           }
