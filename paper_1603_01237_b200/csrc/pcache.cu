@@ -102,6 +102,12 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
   return v;
 }
+template <int NL>
+__device__ __forceinline__ double group_sum(double v) {  // sum over aligned groups of NL lanes
+#pragma unroll
+  for (int off = NL / 2; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
 
 // y_i = sum_k M[i][k] v_k (M row-major d x d, v in smem); lanes >= d return 0.  The row is
 // loaded with every load in flight at once (these reads are HBM-latency-bound).
@@ -183,21 +189,29 @@ __device__ __forceinline__ double2 matvec_adj_row(const double2* M, int d, int i
   return i < d ? cadd(a, b) : cx(0.0, 0.0);
 }
 
-template <bool TRI, int DM, int DIM = 0>
+// NLT lanes per (task, chunk) item: 32, or 16 for d <= 16 (two items per warp; dense kinds
+// with one chunk per task -- every group of a warp then runs the same control flow).
+template <bool TRI, int DM, int DIM = 0, int NLT = 32>
 __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, TaskArgs A, int chunk, int nchunk,
                                                       int ignore_done) {
-  __shared__ PcSmem<32> sm_all[4];
+  constexpr int GPW = 32 / NLT;
+  __shared__ PcSmem<32> sm_all[4 * GPW];
   const int b = blockIdx.y;
   if (ignore_done ? R.status[b] : R.done[b]) return;
-  const int warp = threadIdx.x >> 5, i = threadIdx.x & 31;
-  const int item = blockIdx.x * 4 + warp;
-  if (item >= P.L * nchunk) return;
-  PcSmem<32>& S = sm_all[warp];
+  const int warp = threadIdx.x >> 5, i = threadIdx.x & (NLT - 1), gid = (threadIdx.x & 31) / NLT;
+  const int item_raw = (blockIdx.x * 4 + warp) * GPW + gid;
+  const bool live = item_raw < P.L * nchunk;
+  if (!__any_sync(0xffffffffu, live)) return;
+  const int item = live ? item_raw : P.L * nchunk - 1;
+  PcSmem<32>& S = sm_all[warp * GPW + gid];
   const int n = item / nchunk, ch = item % nchunk;
   const int d = DIM > 0 ? DIM : P.d, C = P.C, mode = A.mode;  // DIM: compile-time dimension
   const int node0 = P.node[n], len = P.node[n + 1] - node0;
   const int j0 = ch * chunk;
   const int j1 = min(len, j0 + chunk);
+  int jmax = j1;  // uniform trip count over the warp's groups
+#pragma unroll
+  for (int off = 16; off >= NLT; off >>= 1) jmax = max(jmax, __shfl_xor_sync(0xffffffffu, jmax, off));
   const double Kd = (double)P.K;
   const double weight = A.weighted ? Kd / (double)len : 1.0;
   const double scale = (double)len / Kd;
@@ -226,10 +240,10 @@ __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, Ta
     if (mode & PC_ENTRY) {  // payoff of the task (objective.cpp:22-29)
       double t = 0.0;
       if (i < d) t = A.form == 0 ? cconjmul(targ, psiL).x : cabs2(csub(psiL, targ));
-      const double s = warp_sum(t);
-      if (i == 0) R.entry_pay[(size_t)b * P.L + n] = A.form == 0 ? (w * s) : (-0.5 * (w * s));
+      const double s = group_sum<NLT>(t);
+      if (i == 0 && live) R.entry_pay[(size_t)b * P.L + n] = A.form == 0 ? (w * s) : (-0.5 * (w * s));
     }
-    if ((mode & PC_FINAL) && i < d) R.psi_end[tix + i] = psiL;
+    if ((mode & PC_FINAL) && i < d && live) R.psi_end[tix + i] = psiL;
     if (mode & PC_LAG) {  // ism.cpp:424-459 through the cached product
       S.vec[i] = i < d ? R.psi_nodes[((size_t)b * (P.L + 1) + n) * d + i] : zero;
       __syncwarp();
@@ -238,7 +252,7 @@ __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, Ta
       S.vec[i] = i < d ? R.chi_nodes[((size_t)b * (P.L + 1) + n + 1) * d + i] : zero;
       __syncwarp();
       const double2 cs = matvec_adj_row<DM>(PL, d, i, S.vec);
-      if (i < d) {
+      if (i < d && live) {
         R.psi_end[tix + i] = pe;
         R.chi_start[tix + i] = cs;
       }
@@ -247,12 +261,12 @@ __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, Ta
   }
   // penalty of the task window at the current control (before any update of this chunk)
   double pen = 0.0;
-  for (int j = j0 + i; j < j1; j += 32) {
+  for (int j = j0 + i; j < j1; j += NLT) {
     double sq = 0.0;
     for (int c = 0; c < C; ++c) sq += u[(size_t)j * C + c] * u[(size_t)j * C + c];
     pen += (P.alpha[node0 + j] * scale) * sq;
   }
-  pen = warp_sum(pen);
+  pen = group_sum<NLT>(pen);
 
   double err = 0.0;
   if (mode & (PC_GRAD | PC_ERR | PC_RAWGRAD)) {
@@ -263,7 +277,9 @@ __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, Ta
     constexpr int DP = DIM > 0 ? DM : 1;
     double2 rcur[DP], rnext[DP];
     if constexpr (DIM > 0) load_row<DP>(Pc + (size_t)(j0 + 1) * dd, d, i, rcur);
-    for (int j = j0; j < j1; ++j) {
+    for (int jj = j0; jj < jmax; ++jj) {
+      const bool act = jj < j1;
+      const int j = act ? jj : j1 - 1;
       double2 psb, chb;
       if constexpr (DIM > 0) {
         if (j + 2 <= j1) load_row<DP>(Pc + (size_t)(j + 2) * dd, d, i, rnext);
@@ -289,22 +305,22 @@ __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, Ta
           h = i < d ? dense_dH_row<DM>(P, b, c, uc, i, S.vec) : zero;
           __syncwarp();
         }
-        const double im = warp_sum(i < d ? cconjmul(cs, h).y : 0.0);
+        const double im = group_sum<NLT>(i < d ? cconjmul(cs, h).y : 0.0);
         g[c] = -aj * dt * uc + 0.25 * dt * (w * im);  // gradient_sweep, objective.cpp:55-57
         sq += g[c] * g[c];
       }
-      if (i == 0) {
+      if (i == 0 && act && live) {
         for (int c = 0; c < C && c < 4; ++c) {
           if (mode & PC_RAWGRAD) R.grad[((size_t)b * P.K + node0 + j) * C + c] = g[c];
           if (mode & PC_GRAD) u[(size_t)j * C + c] = uj[c] + A.rho * (weight * g[c]);
         }
       }
-      err += sqrt(sq);
+      if (act) err += sqrt(sq);
       psa = psb;
       cha = chb;
     }
   }
-  if (i == 0) {
+  if (i == 0 && live) {
     R.chunk_pen[cix] = pen;
     R.chunk_err[cix] = err;
   }
@@ -441,8 +457,14 @@ cudaError_t pc_eval(const DevProblem& P, const DevRun& R, const TaskArgs& A, int
     else if (small) pc_eval_kernel<true, 16><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
     else pc_eval_kernel<true, 32><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
   } else {
-    if (small) pc_eval_kernel<false, 16><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
-    else pc_eval_kernel<false, 32><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
+    if (small && nchunk == 1) {  // two tasks per warp
+      const dim3 g2((P.L * nchunk + 7) / 8, P.B);
+      pc_eval_kernel<false, 16, 0, 16><<<g2, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
+    } else if (small) {
+      pc_eval_kernel<false, 16><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
+    } else {
+      pc_eval_kernel<false, 32><<<grid, 128, 0, st>>>(P, R, A, chunk, nchunk, ignore_done);
+    }
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
