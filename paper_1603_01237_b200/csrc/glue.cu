@@ -59,23 +59,32 @@ __global__ void penalty_kernel(DevProblem P, DevRun R, int ignore_done) {
 }
 
 // Index-order merge of task results (ism.cpp:481-539).
-__global__ void merge_kernel(DevProblem P, DevRun R, int k) {
+// One block per problem: the L task results are reduced in a fixed tree order (deterministic).
+__global__ void __launch_bounds__(128) merge_kernel(DevProblem P, DevRun R, int k) {
   if (R.kdev) k = *R.kdev;  // graph replay: the iteration index lives on the device
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= P.B || R.done[b] || R.status[b]) return;
+  __shared__ double sh[128];
+  __shared__ int bad_sh;
+  const int b = blockIdx.x;
+  if (R.done[b] || R.status[b]) return;
+  if (threadIdx.x == 0) bad_sh = 0;
   double tot = 0.0, esum = 0.0;
   int bad = 0;
   double* tv = R.rec_tv + ((size_t)b * R.cap + (k - 1)) * P.L;
-  for (int n = 0; n < P.L; ++n) {
+  for (int n = threadIdx.x; n < P.L; n += 128) {
     const double e = R.entry[(size_t)b * P.L + n];
     tv[n] = e;
     esum += e;
     tot += R.err[(size_t)b * P.L + n];
     bad |= R.bad_u[(size_t)b * P.L + n];
   }
+  __syncthreads();
+  if (bad) atomicOr(&bad_sh, 1);
+  tot = block_sum<128>(tot, sh);
+  if (P.L == 1) esum = block_sum<128>(esum, sh);
+  if (threadIdx.x != 0) return;
   if (P.L == 1) R.rec_obj[(size_t)b * R.cap + (k - 1)] = esum;
   R.tot_err[b] = tot;
-  if (bad) {
+  if (bad_sh) {
     R.status[b] = 1;
     R.abort_iter[b] = k;
     R.rec_obj[(size_t)b * R.cap + k] = qnan();
@@ -248,6 +257,9 @@ __global__ void __launch_bounds__(NT) boundary_kernel(DevProblem P, DevRun R, in
     else part += cabs2(csub(last[i], tg[i]));
   }
   const double s = block_sum<NT>(part, sh);
+  double penp = 0.0;
+  for (int n = threadIdx.x; n < L; n += NT) penp += R.pen[(size_t)b * L + n];
+  const double pen = block_sum<NT>(penp, sh);
   if (threadIdx.x == 0) {
     double fid;
     if (split) {
@@ -256,8 +268,6 @@ __global__ void __launch_bounds__(NT) boundary_kernel(DevProblem P, DevRun R, in
       const double dist = sqrt(fmax(0.0, P.ip_w * s));
       fid = -0.5 * dist * dist;
     }
-    double pen = 0.0;
-    for (int n = 0; n < L; ++n) pen += R.pen[(size_t)b * L + n];
     R.rec_obj[(size_t)b * R.cap + k] = fid - 0.5 * P.dt * pen;
   }
   // rebuild_tasks (ism.cpp:260-280)
@@ -320,7 +330,7 @@ cudaError_t penalty_partials(const DevProblem& P, const DevRun& R, int ignore_do
   return cudaGetLastError();
 }
 cudaError_t merge_iteration(const DevProblem& P, const DevRun& R, int k, double*, cudaStream_t st) {
-  merge_kernel<<<(P.B + 127) / 128, 128, 0, st>>>(P, R, k);
+  merge_kernel<<<P.B, 128, 0, st>>>(P, R, k);
   return cudaGetLastError();
 }
 cudaError_t chain_propagators(const DevProblem& P, const DevRun& R, cudaStream_t st) {
@@ -353,7 +363,10 @@ cudaError_t split_nodes(const DevProblem& P, const DevRun& R, cudaStream_t st) {
   return cudaGetLastError();
 }
 cudaError_t boundary_update(const DevProblem& P, const DevRun& R, int k, int split, int boot, cudaStream_t st) {
-  boundary_kernel<128><<<P.B, 128, 0, st>>>(P, R, k, split, boot);
+  if (P.B <= 64 && P.L * P.d >= 1024)  // few problems, many nodes: wider blocks hide the L2 latency
+    boundary_kernel<512><<<P.B, 512, 0, st>>>(P, R, k, split, boot);
+  else
+    boundary_kernel<128><<<P.B, 128, 0, st>>>(P, R, k, split, boot);
   return cudaGetLastError();
 }
 cudaError_t set_single_tasks(const DevProblem& P, const DevRun& R, cudaStream_t st) {
