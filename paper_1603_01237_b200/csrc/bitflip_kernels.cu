@@ -451,7 +451,9 @@ cudaError_t bitflip_horizon(const DevProblem& P, const DevRun& R, int which, int
     case 7: return launch_horizon<0, 7>(P, R, which, k, st);
     case 8: return launch_horizon<0, 8>(P, R, which, k, st);
     case 9: return launch_horizon<0, 9>(P, R, which, k, st);
-    case 10: return launch_horizon<1, 9>(P, R, which, k, st);
+    // node sweeps at d = 1024: 128 threads x 8 amplitudes (measured per outer iteration of
+    // config 3: 24.3 ms, vs 25.2 / 25.9 / 36.3 ms at 256 / 512 / 1024 threads)
+    case 10: return launch_horizon<3, 7>(P, R, which, k, st);
     case 11: return launch_horizon<2, 9>(P, R, which, k, st);
     case 12: return launch_horizon<3, 9>(P, R, which, k, st);
   }
