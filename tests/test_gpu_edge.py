@@ -1,0 +1,68 @@
+"""Device edge cases of run_ism (ism.cpp:213-231,385-391,527-539,589-591): input rejection,
+the eta stop, one-step subintervals, ragged partitions, and the numerical abort path, each
+compared with the CPU oracle."""
+import numpy as np
+import pytest
+
+from paper_1603_01237_b200 import ism as I
+from tests import oracle_api as O
+
+pytestmark = pytest.mark.gpu
+
+
+def test_input_rejection_matches_reference(ctx):
+    p, u = O.dense_fixture(2900)
+    sv = I.SolverSpec(step_size=0.1)
+    for bad in (I.IsmConfig(subintervals=0), I.IsmConfig(workers=0), I.IsmConfig(max_outer=-1),
+                I.IsmConfig(eta=-1.0)):
+        with pytest.raises(I.InvalidArgument):
+            I.run_ism(p, u, bad, sv, ctx)
+    with pytest.raises(I.LogicError):
+        I.run_ism(p, u, I.IsmConfig(max_outer=1), I.SolverSpec(kind="newton"), ctx)
+    with pytest.raises(I.QocRuntimeError):  # Decomposition::uniform with K % L != 0
+        I.run_ism(p, u, I.IsmConfig(subintervals=5, max_outer=1, partition="uniform"), sv, ctx)
+    with pytest.raises(I.QocRuntimeError):  # more parts than steps
+        I.run_ism(p, u, I.IsmConfig(subintervals=p.grid.steps + 1, max_outer=1), sv, ctx)
+
+
+def test_eta_stop(ctx):
+    p, u = O.dense_fixture(2800)
+    cfg = I.IsmConfig(subintervals=2, max_outer=50, eta=1e9)
+    g = I.run_ism(p, u, cfg, I.SolverSpec(step_size=0.1), ctx)
+    r = O.ism_run(p, u, cfg, I.SolverSpec(step_size=0.1))[0]
+    assert len(g.record.iterations) == len(r.record.iterations) == 2
+    assert np.max(np.abs(g.control - r.control)) < 1e-13
+
+
+@pytest.mark.parametrize("parts", [16, 11])  # one-step tasks (L = K) and a ragged partition
+def test_extreme_partitions(ctx, parts):
+    p, u = O.dense_fixture(2601, steps=16, random_penalty=True)
+    cfg = I.IsmConfig(subintervals=parts, max_outer=12, eta=0.0)  # >= 8 iterations: graph replay
+    sv = I.SolverSpec(step_size=0.5)
+    g = I.run_ism(p, u, cfg, sv, ctx)
+    r = O.ism_run(p, u, cfg, sv, O.REFERENCE)[0]
+    assert np.max(np.abs(g.control - r.control)) < 1e-12
+    assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-12
+
+
+def test_abort_on_non_finite_controls(ctx):
+    # an absurd step drives the controls to inf/nan: the run stops with the reference's reason
+    p, u = O.dense_fixture(2700, random_penalty=True)
+    cfg = I.IsmConfig(subintervals=4, max_outer=40, eta=0.0)
+    sv = I.SolverSpec(step_size=1e300)
+    g = I.run_ism(p, u, cfg, sv, ctx)
+    r = O.ism_run(p, u, cfg, sv)[0]
+    assert r.record.aborted and g.record.aborted
+    assert g.record.abort_reason == r.record.abort_reason
+    assert len(g.record.iterations) == len(r.record.iterations)
+
+
+def test_batch_members_stop_independently(ctx):
+    # two problems of a batch: the per-problem stop/abort state lives on the device
+    from paper_1603_01237_b200 import problems
+    w = problems.batch4096(batch=3, iterations=12, subintervals=8)
+    gs = I.run_ism_batch(w.problem, w.u0, w.config, w.solver, ctx)
+    rs = O.ism_run(w.problem, w.u0, w.config, w.solver, O.REFERENCE)
+    for g, r in zip(gs, rs):
+        assert np.max(np.abs(g.control - r.control)) / np.max(np.abs(r.control)) < 1e-11
+        assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-11
