@@ -12,7 +12,8 @@
 // is fixed per step from that a-priori bound (q^(k+1) <= 2^-54, as y = 2z - x doubles the error of z) instead of a data-dependent
 // stopping test, so every thread agrees without a reduction.
 //
-// Layout: one CTA of T = min(d, 512) threads per (problem, subinterval) task; thread t
+// Layout: one CTA of T = min(d, 512) threads per (problem, subinterval) task (the d = 1024
+// node sweeps use T = 128, E = 8, see bitflip_horizon); thread t
 // holds the E = d/T amplitudes s = t + e*T (all compile-time: one instantiation per n).  A flip of bit b pairs
 //   b < log2 T         -> thread t ^ 2^b      (shared memory, double buffer; one LDS.128 per
 //                                               partner -- cheaper than 4 SHFL for a double2)
