@@ -161,6 +161,7 @@ struct DevRun {
   // propagator-cache engine (pcache.cu)
   const int* kdev;      // outer-iteration index read on the device (CUDA-graph replays), or null
   double2* pc;          // [B][L][traj_len][d][d] partial products P_j (row-major)
+  double2* cay;         // [B][K][d][d] one-step Cayley matrices C_j (split dense assembly), or null
   double* chunk_pen;    // [B][L][nchunk]
   double* chunk_err;    // [B][L][nchunk]
   double* entry_pay;    // [B][L]

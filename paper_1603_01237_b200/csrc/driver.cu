@@ -376,6 +376,16 @@ void alloc_run(const DeviceProblem& dp, int cap, const std::vector<int>& node, b
   R.err_flags = out.alloc<int>(1);
   if (with_pc) {
     R.pc = out.alloc<double2>(pc_bytes(P, node) / sizeof(double2));
+    R.cay = nullptr;
+    // Few dense tasks (one lane group each would leave the GPU idle through a long dependent
+    // sweep): form every step's Cayley matrix in parallel first, then run the per-task matmul
+    // chain.  Many tasks (the batch) keep the fused sweep, which measured faster there.
+    if (P.kind == QOC_KIND_DENSE && P.d <= 16 && B * L <= 1024) {
+      const size_t cb = sizeof(double2) * B * K * d * d;
+      size_t freeb = 0, total = 0;
+      if (cudaMemGetInfo(&freeb, &total) == cudaSuccess && cb < freeb / 10 * 6)
+        R.cay = out.alloc<double2>(cb / sizeof(double2));
+    }
     const int nchunk = pc_nchunk(P, R);
     R.chunk_pen = out.alloc<double>(B * L * nchunk);
     R.chunk_err = out.alloc<double>(B * L * nchunk);

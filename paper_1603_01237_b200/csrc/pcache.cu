@@ -434,6 +434,161 @@ __global__ void __launch_bounds__(128) dense_pc_assemble_kernel(DevProblem P, De
 
 }  // namespace
 
+// ---- dense split assembly (few tasks): (1) every one-step Cayley matrix C_j = 2 B_j^-1 - I,
+// j < K, in parallel (one lane group per step); (2) per task the sequential product
+// P_{j+1} = C_j P_j, a pure matmul chain with the next C_j row prefetched into registers.
+template <int D>
+__global__ void __launch_bounds__(128) dense_cayley_kernel(DevProblem P, DevRun R, int steps_per_cta,
+                                                           int ignore_done) {
+  using Cfg = DenseCfg<D, 1>;
+  constexpr int NL = Cfg::NL, COLS = Cfg::COLS, TPW = Cfg::TPW;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* ops = reinterpret_cast<double2*>(smem_raw);
+  const int b = blockIdx.y;
+  if (ignore_done ? R.status[b] : R.done[b]) return;
+  const int nops = 1 + P.C + (P.has_quad ? P.C : 0);
+  const int d = P.d;
+  for (int e = threadIdx.x; e < nops * D * D; e += blockDim.x) {
+    const int o = e / (D * D), r = (e / D) % D, c = e % D;
+    double2 v = cx(0.0, 0.0);
+    if (r < d && c < d) {
+      const size_t dd = (size_t)d * d;
+      if (o == 0) v = P.h0[(size_t)b * dd + r * d + c];
+      else if (o <= P.C) v = P.lin[((size_t)b * P.C + (o - 1)) * dd + r * d + c];
+      else v = P.quad[((size_t)b * P.C + (o - 1 - P.C)) * dd + r * d + c];
+    }
+    ops[e] = v;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, l32 = threadIdx.x & 31;
+  const int gid = warp * TPW + l32 / NL, lane = l32 % NL;
+  const int j_raw = blockIdx.x * steps_per_cta + gid;
+  if (!__any_sync(0xffffffffu, j_raw < P.K)) return;
+  const int j = j_raw < P.K ? j_raw : P.K - 1;
+  const size_t gbytes = sizeof(double2) * (Cfg::PIV + Cfg::VEC + 2 * Cfg::MAT) + sizeof(int) * 2 * D;
+  unsigned char* sp = smem_raw + sizeof(double2) * (size_t)nops * D * D + gbytes * gid;
+  DenseScratch<D, 1> S;
+  S.piv = reinterpret_cast<double2*>(sp);
+  S.vec = S.piv + Cfg::PIV;
+  S.matW = S.vec + Cfg::VEC;
+  S.matP = S.matW + Cfg::MAT;
+  S.perm = reinterpret_cast<int*>(S.matP + Cfg::MAT);
+  DenseLane<D, 1> Ln;
+  Ln.row = lane;
+  Ln.g = 0;
+  const int C = P.C;
+  const double half = 0.5 * P.dt;
+  const double* uj = R.u + ((size_t)b * P.K + j) * C;
+  double2 W[COLS];
+  Ln.build(W, ops, C, P.has_quad, uj, half, false);
+  const double* nrm = P.norm1 + (size_t)b * (1 + 2 * C);
+  double bound = nrm[0];
+  for (int c = 0; c < C; ++c) {
+    bound += fabs(uj[c]) * nrm[1 + c];
+    if (P.has_quad) bound += 0.5 * uj[c] * uj[c] * nrm[1 + C + c];
+  }
+  if (__any_sync(0xffffffffu, !(half * bound < 1.0)))
+    Ln.invert_pivot(W, S, lane);
+  else
+    Ln.invert_fast(W, S.piv);
+  if (j_raw < P.K && lane < d) {
+    double2* dst = R.cay + ((size_t)b * P.K + j) * (size_t)d * d + (size_t)lane * d;
+#pragma unroll
+    for (int t = 0; t < COLS; ++t)
+      if (t < d) dst[t] = cx(2.0 * W[t].x - (t == lane ? 1.0 : 0.0), 2.0 * W[t].y);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) dense_pc_chain_kernel(DevProblem P, DevRun R, int tasks_per_cta,
+                                                             int ignore_done) {
+  constexpr int NL = D, TPW = 32 / D;
+  __shared__ __align__(16) double2 matP_all[(128 / 32) * TPW][D * D];
+  const int b = blockIdx.y;
+  if (ignore_done ? R.status[b] : R.done[b]) return;
+  const int warp = threadIdx.x >> 5, l32 = threadIdx.x & 31;
+  const int gid = warp * TPW + l32 / NL, row = l32 % NL;
+  const int n_raw = blockIdx.x * tasks_per_cta + gid;
+  const bool live_task = n_raw < P.L;
+  if (!__any_sync(0xffffffffu, live_task)) return;
+  const int n = live_task ? n_raw : P.L - 1;
+  const int d = P.d;
+  double2* matP = matP_all[gid];
+  const int node0 = P.node[n], len = P.node[n + 1] - node0;
+  int lenmax = len;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) lenmax = max(lenmax, __shfl_xor_sync(0xffffffffu, lenmax, off));
+  const size_t dd = (size_t)d * d;
+  double2* Pc = R.pc + ((size_t)b * P.L + n) * (size_t)R.traj_len * dd;
+  const double2* Cb = R.cay + ((size_t)b * P.K + node0) * dd;
+  const bool wr = live_task && row < d;
+  double2 Pm[D], cr[D], cn[D];
+#pragma unroll
+  for (int t = 0; t < D; ++t) Pm[t] = cx(row == t ? 1.0 : 0.0, 0.0);
+  if (wr)
+#pragma unroll
+    for (int t = 0; t < D; ++t)
+      if (t < d) Pc[(size_t)row * d + t] = Pm[t];
+  auto load_row = [&](int j, double2 (&r)[D]) {
+    const double2* src = Cb + (size_t)min(j, len - 1) * dd + (size_t)(row < d ? row : 0) * d;
+#pragma unroll
+    for (int t = 0; t < D; ++t) r[t] = t < d ? src[t] : cx(0.0, 0.0);
+  };
+  load_row(0, cr);
+  for (int j = 0; j < lenmax; ++j) {
+    if (j + 1 < lenmax) load_row(j + 1, cn);
+    const bool live = j < len;
+#pragma unroll
+    for (int t = 0; t < D; ++t) matP[row * D + t] = Pm[t];
+    __syncwarp();
+    double2 acc[D];
+#pragma unroll
+    for (int t = 0; t < D; ++t) acc[t] = cx(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+#pragma unroll
+      for (int t = 0; t < D; ++t) acc[t] = cfma(cr[k], matP[k * D + t], acc[t]);
+    }
+    __syncwarp();
+    if (live) {
+#pragma unroll
+      for (int t = 0; t < D; ++t) Pm[t] = acc[t];
+      if (wr) {
+        double2* dst = Pc + (size_t)(j + 1) * dd + (size_t)row * d;
+#pragma unroll
+        for (int t = 0; t < D; ++t)
+          if (t < d) dst[t] = Pm[t];
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < D; ++t) cr[t] = cn[t];
+  }
+  if (wr && R.prop) {
+    double2* M = R.prop + ((size_t)b * P.L + n) * dd + (size_t)row * d;
+#pragma unroll
+    for (int t = 0; t < D; ++t)
+      if (t < d) M[t] = Pm[t];
+  }
+}
+
+template <int D>
+static cudaError_t launch_dense_split(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st) {
+  using Cfg = DenseCfg<D, 1>;
+  constexpr int TPW = Cfg::TPW;
+  const int nops = 1 + P.C + (P.has_quad ? P.C : 0);
+  const size_t gbytes = sizeof(double2) * (Cfg::PIV + Cfg::VEC + 2 * Cfg::MAT) + sizeof(int) * 2 * D;
+  const int spc = 4 * TPW;  // steps per CTA (4 warps)
+  const size_t smem = sizeof(double2) * (size_t)nops * D * D + gbytes * spc;
+  auto kc = dense_cayley_kernel<D>;
+  cudaError_t e = cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kc<<<dim3((P.K + spc - 1) / spc, P.B), 128, smem, st>>>(P, R, spc, ignore_done);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const int tpc = 4 * TPW;
+  dense_pc_chain_kernel<D><<<dim3((P.L + tpc - 1) / tpc, P.B), 128, 0, st>>>(P, R, tpc, ignore_done);
+  return cudaGetLastError();
+}
+
 // ---- tridiagonal assembly sweep (defined in tridiag_kernels.cu) ---------------------------
 cudaError_t tri_pc_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st);
 
@@ -491,6 +646,15 @@ static cudaError_t launch_dense_pc(const DevProblem& P, const DevRun& R, int ign
 
 cudaError_t pc_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st) {
   if (P.kind == QOC_KIND_TRIDIAG) return tri_pc_assemble(P, R, ignore_done, st);
+  if (R.cay) {
+    switch (dense_pad(P.d)) {
+      case 2: return launch_dense_split<2>(P, R, ignore_done, st);
+      case 4: return launch_dense_split<4>(P, R, ignore_done, st);
+      case 8: return launch_dense_split<8>(P, R, ignore_done, st);
+      case 16: return launch_dense_split<16>(P, R, ignore_done, st);
+      default: break;
+    }
+  }
   switch (dense_pad(P.d)) {
     case 2: return launch_dense_pc<2>(P, R, ignore_done, st);
     case 4: return launch_dense_pc<4>(P, R, ignore_done, st);
