@@ -760,9 +760,23 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
                 }
                 ok = (cudaStreamEndCapture(st, &graph) == cudaSuccess) && ok && graph;
                 if (ok) ok = cudaGraphInstantiate(&gexec, graph, 0) == cudaSuccess;
-                if (graph) cudaGraphDestroy(graph);
               }
               launches_per_body = ctx->launches - l0;  // counted during capture, added per replay
+              if (ok) {  // exact kernel count of one replay: the graph's kernel nodes
+                size_t nn = 0;
+                if (cudaGraphGetNodes(graph, nullptr, &nn) == cudaSuccess && nn) {
+                  std::vector<cudaGraphNode_t> nodes(nn);
+                  if (cudaGraphGetNodes(graph, nodes.data(), &nn) == cudaSuccess) {
+                    int64_t kn = 0;
+                    for (auto nd : nodes) {
+                      cudaGraphNodeType ty;
+                      if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) ++kn;
+                    }
+                    launches_per_body = kn;
+                  }
+                }
+              }
+              if (graph) cudaGraphDestroy(graph);
               ctx->launches = l0;
               ctx->prof.iteration_launches = i0;
               if (!ok) {  // capture unsupported here: fall back to direct launches
