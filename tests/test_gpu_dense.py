@@ -66,3 +66,18 @@ def test_batch_subset(ctx):
     for g, r in zip(gs, rs):
         assert rel(g.control, r.control) < 1e-11
         assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-11
+
+
+@pytest.mark.slow
+def test_batch4096_problem_sample_long_run(ctx):
+    # BASELINE config 5 at full problem size (d = 16, K = 2000, L = 128), SURVEY §8(d) parity
+    # plan: 64 fixed problem indices (8 blocks of 8 spread over the 4096 seeds), 200 iterations
+    # at rho = 0.1/dt
+    for first in range(0, 4096, 512):
+        w = problems.batch4096(batch=8, iterations=200, first=first)
+        w.solver.step_size = w.rho_fast
+        gs = I.run_ism_batch(w.problem, w.u0, w.config, w.solver, ctx)
+        rs = O.ism_run(w.problem, w.u0, w.config, w.solver, O.REFERENCE)
+        for g, r in zip(gs, rs):
+            assert rel(g.control, r.control) < 1e-9
+            assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-10

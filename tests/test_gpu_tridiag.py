@@ -62,3 +62,14 @@ def test_rotor21_config(ctx, L):
     r = O.ism_run(w.problem, w.u0, w.config, w.solver, O.STRUCTURED)[0]
     assert rel(g.control, r.control) < 1e-9
     assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-10
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("rho", [0.1, 100.0])  # literal rho and rho = 0.1/dt
+def test_rotor21_config_200_iterations(ctx, rho):
+    # north_star parity bar at BASELINE size: L = 128 (32 x 157 + 96 x 156), 200 iterations
+    w = problems.rotor21(subintervals=128, iterations=200, rho=rho)
+    g = I.run_ism(w.problem, w.u0, w.config, w.solver, ctx)
+    r = O.ism_run(w.problem, w.u0, w.config, w.solver, O.STRUCTURED)[0]
+    assert rel(g.control, r.control) < 1e-9
+    assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-10
