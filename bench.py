@@ -9,10 +9,12 @@ single-state step per grid step, B independent problems.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload NAME]
 
-Default workload = BASELINE.json configs[1]: the rotor j<=20 (d = 21, tridiagonal), K = 20000,
-L = 128 (32 x 157 + 96 x 156 steps), rho = 0.1/dt.  N > 1 runs N independent replicas of it
-(the path is one small latency-bound problem: "replicas only"); batch4096 shards its
-problems over the ranks instead.  Rank 0 prints one JSON line.
+Default workload = BASELINE.json configs[4], the largest configuration and the one that fits one
+GPU: 4096 independent 4-qubit problems (d = 16, dense), K = 2000, L = 128 (80 x 16 + 48 x 15
+steps), rho = 0.1/dt.  N > 1 shards the 4096 problems over N ranks (one process per GPU, no
+data-path collective; controls gathered once at the end); without torchrun in the environment
+``--gpus N`` spawns the N ranks itself.  The single-problem configs (rotor21, spin2, gpe1024)
+run N replicas ("replicas only").  Rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
@@ -140,13 +142,14 @@ class Clocks:
 
 def build_workload(name: str, iterations: int, rank: int, world: int, rho_fast: bool = True):
     from paper_1603_01237_b200 import problems
+    from paper_1603_01237_b200.partition import shard
     if name == "rotor21":
         w = problems.rotor21(subintervals=128, iterations=iterations)
     elif name == "spin2":
         w = problems.spin2(iterations=iterations)
     elif name == "batch4096":
-        per = 4096 // world
-        w = problems.batch4096(batch=per, iterations=iterations, first=rank * per)
+        first, count = shard(4096, world, rank)
+        w = problems.batch4096(batch=count, iterations=iterations, first=first)
     elif name == "ising10":
         w = problems.ising10(iterations=iterations)
     elif name == "gpe1024":
@@ -159,6 +162,20 @@ def build_workload(name: str, iterations: int, rank: int, world: int, rho_fast: 
     if rho_fast:
         w.solver.step_size = w.rho_fast
     return w
+
+
+def workload_config(name: str, world: int) -> dict:
+    """The `config` echo shared by both arms (same keys and values for the same N)."""
+    from paper_1603_01237_b200 import problems
+    w = build_workload(name, 1, 0, world)
+    desc = problems.describe(w)
+    total = 4096 if name == "batch4096" else 1
+    return {"workload": name, "dim": desc["dim"], "channels": desc["channels"], "grid_steps": desc["steps"],
+            "subintervals": desc["subintervals"], "partition": desc["partition"], "problems": total,
+            "problems_per_gpu": w.problem.batch, "step_size": w.solver.step_size, "variant": desc["variant"],
+            "plan": desc["plan"],
+            "parallelism": (f"problem blocks x{world}" if name == "batch4096" else f"replicas x{world}"),
+            "l2": "flushed between timed iterations (256 MiB memset outside the event brackets)"}
 
 
 def problem_bytes(w) -> int:
@@ -177,17 +194,34 @@ def dist_setup():
         import torch.distributed as dist
         if torch.cuda.is_available():
             torch.cuda.set_device(local)
-            dist.init_process_group("nccl")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
     return world, rank, local, dist
 
 
+def spawn_ranks(nproc: int) -> int:
+    """`bench.py --gpus N` outside torchrun: launch the N ranks (one process per GPU) through
+    torch.distributed.run on 127.0.0.1 and pass rank 0's JSON line through."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def _t(dist, v: float):
+    import torch
+    dev = "cuda" if (torch.cuda.is_available() and dist.get_backend() == "nccl") else "cpu"
+    return torch.tensor([v], dtype=torch.float64, device=dev)
+
+
 def allmax(dist, v: float) -> float:
     if dist is None:
         return v
-    import torch
-    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    t = _t(dist, v)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -195,8 +229,7 @@ def allmax(dist, v: float) -> float:
 def allsum(dist, v: float) -> float:
     if dist is None:
         return v
-    import torch
-    t = torch.tensor([v], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    t = _t(dist, v)
     dist.all_reduce(t)
     return float(t.item())
 
@@ -212,17 +245,22 @@ def barrier_sync(dist):
         dist.barrier()
 
 
-def cpu_reference(name: str, warmup: int, steps: int, sample_iters: int | None = None):
+# sample of the CPU path per workload: problems of the batch timed (the rest scale linearly)
+CPU_SAMPLE_PROBLEMS = {"batch4096": 256}
+
+
+def cpu_reference(name: str, warmup: int, steps: int, world: int = 1):
     """The reference's CPU path: the oracle restatement with reference arithmetic (dense
     partial-pivot LU per step, like Eigen::PartialPivLU in propagation.cpp:85-106) on all host
-    threads, as WorkerPool does (runtime.cpp:72-90)."""
+    threads, as WorkerPool does (runtime.cpp:72-90).  Test infrastructure: only this leg and the
+    --impl reference arm execute oracle/ code, after (or instead of) the timed device region."""
     from tests import oracle_api as O
     from paper_1603_01237_b200 import problems
     threads = os.cpu_count() or 1
     if name == "batch4096":
-        sample_b = 16
+        sample_b = CPU_SAMPLE_PROBLEMS[name]
         w = problems.batch4096(batch=sample_b, iterations=warmup + steps)
-        desc = f"{sample_b} of 4096 problems (d=16, K=2000, L=128)"
+        desc = f"{sample_b} of the 4096 problems (d=16, K=2000, L=128); steps/s of the sample"
     else:
         w = build_workload(name, warmup + steps, 0, 1)
         desc = f"full {name} workload"
@@ -231,7 +269,7 @@ def cpu_reference(name: str, warmup: int, steps: int, sample_iters: int | None =
         arith = O.STRUCTURED
         steps = min(steps, 2)
         warmup = 0
-    if name == "rotor21":  # the reference builds the rotor as a dense model (models.cpp:361-399)
+    if name == "rotor21":  # the reference builds the rotor as a dense model (models.cpp:361-380)
         from paper_1603_01237_b200.models import TridiagonalModel
         assert isinstance(w.problem.model, TridiagonalModel)
         w.problem.model = w.problem.model.to_dense()
@@ -248,7 +286,12 @@ def cpu_reference(name: str, warmup: int, steps: int, sample_iters: int | None =
             "sample": f"{desc}; {steps} timed outer iterations after {warmup} warm-up, "
                       f"{'dense-LU reference' if arith == O.REFERENCE else 'structured (Neumann) Cayley'} "
                       f"arithmetic, {threads} threads",
-            "seconds": secs, "wall": wall}
+            "seconds": secs, "wall": wall, "seconds_per_iteration": secs / steps,
+            "sample_problems": p.batch}
+
+
+def full_batch(name: str) -> int:
+    return 4096 if name == "batch4096" else 1
 
 
 def run_reference_arm(args, world, rank, dist):
@@ -257,13 +300,39 @@ def run_reference_arm(args, world, rank, dist):
     ref = cpu_reference(args.workload, args.warmup, args.steps)
     line = {"metric": METRIC, "value": ref["value"], "unit": "steps/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * ref["seconds"] / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload},
+            # one outer iteration of the whole workload at the sample's rate
+            "ms_per_step": 1e3 * ref["seconds_per_iteration"] * full_batch(args.workload) / ref["sample_problems"],
+            "higher_is_better": True,
+            "scaling": "strong" if args.workload == "batch4096" else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d))",
+            "config": workload_config(args.workload, max(args.gpus, world)),
             "cpu_baseline": {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": ref["value"], "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def label_flops(name: str, label: str, w) -> float:
+    """Algorithmic fp64 flops of one launch of the kernel behind a launch label (SURVEY §8(d)
+    per-grid-step model x K x B).  'assembly' = the d-column propagator product sweep
+    (assemble_propagator, propagation.cpp:236-249); 'gradient'/'residual' = a forward sweep +
+    an adjoint/gradient sweep (objective.cpp:38-89); 'task'/'node sweeps' = the whole
+    iteration's task work (flops_per_iteration)."""
+    p = w.problem
+    d, C, K, B = p.model.state_dim(), p.model.channels(), p.grid.steps, p.batch
+    if name in ("spin2", "batch4096"):
+        w_cay = (8 / 3) * d ** 3 + (4 * C + 20) * d ** 2
+        w_bg = w_cay + 4 * d + C * (8 * d ** 2 + 8 * d)
+        per = {"assembly": (56 / 3) * d ** 3 + (4 * C + 4) * d ** 2, "gradient": w_cay + w_bg,
+               "residual": w_cay + w_bg}.get(label)
+    elif name == "rotor21":
+        per = {"assembly": 41 * d * d + 23 * d, "gradient": 64 * d + 64 * d + 24 * d,
+               "residual": 64 * d + 64 * d + 24 * d}.get(label)
+    else:
+        per = None
+    if per is None:
+        return flops_per_iteration(name, w)
+    return per * K * B
 
 
 def main():
@@ -272,10 +341,13 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="rotor21",
-                    choices=["rotor21", "spin2", "batch4096", "ising10", "gpe1024"])
+    ap.add_argument("--workload", default="batch4096",
+                    choices=["batch4096", "rotor21", "spin2", "ising10", "gpe1024"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ttf", action="store_true", help="skip the time-to-fidelity run")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     world, rank, local, dist = dist_setup()
     if args.impl == "reference":
         return run_reference_arm(args, world, rank, dist)
@@ -302,11 +374,13 @@ def main():
         runs = I.run_ism_batch(p, w.u0, w.config, w.solver, ctx)
         barrier_sync(dist)
     prof_main = ctx.profile(reset=True)
-    # ---- a separate short profiled run: per-launch CUDA events for the task-kernel share
+    # ---- a separate short profiled run: per-launch CUDA events on the launching stream
     wp = build_workload(args.workload, W_ + 2, rank, world)
     ctx.set_option(abi.OPT_PROFILE, 1)
     I.run_ism_batch(wp.problem, wp.u0, wp.config, wp.solver, ctx)
-    prof = ctx.profile(reset=True)
+    prof = ctx.profile()
+    kprof = ctx.kernel_profile()
+    ctx.profile(reset=True)
     ctx.set_option(abi.OPT_PROFILE, 0)
     its = runs[0].record.iterations
     timed = its[W_ + 1:W_ + K_ + 1]
@@ -318,14 +392,18 @@ def main():
     value = work / t_max
     launches_per_iter = prof_main["iteration_launches"] / max(prof_main["iterations"], 1)
 
-    # ---- roofline of the dominant kernel (per-subinterval task kernel)
-    # task kernels of one outer iteration (the propagator-cache path launches several)
+    # ---- roofline of the dominant kernel: the launch site with the most device time in the
+    # profiled run (its launches bracketed by CUDA events on the launching stream)
     n_iter = max(prof["iterations"], 1)
-    task_ms = prof["task_ms"] / n_iter
-    task_launches_per_iter = prof["task_launches"] / n_iter
-    fl = flops_per_iteration(args.workload, w)
+    iter_ms = prof["iteration_ms"] / n_iter
+    dom, (dom_ms, dom_n) = max(kprof.items(), key=lambda kv: kv[1][0]) if kprof else ("task", (float("nan"), 1))
+    per_launch_ms = dom_ms / max(dom_n, 1)
+    fl_launch = label_flops(args.workload, dom, wp)
     peak, peak_src = fp64_peak()
-    achieved = fl / (task_ms * 1e-3) / 1e12 if task_ms > 0 else float("nan")
+    achieved = fl_launch / (per_launch_ms * 1e-3) / 1e12
+    fl_iter = flops_per_iteration(args.workload, w)
+    kernels = {k: {"ms_per_iteration": v[0] / n_iter, "launches_per_iteration": v[1] / n_iter,
+                   "share": v[0] / max(sum(x[0] for x in kprof.values()), 1e-12)} for k, v in kprof.items()}
 
     # ---- end to end through the public API: host buffers in, host results out
     ctx.set_option(abi.OPT_FLUSH_L2_BYTES, 0)
@@ -343,64 +421,78 @@ def main():
     d2h = int(np.asarray(e2e_runs[0].control).nbytes * len(e2e_runs)
               + (K_ + 1) * (abi.REC_DTYPE.itemsize + 8 * we.config.subintervals) * len(e2e_runs))
 
-    # ---- time to fidelity 0.999 (rho = 0.1/dt), device time summed over iterations
+    # ---- time to fidelity 0.999 (rho = 0.1/dt): device time and wall clock of a run_ism call
     ttf = None
-    if args.workload in ("rotor21", "spin2", "batch4096") and rank == 0:
-        # iteration cap of the time-to-fidelity run (the rotor converges slowly at rho = 0.1/dt)
-        wt = build_workload(args.workload, 4000 if args.workload == "rotor21" else 300, 0, 1)
-        if args.workload == "batch4096":
-            wt = problems.batch4096(batch=64, iterations=300)
-            wt.solver.step_size = wt.rho_fast
-        rr = I.run_ism_batch(wt.problem, wt.u0, wt.config, wt.solver, ctx)
-        r0 = rr[0]
-        F = 1.0 + r0.record.objectives()
-        hit = np.nonzero(F >= 0.999)[0]
-        if len(hit):
-            k = int(hit[0])
-            ttf = {"target": 0.999, "iterations": k,
-                   "seconds": float(sum(it.device_seconds for it in r0.record.iterations[:k + 1])),
-                   "rho": wt.solver.step_size, "problem": "problem 0 of 64" if args.workload == "batch4096" else args.workload}
-        else:
-            ttf = {"target": 0.999, "iterations": None, "reached": False, "rho": wt.solver.step_size}
+    if not args.no_ttf and args.workload in ("rotor21", "spin2", "batch4096") and rank == 0:
+        ttf = time_to_fidelity(args.workload, ctx, I, problems)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ref = cpu_reference(args.workload, 0, 2)
+        ref = cpu_reference(args.workload, 0, 3)
         cpu = {k: ref[k] for k in ("value", "unit", "cores", "kind", "sample")}
         if ttf and ttf.get("iterations"):
-            ttf["cpu_seconds_est"] = ttf["iterations"] * ref["seconds"] / 2 * (
-                4096 / 16 if args.workload == "batch4096" else 1)
+            scale = 1.0 / ref["sample_problems"] if args.workload == "batch4096" else 1.0
+            ttf["cpu_seconds_est"] = ttf["iterations"] * ref["seconds_per_iteration"] * scale * ttf.get("problems", 1)
 
     if rank != 0:
         return 0
-    desc = problems.describe(w)
-    cfg = {"workload": args.workload, "dim": desc["dim"], "channels": desc["channels"],
-           "grid_steps": desc["steps"], "subintervals": desc["subintervals"], "partition": desc["partition"],
-           "batch_per_gpu": p.batch, "step_size": w.solver.step_size, "variant": desc["variant"],
-           "plan": desc["plan"], "parallelism": f"{'batch shards' if args.workload == 'batch4096' else 'replicas'} x{world}",
-           "l2": "flushed between timed iterations (256 MiB memset outside the event brackets)"}
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": K_, "warmup": W_,
         "ms_per_step": 1e3 * t_max / K_, "higher_is_better": True,
         "scaling": "strong" if args.workload == "batch4096" else "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d))", "config": cfg,
+        "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d))", "config": workload_config(args.workload, world),
         "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": h2d // K_,
-                "d2h_bytes_per_step": d2h // K_, "note": "one run_ism call of K outer iterations from pageable "
-                "host arrays (median of 3 calls), wall clock incl. packing, upload, bootstrap, trailing "
+                "d2h_bytes_per_step": d2h // K_, "note": "one run_ism_batch call of K outer iterations from host "
+                "arrays (median of 3 calls), wall clock incl. packing, upload, bootstrap, trailing "
                 "evaluation and download"},
         "gpu_launches": int(round(launches_per_iter * K_)),
         "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(args.workload),
-                     "kernel": "task kernels of one outer iteration (per-subinterval sweeps)",
-                     "kernel_ms_per_iteration": task_ms, "task_launches_per_iteration": task_launches_per_iter,
-                     "flops_per_iteration": fl, "peak_source": peak_src,
-                     "share_of_step": prof["task_ms"] / max(prof["task_ms"] + prof["other_ms"], 1e-12)},
+                     "kernel": dom, "kernel_ms_per_launch": per_launch_ms, "flops_per_launch": fl_launch,
+                     "share_of_step": dom_ms / max(prof["iteration_ms"], 1e-12), "peak_source": peak_src,
+                     "iteration": {"flops": fl_iter, "ms": iter_ms,
+                                   "tflops": fl_iter / (iter_ms * 1e-3) / 1e12 if iter_ms > 0 else None},
+                     "kernels": kernels},
         "time_to_fidelity": ttf,
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def time_to_fidelity(name, ctx, I, problems):
+    """Iterations, device seconds and wall-clock seconds until F = 1 + objective >= 0.999
+    (rho = 0.1/dt).  Batch: 64 problems, the first one that reaches it counts."""
+    if name == "batch4096":
+        wt = problems.batch4096(batch=64, iterations=400)
+    else:
+        wt = build_workload(name, 4000 if name == "rotor21" else 300, 0, 1)
+    wt.solver.step_size = wt.rho_fast
+    rr = I.run_ism_batch(wt.problem, wt.u0, wt.config, wt.solver, ctx)
+    hits = []
+    for b, r in enumerate(rr):
+        h = np.nonzero(1.0 + r.record.objectives() >= 0.999)[0]
+        if len(h):
+            hits.append((int(h[0]), b))
+    best = [float(np.nanmax(1.0 + r.record.objectives())) for r in rr]
+    out = {"target": 0.999, "rho": wt.solver.step_size, "problems": wt.problem.batch,
+           "reached": len(hits), "best_fidelity_max": max(best)}
+    if not hits:
+        out["iterations"] = None
+        return out
+    k = max(h for h, _ in hits)  # iterations until every reaching problem got there
+    r0 = rr[hits[0][1]]
+    out["iterations"] = k
+    out["device_seconds"] = float(sum(it.device_seconds for it in rr[0].record.iterations[:k + 1]))
+    # wall clock: the same call stopped at k iterations (host arrays in and out)
+    wt.config.max_outer = k
+    t0 = time.perf_counter()
+    I.run_ism_batch(wt.problem, wt.u0, wt.config, wt.solver, ctx)
+    out["wall_seconds"] = time.perf_counter() - t0
+    out["first_problem_iterations"] = int(min(h for h, _ in hits))
+    del r0
+    return out
 
 
 if __name__ == "__main__":

@@ -44,6 +44,10 @@ extern "C" {
 
 #define QOC_ABI_VERSION 1
 
+/* Largest control-channel count C the device kernels carry (DENSE, TRIDIAG, STRANG; the BITFLIP
+ * kind takes C <= 4).  Larger C is rejected with QOC_ELOGIC before any work runs. */
+#define QOC_MAX_CHANNELS 8
+
 enum qoc_status_code {
   QOC_OK = 0,
   QOC_EINVAL = 1,
@@ -229,6 +233,11 @@ typedef struct qoc_profile_v1 {
   int64_t iteration_launches; /* kernel launches inside the outer iterations */
 } qoc_profile_v1;
 int32_t qoc_ctx_profile(qoc_ctx* ctx, qoc_profile_v1* out, int32_t reset);
+/* Per-launch-site device time of the profiled launches since the last reset (QOC_OPT_PROFILE):
+ * entry `index` (0-based, first-seen order) -> its label ("assembly", "gradient", "residual",
+ * "node sweeps", "task", "merge", ...), summed ms and launch count.  QOC_EINVAL past the end. */
+int32_t qoc_ctx_kernel_profile(const qoc_ctx* ctx, int32_t index, char* name, size_t name_len, double* ms,
+                               int64_t* launches);
 
 #ifdef __cplusplus
 }

@@ -42,6 +42,8 @@ def lib():
         L.qoc_ctx_set_option.restype = i32
         L.qoc_ctx_profile.argtypes = [vp, C.POINTER(abi.ProfileV1), i32]
         L.qoc_ctx_profile.restype = i32
+        L.qoc_ctx_kernel_profile.argtypes = [vp, i32, C.c_char_p, C.c_size_t, dp, C.POINTER(C.c_int64)]
+        L.qoc_ctx_kernel_profile.restype = i32
         L.qoc_ism_run.argtypes = [vp, vp, vp, vp, dp, dp, vp, i32, dp, vp]
         L.qoc_ism_run.restype = i32
         L.qoc_propagate_final.argtypes = [vp, vp, dp, dp]
@@ -84,6 +86,16 @@ class Context:
         p = abi.ProfileV1()
         self.lib.qoc_ctx_profile(self.handle, C.byref(p), int(reset))
         return {f: getattr(p, f) for f, _ in abi.ProfileV1._fields_}
+
+    def kernel_profile(self) -> dict:
+        """label -> (ms, launches) of the profiled launches since the last profile reset."""
+        out, i = {}, 0
+        name = C.create_string_buffer(64)
+        ms, n = C.c_double(), C.c_int64()
+        while self.lib.qoc_ctx_kernel_profile(self.handle, i, name, 64, C.byref(ms), C.byref(n)) == abi.QOC_OK:
+            out[name.value.decode()] = (ms.value, n.value)
+            i += 1
+        return out
 
     def close(self):
         if self.handle:

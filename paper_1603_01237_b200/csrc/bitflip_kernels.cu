@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(1 << LOG2T) bitflip_task_kernel(DevProblem P, 
   constexpr int E = 1 << LOG2E, T = 1 << LOG2T;
   using Vec = double2[1 << LOG2E];
   const int n = blockIdx.x, b = blockIdx.y;
-  if (ignore_done ? R.status[b] : R.done[b]) return;
+  if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
   extern __shared__ __align__(16) unsigned char smem[];
   F_ F = make_bf<LOG2E, LOG2T>(P, b, smem);
   const int d = P.d, C = P.C, t = F.t;

@@ -6,6 +6,10 @@
 
 namespace qoc {
 
+// Control channels the device kernels carry per grid step (per-step register arrays).  The
+// driver rejects larger C with QOC_ELOGIC before anything runs (qoc_gpu.h QOC_MAX_CHANNELS).
+constexpr int MAXC = 8;
+
 // ---- complex128 as double2 ------------------------------------------------------------
 __host__ __device__ __forceinline__ double2 cx(double r, double i) { return make_double2(r, i); }
 __host__ __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return cx(a.x + b.x, a.y + b.y); }
@@ -124,6 +128,7 @@ struct DevProblem {
   int potential;
   double pp[4];
   double kappa;
+  int naive;  // GradientOptions::naive_nonlinear_adjoint (split-step adjoints, propagation.cpp:159-166)
   // states and penalty
   const double2* init;  // [B][d]
   const double2* targ;  // [B][d]

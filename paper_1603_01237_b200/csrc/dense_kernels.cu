@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) dense_task_kernel(DevProblem P, DevRun R,
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* ops = reinterpret_cast<double2*>(smem_raw);
   const int b = blockIdx.y;
-  const bool skip = ignore_done ? (R.status[b] != 0) : (R.done[b] != 0);
+  const bool skip = ignore_done ? (R.status[b] != 0) : ((R.done[b] | R.status[b]) != 0);
   if (skip) return;  // uniform over the CTA
   load_ops(ops, P, b, D);
   __syncthreads();
@@ -170,15 +170,13 @@ __global__ void __launch_bounds__(256) dense_task_kernel(DevProblem P, DevRun R,
           const bool live = j < len;
           const int jj = min(j, len - 1);
           const double* uj = u + (size_t)jj * C;
-          double uold[4];
-          for (int c = 0; c < C && c < 4; ++c) uold[c] = uj[c];
           step_inverse<D, G>(L, W, ops, P, b, uj, half, true, S, lane);
           const double2 cn = L.cayley_apply(W, chi, S.vec);
           const double2 ps = cadd(traj[(size_t)jj * D + row], traj[(size_t)(jj + 1) * D + row]);
           const double2 cs = cadd(cn, chi);
           const double aj = P.alpha[node0 + jj] * scale;
           for (int c = 0; c < C; ++c) {
-            const double uc = c < 4 ? uold[c] : uj[c];
+            const double uc = uj[c];  // channel c is written only after its own gradient
             const double im = L.grad_term(ops, C, P.has_quad, c, uc, ps, cs, S.vec);
             const double gc = -aj * dt * uc + 0.25 * dt * (w * im);
             if (live && lead) {

@@ -22,6 +22,8 @@
 #include "../../include/qoc_gpu.h"
 #include "kernels.h"
 
+static_assert(qoc::MAXC == QOC_MAX_CHANNELS, "device channel arrays must match the ABI bound");
+
 using namespace qoc;
 
 struct qoc_ctx {
@@ -35,8 +37,10 @@ struct qoc_ctx {
   int64_t flush_bytes = 0;
   void* flush_buf = nullptr;
   qoc_profile_v1 prof{};
-  // event pairs of the current run: (start, stop, is_task)
-  std::vector<std::tuple<cudaEvent_t, cudaEvent_t, bool>> marks;
+  // event pairs of the current run: (start, stop, is_task, label)
+  std::vector<std::tuple<cudaEvent_t, cudaEvent_t, bool, const char*>> marks;
+  // per-label device time of profiled launches: label -> (ms, launches), first-seen order
+  std::vector<std::pair<std::string, std::pair<double, int64_t>>> by_label;
   int* khost = nullptr;        // pinned iteration indices for graph replays
   cudaGraphExec_t gcache = nullptr;  // last instantiated iteration graph and its parameter key
   std::vector<unsigned char> gkey;
@@ -161,6 +165,9 @@ void validate_problem(const qoc_problem_v1* p) {
   if (p->dim < 1 || p->channels < 1 || p->steps < 1 || p->batch < 1)
     fail(QOC_EINVAL, "dim, channels, steps and batch must be positive");
   if (!(p->dt > 0.0)) fail(QOC_EINVAL, "TimeGrid: dt must be positive");
+  if (p->channels > QOC_MAX_CHANNELS || (p->kind == QOC_KIND_BITFLIP && p->channels > 4))
+    fail(QOC_ELOGIC, "control channel count above what the device kernels carry (QOC_MAX_CHANNELS; 4 for the "
+                     "bit-flip kind)");
   if (!p->initial || !p->target) fail(QOC_EINVAL, "initial and target states are required");
 }
 
@@ -455,7 +462,7 @@ struct Launcher {
     if (in_iteration) ++ctx->prof.iteration_launches;
     if (ctx->profile) {
       ck(cudaEventRecord(b, ctx->stream), "event");
-      ctx->marks.emplace_back(a, b, is_task);
+      ctx->marks.emplace_back(a, b, is_task, what);
     }
     if (e == cudaErrorNotSupported) fail(QOC_ELOGIC, std::string(what) + ": not supported for this model kind");
     ck(e, what);
@@ -468,9 +475,17 @@ struct Launcher {
 };
 
 void harvest_marks(qoc_ctx* ctx) {
-  for (auto& [a, b, is_task] : ctx->marks) {
+  for (auto& [a, b, is_task, what] : ctx->marks) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, a, b) == cudaSuccess) {
+      auto it = std::find_if(ctx->by_label.begin(), ctx->by_label.end(),
+                             [&](const auto& e) { return e.first == what; });
+      if (it == ctx->by_label.end()) {
+        ctx->by_label.push_back({std::string(what), {0.0, 0}});
+        it = ctx->by_label.end() - 1;
+      }
+      it->second.first += ms;
+      it->second.second += 1;
       if (is_task) {
         ctx->prof.task_ms += ms;
         ++ctx->prof.task_launches;
@@ -570,7 +585,21 @@ int32_t qoc_ctx_set_option(qoc_ctx* ctx, int32_t option, int64_t value) {
 int32_t qoc_ctx_profile(qoc_ctx* ctx, qoc_profile_v1* out, int32_t reset) {
   if (!ctx) return QOC_EINVAL;
   if (out) *out = ctx->prof;
-  if (reset) ctx->prof = qoc_profile_v1{};
+  if (reset) {
+    ctx->prof = qoc_profile_v1{};
+    ctx->by_label.clear();
+  }
+  return QOC_OK;
+}
+
+int32_t qoc_ctx_kernel_profile(const qoc_ctx* ctx, int32_t index, char* name, size_t name_len, double* ms,
+                               int64_t* launches) {
+  if (!ctx || index < 0) return QOC_EINVAL;
+  if ((size_t)index >= ctx->by_label.size()) return QOC_EINVAL;
+  const auto& e = ctx->by_label[(size_t)index];
+  if (name && name_len) std::snprintf(name, name_len, "%s", e.first.c_str());
+  if (ms) *ms = e.second.first;
+  if (launches) *launches = e.second.second;
   return QOC_OK;
 }
 
@@ -606,6 +635,8 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
     DeviceProblem dp;
     dp.slots = fresh_slots(ctx->prob_slots);
     upload_problem(p, node, st, dp);
+    // gradient options of the task sweeps, lagged refresh and node sweeps (ism.cpp:373,437,446,543)
+    dp.P.naive = (solver->naive_nonlinear_adjoint && p->kind == QOC_KIND_STRANG) ? 1 : 0;
     const DevProblem& P = dp.P;
     DeviceRun dr;
     dr.slots = fresh_slots(ctx->run_slots);
@@ -642,11 +673,14 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
       ck(cudaEventRecord(ev[1], st), "event");
 
       const int form = split ? QOC_FORM_OVERLAP : QOC_FORM_TRACKING;
-      int mode = M_ENTRY | M_UPDATE;
+      // run_inner (optimizers.cpp:261-285): inner_iterations <= 0 makes no update but the entry
+      // value is still evaluated (ism.cpp:407)
+      const int inner = std::max(0, solver->inner_iterations);
+      int mode = M_ENTRY | (inner > 0 ? M_UPDATE : 0);
       if (cfg->compute_error) mode |= M_ERROR;
       if (assembled_interp) mode |= M_ASSEMBLE;
       if (L > 1 && split && !direct) mode |= M_LAGGED;
-      TaskArgs A{mode, form, split ? 0 : 1, std::max(0, solver->inner_iterations), solver->step_size};
+      TaskArgs A{mode, form, split ? 0 : 1, inner, solver->step_size};
       std::vector<int> h_done(B), h_status(B);
       std::vector<cudaEvent_t> ev_end(max_outer + 2);
       for (auto& e : ev_end) ck(cudaEventCreate(&e), "event");
@@ -657,14 +691,15 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
         if (pcache) {
           // gradient + update through the cache, then the assembly sweep at the new control,
           // then residual / lagged endpoints through the new cache
-          const TaskArgs G{PCM_ENTRY | PCM_GRAD, form, split ? 0 : 1, 1, solver->step_size};
+          const TaskArgs G{PCM_ENTRY | (inner > 0 ? PCM_GRAD : 0), form, split ? 0 : 1, 1, solver->step_size};
           launch.run([&] { return pc_eval(P, RR, G, 0, st); }, "gradient", true);
-          for (int it = 1; it < std::max(1, solver->inner_iterations); ++it) {
+          for (int it = 1; it < inner; ++it) {
             launch.run([&] { return pc_assemble(P, RR, 0, st); }, "assembly", true);
             const TaskArgs G2{PCM_GRAD, form, split ? 0 : 1, 1, solver->step_size};
             launch.run([&] { return pc_eval(P, RR, G2, 0, st); }, "gradient", true);
           }
-          launch.run([&] { return pc_assemble(P, RR, 0, st); }, "assembly", true);
+          // no update (inner = 0): the cache and the propagators already belong to this control
+          if (inner > 0) launch.run([&] { return pc_assemble(P, RR, 0, st); }, "assembly", true);
           if (assembled_interp) {
             // the boundary chain needs only the new propagators: run it on the side stream,
             // concurrently with the residual sweep, penalty and merge (joined before boundary)

@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, Ta
   constexpr int GPW = 32 / NLT;
   __shared__ PcSmem<32> sm_all[4 * GPW];
   const int b = blockIdx.y;
-  if (ignore_done ? R.status[b] : R.done[b]) return;
+  if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
   const int warp = threadIdx.x >> 5, i = threadIdx.x & (NLT - 1), gid = (threadIdx.x & 31) / NLT;
   const int item_raw = (blockIdx.x * 4 + warp) * GPW + gid;
   const bool live = item_raw < P.L * nchunk;
@@ -292,9 +292,10 @@ __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, Ta
       const double2 ps = cadd(psa, psb), cs = cadd(cha, chb);
       const double* uj = u + (size_t)j * C;
       const double aj = P.alpha[node0 + j] * scale;
-      double g[4];
+      double g[MAXC];
       double sq = 0.0;
-      for (int c = 0; c < C && c < 4; ++c) {
+#pragma unroll 1
+      for (int c = 0; c < C; ++c) {
         const double uc = uj[c];
         double2 h;
         if (TRI) {
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(128) pc_eval_kernel(DevProblem P, DevRun R, Ta
         sq += g[c] * g[c];
       }
       if (i == 0 && act && live) {
-        for (int c = 0; c < C && c < 4; ++c) {
+        for (int c = 0; c < C; ++c) {
           if (mode & PC_RAWGRAD) R.grad[((size_t)b * P.K + node0 + j) * C + c] = g[c];
           if (mode & PC_GRAD) u[(size_t)j * C + c] = uj[c] + A.rho * (weight * g[c]);
         }
@@ -331,7 +332,7 @@ __global__ void pc_finalize_kernel(DevProblem P, DevRun R, TaskArgs A, int nchun
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= P.B * P.L) return;
   const int b = t / P.L, n = t % P.L;
-  if (ignore_done ? R.status[b] : R.done[b]) return;
+  if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
   const int len = P.node[n + 1] - P.node[n];
   const double weight = A.weighted ? (double)P.K / (double)len : 1.0;
   double pen = 0.0, err = 0.0;
@@ -352,7 +353,7 @@ __global__ void __launch_bounds__(128) dense_pc_assemble_kernel(DevProblem P, De
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* ops = reinterpret_cast<double2*>(smem_raw);
   const int b = blockIdx.y;
-  if (ignore_done ? R.status[b] : R.done[b]) return;
+  if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
   const int nops = 1 + P.C + (P.has_quad ? P.C : 0);
   const int d = P.d;
   for (int e = threadIdx.x; e < nops * D * D; e += blockDim.x) {
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(128) dense_cayley_kernel(DevProblem P, DevRun 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* ops = reinterpret_cast<double2*>(smem_raw);
   const int b = blockIdx.y;
-  if (ignore_done ? R.status[b] : R.done[b]) return;
+  if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
   const int nops = 1 + P.C + (P.has_quad ? P.C : 0);
   const int d = P.d;
   for (int e = threadIdx.x; e < nops * D * D; e += blockDim.x) {
@@ -505,7 +506,7 @@ __global__ void __launch_bounds__(128) dense_pc_chain_kernel(DevProblem P, DevRu
   constexpr int NL = D, TPW = 32 / D;
   __shared__ __align__(16) double2 matP_all[(128 / 32) * TPW][D * D];
   const int b = blockIdx.y;
-  if (ignore_done ? R.status[b] : R.done[b]) return;
+  if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
   const int warp = threadIdx.x >> 5, l32 = threadIdx.x & 31;
   const int gid = warp * TPW + l32 / NL, row = l32 % NL;
   const int n_raw = blockIdx.x * tasks_per_cta + gid;

@@ -305,7 +305,7 @@ __device__ __forceinline__ void store_vec(double2* dst, const double2* src, int 
 
 __global__ void __launch_bounds__(ST_T) strang_task_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done) {
   const int n = blockIdx.x, b = blockIdx.y;
-  if (ignore_done ? R.status[b] : R.done[b]) return;
+  if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
   extern __shared__ __align__(16) unsigned char smem[];
   const StrangCtx X = make_ctx(P, smem);
   const int d = P.d, t = threadIdx.x;
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(ST_T) strang_task_kernel(DevProblem P, DevRun 
   const double weight = A.weighted ? Kd / (double)len : 1.0;
   const double scale = (double)len / Kd;
   const double dt = P.dt, w = P.ip_w;
-  const bool naive = (A.mode & (1 << 10)) != 0;
+  const bool naive = (A.mode & (1 << 10)) != 0 || P.naive != 0;
   double* u = R.u + ((size_t)b * P.K + node0);  // C == 1
   int mode = A.mode;
   // phase-2 roles in separate CTAs (blockIdx.z): 0 = residual sweep, 1 = lagged refresh with
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(ST_T) strang_horizon_kernel(DevProblem P, DevR
     __syncthreads();
     for (int i = t; i < d; i += ST_T) X.Q[i] = traj[(size_t)j * d + i];
     __syncthreads();
-    strang_backward(X, P, u[j], dt, false, false);
+    strang_backward(X, P, u[j], dt, P.naive != 0, false);  // node_sweeps(.., naive), ism.cpp:373,543
     if (prev >= 0 && P.node[prev] == j) {
       store_vec(R.chi_nodes + nb + (size_t)prev * d, X.A, d);
       --prev;

@@ -157,7 +157,7 @@ __device__ __forceinline__ double grad_im(const TriView& T, int c, double uc, co
 template <int TD>
 __global__ void __launch_bounds__(32) tridiag_task_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done) {
   const int n = blockIdx.x, b = blockIdx.y, lane = threadIdx.x;
-  if (ignore_done ? R.status[b] : R.done[b]) return;
+  if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
   const int d = P.d, C = P.C;
   const int nops = 1 + C + (P.has_quad ? C : 0);
   const TriView T{P.tri_diag + (size_t)b * nops * d, P.tri_sub + (size_t)b * nops * (d - 1), d, C, P.has_quad};
@@ -219,15 +219,15 @@ __global__ void __launch_bounds__(32) tridiag_task_kernel(DevProblem P, DevRun R
           for (int i = 0; i < TD; ++i) x[i] = y[i];
           ok &= cayley_tri<TD>(T, uj, -half, x);  // x = chi_j, y = chi_{j+1}
           const double aj = P.alpha[node0 + j] * scale;
-          double gcs[4];
-          for (int c = 0; c < C && c < 4; ++c) {
+          double gcs[MAXC];
+          for (int c = 0; c < C; ++c) {
             const double uc = uj[c];
             const double im = grad_im<TD>(T, c, uc, x, y, traj + (size_t)j * d, traj + (size_t)(j + 1) * d);
             gcs[c] = -aj * dt * uc + 0.25 * dt * (w * im);
           }
           __syncwarp();
           if (lane == 0) {
-            for (int c = 0; c < C && c < 4; ++c) {
+            for (int c = 0; c < C; ++c) {
               if (mode & M_GRAD) R.grad[((size_t)b * P.K + node0 + j) * C + c] = gcs[c];
               if (mode & M_UPDATE) u[(size_t)j * C + c] = uj[c] + A.rho * (weight * gcs[c]);
             }
@@ -376,7 +376,7 @@ struct TriFactors {
 template <int TD>
 __global__ void __launch_bounds__(32) tri_pc_assemble_kernel(DevProblem P, DevRun R, int ignore_done) {
   const int n = blockIdx.x, b = blockIdx.y, lane = threadIdx.x;
-  if (ignore_done ? R.status[b] : R.done[b]) return;
+  if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TriFactors<TD>& F = *reinterpret_cast<TriFactors<TD>*>(smem_raw);
   const int d = P.d, C = P.C;
@@ -489,7 +489,7 @@ struct TwistFactors {
 template <int TD, int DIM>
 __global__ void __launch_bounds__(64) tri_pc_assemble2_kernel(DevProblem P, DevRun R, int ignore_done) {
   const int n = blockIdx.x, b = blockIdx.y, lane = threadIdx.x & 31, side = threadIdx.x >> 5;
-  if (ignore_done ? R.status[b] : R.done[b]) return;
+  if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TwistFactors<TD>& F = *reinterpret_cast<TwistFactors<TD>*>(smem_raw);
   constexpr int d = DIM, m = DIM / 2;  // compile-time: every row loop unrolls to its own half
