@@ -170,6 +170,10 @@ struct DevRun {
   double* chunk_pen;    // [B][L][nchunk]
   double* chunk_err;    // [B][L][nchunk]
   double* entry_pay;    // [B][L]
+  // Neumann-in-the-control assembly (dense_nm.cu): per-problem coefficient matrices in MMA
+  // fragment order [B][NM_TERMS][8][32], and the per-task hand-off flag to Gauss-Jordan
+  double2* nm;
+  int* nm_fallback;     // [B][L]
   int cap;
 };
 

@@ -1,0 +1,451 @@
+// dense_nm.cu — propagator assembly for batched dense single-control problems (BASELINE
+// config 5: d = 16, C = 1, H(u) = H0 + u Hc), sm_100a.
+//
+// The reference forms every one-step map by an LU solve of B(u_j) = I + i(dt/2)H(u_j)
+// (propagation.cpp:14-16,85-90) and assembles M = prod_j C_j (propagation.cpp:236-249).  For a
+// single linear control the step matrix factors as
+//     B(u) = B0 (I + u G),   B0 = I + i a H0,   G = B0^-1 (i a Hc),   a = dt/2,
+// so its inverse is the Neumann series of (I + uG)^-1 -- the "Taylor expansion of
+// (I + iA)^-1 truncated at fp64 precision" of SURVEY F3 -- and the Cayley matrix is a
+// polynomial in the control with per-problem matrix coefficients:
+//     C(u) = 2 B(u)^-1 - I = sum_{m>=0} u^m N_m,
+//     N_0 = 2 B0^-1 - I,   N_m = 2 (-G)^m B0^-1  (m >= 1).
+// ||B0^-1||_2 <= 1 (B0 is normal with |eigenvalues| >= 1) and ||G||_2 <= a ||Hc||_1, so with
+// x = |u| a ||Hc||_1 the truncation after M terms is bounded by 2 x^(M+1) / (1 - x); every step
+// uses the smallest M that puts this below 2^-54 (the certified fp64 evaluation of the same
+// discrete map; the reference's LU solve differs from it at rounding level, like the
+// Gauss-Jordan path it replaces).
+//
+//   dense_nm_setup_kernel     warp per problem: B0^-1 by pivoted Gauss-Jordan, then the
+//                             coefficient chain N_m, stored in MMA-fragment order.
+//   dense_nm_assemble_kernel  warp per task: per grid step, Horner in u_j over the N_m
+//                             staged in shared memory (TMA bulk copy), elementwise in
+//                             registers; then P_{j+1}^T = P_j^T C_j^T on the fp64 tensor
+//                             cores (mma.sync m8n8k4 f64, four real products) and the cache
+//                             store (column-major P_j: the evaluation kernel below reads each
+//                             matrix as 512-byte runs).  A task whose control leaves the certified range is
+//                             flagged and handed to the Gauss-Jordan kernel (pcache.cu),
+//                             which keeps the partial-pivoting path.
+#include <cstdlib>
+#include <cstring>
+
+#include "dense.cuh"
+#include "kernels.h"
+#include "qoc_gpu.h"
+
+namespace qoc {
+
+namespace {
+
+constexpr int ND = 16;                 // matrix dimension of this path
+constexpr int SLOTS = 8;               // complex fragment slots per lane (256 / 32)
+constexpr int NM_WARPS = 8;            // tasks (warps) per CTA
+constexpr int XS = ND + 1;             // padded row stride of the layout-exchange scratch
+
+// Fragment order: slot s = jn*4 + kk of lane (q = l >> 2, r = l & 3) holds element
+// (8 jn + q, 4 kk + r) of a 16 x 16 matrix -- the B operand of m8n8k4 for its transpose.
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// ---- setup: one warp per problem ------------------------------------------------------
+__global__ void __launch_bounds__(32) dense_nm_setup_kernel(DevProblem P, DevRun R) {
+  using Cfg = DenseCfg<ND, 1>;
+  __shared__ __align__(16) double2 ops[ND * ND];   // H0 (row-major), then i a Hc
+  __shared__ __align__(16) double2 hc[ND * ND];
+  __shared__ __align__(16) double2 T[ND * ND];
+  __shared__ __align__(16) unsigned char scratch[sizeof(double2) * (Cfg::PIV + Cfg::VEC + 2 * Cfg::MAT) + 2 * ND * 4];
+  const int b = blockIdx.x, lane = threadIdx.x, row = lane & 15;
+  const double a = 0.5 * P.dt;
+  for (int e = lane; e < ND * ND; e += 32) {
+    ops[e] = P.h0[(size_t)b * ND * ND + e];
+    const double2 h = P.lin[(size_t)b * ND * ND + e];
+    hc[e] = cx(-a * h.y, a * h.x);  // i a Hc
+  }
+  __syncwarp();
+  DenseScratch<ND, 1> S;
+  S.piv = reinterpret_cast<double2*>(scratch);
+  S.vec = S.piv + Cfg::PIV;
+  S.matW = S.vec + Cfg::VEC;
+  S.matP = S.matW + Cfg::MAT;
+  S.perm = reinterpret_cast<int*>(S.matP + Cfg::MAT);
+  DenseLane<ND, 1> Ln;
+  Ln.row = row;
+  Ln.g = 0;
+  double2 W[ND];
+  const double u0 = 0.0;
+  Ln.build(W, ops, 0, 0, &u0, a, false);  // B0 = I + i a H0
+  // both half-warps run the same 16-lane Gauss-Jordan (partial pivoting: setup, once per run)
+  Ln.invert_pivot(W, S, row);            // W = B0^-1, row `row`
+  double2 G[ND];
+#pragma unroll
+  for (int c = 0; c < ND; ++c) {
+    double2 acc = cx(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < ND; ++k) acc = cfma(W[k], hc[k * ND + c], acc);
+    G[c] = cneg(acc);  // -G
+  }
+  double2* nm = R.nm + (size_t)b * NM_TERMS * SLOTS * 32;
+  auto store_term = [&](int m, const double2 (&Trow)[ND]) {
+    if (lane < 16) {
+#pragma unroll
+      for (int c = 0; c < ND; ++c) {
+        const int s = (row >> 3) * 4 + (c >> 2), l = (row & 7) * 4 + (c & 3);
+        nm[((size_t)m * SLOTS + s) * 32 + l] = Trow[c];
+      }
+    }
+  };
+  double2 Tr[ND];
+#pragma unroll
+  for (int c = 0; c < ND; ++c) Tr[c] = cx(2.0 * W[c].x, 2.0 * W[c].y);  // T_0 = 2 B0^-1
+  {
+    double2 N0[ND];
+#pragma unroll
+    for (int c = 0; c < ND; ++c) N0[c] = cx(Tr[c].x - (c == row ? 1.0 : 0.0), Tr[c].y);
+    store_term(0, N0);
+  }
+  for (int m = 1; m < NM_TERMS; ++m) {  // T_m = (-G) T_{m-1} = N_m
+    __syncwarp();
+    if (lane < 16)
+#pragma unroll
+      for (int c = 0; c < ND; ++c) T[row * ND + c] = Tr[c];
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < ND; ++c) {
+      double2 acc = cx(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < ND; ++k) acc = cfma(G[k], T[k * ND + c], acc);
+      Tr[c] = acc;
+    }
+    store_term(m, Tr);
+  }
+}
+
+// smallest M with 2 x^(M+1) / (1 - x) <= 2^-54, or -1 past the staged terms
+__device__ __forceinline__ int neumann_terms(double x) {
+  if (!(x < 0.5)) return -1;
+  const double lim = 0x1p-54 * (1.0 - x) * 0.5;
+  double p = x;
+  int M = 0;
+  while (p > lim) {
+    p *= x;
+    if (++M >= NM_TERMS) return -1;
+  }
+  return M;
+}
+
+// ---- assembly: one warp per task ----------------------------------------------------------
+template <int TPW>
+__global__ void __launch_bounds__(NM_WARPS * 32, 2) dense_nm_assemble_kernel(DevProblem P, DevRun R, int ignore_done) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* nm_s = reinterpret_cast<double2*>(smem_raw);                       // [NM_TERMS][SLOTS][32]
+  double2* xch_all = nm_s + NM_TERMS * SLOTS * 32;                            // [NM_WARPS][ND][XS]
+  __shared__ __align__(8) unsigned long long bar;
+  const int b = blockIdx.y;
+  if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
+  const int tid = threadIdx.x, warp = tid >> 5, l = tid & 31, q = l >> 2, r = l & 3;
+  // stage the problem's coefficient matrices once per CTA (TMA bulk copy, 4 x 16 KB)
+  constexpr unsigned kBytes = NM_TERMS * SLOTS * 32 * sizeof(double2);
+  constexpr unsigned kChunk = 16384;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_expect_tx(&bar, kBytes);
+    const char* src = reinterpret_cast<const char*>(R.nm + (size_t)b * NM_TERMS * SLOTS * 32);
+    for (unsigned off = 0; off < kBytes; off += kChunk)
+      bulk_g2s(reinterpret_cast<char*>(nm_s) + off, src + off, kChunk < kBytes - off ? kChunk : kBytes - off, &bar);
+  }
+  const int C = P.C;
+  const double gam = 0.5 * P.dt * P.norm1[(size_t)b * (1 + 2 * C) + 1];  // a ||Hc||_1 >= ||G||_2
+  double2* xch = xch_all + warp * ND * XS;
+  const size_t dd = (size_t)ND * ND;
+
+  int n[TPW], node0[TPW], len[TPW];
+  bool live[TPW];
+  int lenmax = 0;
+#pragma unroll
+  for (int t = 0; t < TPW; ++t) {
+    const int nr = (blockIdx.x * NM_WARPS + warp) * TPW + t;
+    live[t] = nr < P.L;
+    n[t] = live[t] ? nr : P.L - 1;
+    node0[t] = P.node[n[t]];
+    len[t] = P.node[n[t] + 1] - node0[t];
+    lenmax = max(lenmax, len[t]);
+  }
+  // certified range check over the task's steps (warp-uniform); out-of-range tasks are handed
+  // to the Gauss-Jordan kernel
+#pragma unroll
+  for (int t = 0; t < TPW; ++t) {
+    double um = 0.0;
+    for (int j = l; j < len[t]; j += 32) um = fmax(um, fabs(R.u[(size_t)b * P.K + node0[t] + j]));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) um = fmax(um, __shfl_xor_sync(0xffffffffu, um, off));
+    const bool ok = neumann_terms(um * gam) >= 0;  // NaN controls also fail here
+    if (l == 0 && live[t]) R.nm_fallback[(size_t)b * P.L + n[t]] = ok ? 0 : 1;
+    if (!ok) live[t] = false;
+  }
+  // P^T in A-fragment layout: Pa[i][kk] = P[4kk + r][8i + q]
+  double2 Pa[TPW][2][4];
+#pragma unroll
+  for (int t = 0; t < TPW; ++t)
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) Pa[t][i][kk] = cx((4 * kk + r) == (8 * i + q) ? 1.0 : 0.0, 0.0);
+  // P_0 = I into the cache
+#pragma unroll
+  for (int t = 0; t < TPW; ++t) {
+    if (!live[t]) continue;
+    double2* Pc = R.pc + ((size_t)b * P.L + n[t]) * (size_t)R.traj_len * dd;
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) Pc[(8 * i + q) * ND + 4 * kk + r] = Pa[t][i][kk];  // column-major
+  }
+  mbar_wait(&bar, 0);
+
+  for (int j = 0; j < lenmax; ++j) {
+    double uj[TPW];
+    int M = 0;
+#pragma unroll
+    for (int t = 0; t < TPW; ++t) {
+      uj[t] = R.u[(size_t)b * P.K + node0[t] + min(j, len[t] - 1)];
+      const int mt = live[t] ? neumann_terms(fabs(uj[t]) * gam) : 0;
+      M = max(M, mt);
+    }
+    // Horner: Y = N_M; Y = N_m + u Y (m = M-1 .. 0); Y[s] = C(u)[8 jn + q][4 kk + r]
+    double2 Y[TPW][SLOTS];
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      const double2 nv = nm_s[(M * SLOTS + s) * 32 + l];
+#pragma unroll
+      for (int t = 0; t < TPW; ++t) Y[t][s] = nv;
+    }
+    for (int m = M - 1; m >= 0; --m) {
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s) {
+        const double2 nv = nm_s[(m * SLOTS + s) * 32 + l];
+#pragma unroll
+        for (int t = 0; t < TPW; ++t) Y[t][s] = cx(fma(uj[t], Y[t][s].x, nv.x), fma(uj[t], Y[t][s].y, nv.y));
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < TPW; ++t) {
+      // P_{j+1}^T = P_j^T C_j^T: A = P^T (Pa), B = C^T (Y: B[4kk + r][8jn + q] = C[8jn + q][4kk + r])
+      double cr[2][2][2], ci[2][2][2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int jn = 0; jn < 2; ++jn) {
+          cr[i][jn][0] = cr[i][jn][1] = ci[i][jn][0] = ci[i][jn][1] = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const double2 av = Pa[t][i][kk], bv = Y[t][jn * 4 + kk];
+            dmma(cr[i][jn][0], cr[i][jn][1], av.x, bv.x);
+            dmma(cr[i][jn][0], cr[i][jn][1], -av.y, bv.y);
+            dmma(ci[i][jn][0], ci[i][jn][1], av.x, bv.y);
+            dmma(ci[i][jn][0], ci[i][jn][1], av.y, bv.x);
+          }
+        }
+      // lane holds P_{j+1}[8 jn + 2r + e][8 i + q]; C-fragment -> A-fragment layout through the
+      // warp's scratch, then the cache store (column-major: 64-byte runs of a column per lane quad)
+      const bool act = live[t] && j < len[t];
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int jn = 0; jn < 2; ++jn)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) xch[(8 * jn + 2 * r + e) * XS + 8 * i + q] = cx(cr[i][jn][e], ci[i][jn][e]);
+      __syncwarp();
+      if (act) {
+        double2* dst = R.pc + (((size_t)b * P.L + n[t]) * (size_t)R.traj_len + j + 1) * dd;
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            Pa[t][i][kk] = xch[(4 * kk + r) * XS + 8 * i + q];
+            __stcs(dst + (8 * i + q) * ND + 4 * kk + r, Pa[t][i][kk]);
+          }
+      }
+    }
+  }
+  // M_n = P_len for the boundary chain (row-major)
+  if (R.prop) {
+#pragma unroll
+    for (int t = 0; t < TPW; ++t) {
+      if (!live[t]) continue;
+      double2* M = R.prop + ((size_t)b * P.L + n[t]) * dd;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) M[(4 * kk + r) * ND + 8 * i + q] = Pa[t][i][kk];
+    }
+  }
+}
+
+// ---- gradient / residual evaluation through the cache: one warp per task ----------------
+// Streams P_1..P_len (4 KB each, coalesced 512-byte rows of lanes) once with two steps in
+// flight and evaluates, exactly as pc_eval_kernel (pcache.cu) does,
+//   psi_j = P_j phi,  chi_j = P_j chi_0,  chi_0 = P_len^dag seed       (objective.cpp:31-34)
+//   g_j = -alpha_j dt u_j + dt/4 w Im<chi_j + chi_{j+1}, Hc (psi_j + psi_{j+1})>  (objective.cpp:55-57)
+// Lane (row = l & 15, g = l >> 4) holds columns 2t + g of its row of every matrix.
+__global__ void __launch_bounds__(256, 2) dense_pc_eval16_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done) {
+  constexpr int PE_ENTRY = 1, PE_GRAD = 2, PE_ERR = 4;
+  __shared__ double2 hcs[ND * ND];  // Hc column-major: lane (row, g) reads 512-byte runs
+  __shared__ double2 xs[8][ND];
+  const int b = blockIdx.y;
+  if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
+  const size_t dd = (size_t)ND * ND;
+  for (int e = threadIdx.x; e < ND * ND; e += blockDim.x) hcs[(e & 15) * ND + (e >> 4)] = P.lin[(size_t)b * dd + e];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, l = threadIdx.x & 31, row = l & 15, g = l >> 4;
+  const int n = blockIdx.x * 8 + warp;
+  if (n >= P.L) return;
+  const int mode = A.mode;
+  const int node0 = P.node[n], len = P.node[n + 1] - node0;
+  const double Kd = (double)P.K, weight = A.weighted ? Kd / (double)len : 1.0, scale = (double)len / Kd;
+  const double dt = P.dt, w = P.ip_w;
+  const size_t tix = ((size_t)b * P.L + n) * ND;
+  // column-major cache: P_j[row][2t + g] at (2t + g) * 16 + row = l + 32 t
+  const double2* Pc = R.pc + ((size_t)b * P.L + n) * (size_t)R.traj_len * dd + l;
+  double* u = R.u + (size_t)b * P.K + node0;
+  double2 phi[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) phi[t] = R.task_init[tix + 2 * t + g];
+  auto half_sum = [&](double2 v) { return cadd(v, shfl_xor(v, 16)); };
+  auto row_sum = [&](double v) {
+#pragma unroll
+    for (int off = 1; off < 16; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    return v;
+  };
+  double2 m[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) m[t] = __ldcs(Pc + (size_t)len * dd + 32 * t);  // P_len
+  double2 acc = cx(0.0, 0.0);
+#pragma unroll
+  for (int t = 0; t < 8; ++t) acc = cfma(m[t], phi[t], acc);
+  const double2 psiL = half_sum(acc);  // row `row` of P_len phi
+  const double2 targ = R.task_targ[tix + row];
+  if (mode & PE_ENTRY) {
+    const double tv = A.form == 0 ? cconjmul(targ, psiL).x : cabs2(csub(psiL, targ));
+    const double s = row_sum(g == 0 ? tv : 0.0);
+    if (l == 0) R.entry_pay[(size_t)b * P.L + n] = A.form == 0 ? (w * s) : (-0.5 * (w * s));
+  }
+  double pen = 0.0;
+  for (int j = l; j < len; j += 32) pen += (P.alpha[node0 + j] * scale) * (u[j] * u[j]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) pen += __shfl_xor_sync(0xffffffffu, pen, off);
+  double err = 0.0;
+  if (mode & (PE_GRAD | PE_ERR)) {
+    // chi_0[c] = sum_r conj(P_len[r][c]) seed[r]: lane keeps columns 2t + g
+    const double2 seed = A.form == 0 ? targ : csub(targ, psiL);
+    double2 chi0[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      double2 v = cconjmul(m[t], seed);
+#pragma unroll
+      for (int off = 1; off < 16; off <<= 1) v = cadd(v, shfl_xor(v, off));
+      chi0[t] = v;
+    }
+    // row-distributed psi_0 = phi and chi_0 (column slots -> rows through shared memory)
+    if (row == 0)
+#pragma unroll
+      for (int t = 0; t < 8; ++t) xs[warp][2 * t + g] = chi0[t];
+    __syncwarp();
+    double2 psi_prev = R.task_init[tix + row], chi_prev = xs[warp][row];
+    for (int j = 0; j < len; ++j) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) m[t] = __ldcs(Pc + (size_t)(j + 1) * dd + 32 * t);
+      double2 a = cx(0.0, 0.0), c = cx(0.0, 0.0);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        a = cfma(m[t], phi[t], a);
+        c = cfma(m[t], chi0[t], c);
+      }
+      const double2 psi_n = half_sum(a), chi_n = half_sum(c);
+      const double2 ps = cadd(psi_prev, psi_n), cs = cadd(chi_prev, chi_n);
+      // (Hc ps)[row]: ps of column 2t + g comes from lane 2t + g (its own row)
+      double2 h = cx(0.0, 0.0);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) h = cfma(hcs[(2 * t + g) * ND + row], shfl(ps, 2 * t + g), h);
+      h = half_sum(h);
+      const double im = row_sum(g == 0 ? cconjmul(cs, h).y : 0.0);
+      const double uj = u[j];
+      const double gj = -(P.alpha[node0 + j] * scale) * dt * uj + 0.25 * dt * (w * im);
+      if (l == 0 && (mode & PE_GRAD)) u[j] = uj + A.rho * (weight * gj);
+      err += fabs(gj);  // C = 1: ||g_j||_2 = |g_j| (error_norm, objective.cpp:152-160)
+      psi_prev = psi_n;
+      chi_prev = chi_n;
+    }
+  }
+  if (l == 0) {
+    R.chunk_pen[(size_t)b * P.L + n] = pen;
+    R.chunk_err[(size_t)b * P.L + n] = err;
+  }
+}
+
+}  // namespace
+
+// QOC_DISABLE="nm,eval16" switches either path off (A/B and bisection on the GPU box)
+static bool disabled(const char* what) {
+  const char* e = std::getenv("QOC_DISABLE");
+  return e && std::strstr(e, what) != nullptr;
+}
+
+bool dense_nm_applicable(const DevProblem& P) {
+  return P.kind == QOC_KIND_DENSE && P.d == ND && P.C == 1 && !P.has_quad && !disabled("nm");
+}
+
+cudaError_t dense_nm_setup(const DevProblem& P, const DevRun& R, cudaStream_t st) {
+  dense_nm_setup_kernel<<<P.B, 32, 0, st>>>(P, R);
+  return cudaGetLastError();
+}
+
+size_t dense_nm_smem() {
+  return sizeof(double2) * ((size_t)NM_TERMS * SLOTS * 32 + (size_t)NM_WARPS * ND * XS);
+}
+
+// tasks per warp (1 or 2: two tasks of a problem share every coefficient load); QOC_NM_TPW
+// overrides the default for A/B measurements
+static int nm_tpw() {
+  static int v = [] {
+    const char* e = std::getenv("QOC_NM_TPW");
+    return (e && std::atoi(e) == 2) ? 2 : 1;
+  }();
+  return v;
+}
+
+template <int TPW>
+static cudaError_t launch_nm(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st) {
+  auto kern = dense_nm_assemble_kernel<TPW>;
+  const size_t smem = dense_nm_smem();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int tpc = NM_WARPS * TPW;
+  kern<<<dim3((P.L + tpc - 1) / tpc, P.B), NM_WARPS * 32, smem, st>>>(P, R, ignore_done);
+  return cudaGetLastError();
+}
+
+// pc_eval for the same problems when the evaluation needs only ENTRY / GRAD / ERR and the task
+// is a single chunk (pc_finalize_kernel then reduces exactly as for pc_eval_kernel)
+bool dense_pc_eval16_applicable(const DevProblem& P, const DevRun& R, int mode, int nchunk) {
+  return R.nm && !disabled("eval16") && nchunk == 1 && (mode & ~7) == 0 && R.traj_len - 1 <= 32;
+}
+
+cudaError_t dense_pc_eval16(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
+  dense_pc_eval16_kernel<<<dim3((P.L + 7) / 8, P.B), 256, 0, st>>>(P, R, A, ignore_done);
+  return cudaGetLastError();
+}
+
+cudaError_t dense_nm_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st) {
+  return nm_tpw() == 2 ? launch_nm<2>(P, R, ignore_done, st) : launch_nm<1>(P, R, ignore_done, st);
+}
+
+}  // namespace qoc

@@ -11,6 +11,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <exception>
+#include <mutex>
+#include <thread>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -171,16 +176,42 @@ void validate_problem(const qoc_problem_v1* p) {
   if (!p->initial || !p->target) fail(QOC_EINVAL, "initial and target states are required");
 }
 
+// Host-side per-problem packing of large batches on the host threads (the batch's operator
+// conversion is the bulk of the e2e upload); the first exception is rethrown on the caller.
+template <class F>
+void parallel_for(int n, F&& f) {
+  const int hw = static_cast<int>(std::thread::hardware_concurrency());
+  const int nt = std::max(1, std::min({hw, 16, n / 64}));
+  if (nt <= 1) {
+    for (int i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::exception_ptr err;
+  std::mutex mu;
+  std::vector<std::thread> pool;
+  for (int t = 0; t < nt; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        for (int i = t; i < n; i += nt) f(i);
+      } catch (...) {
+        std::lock_guard<std::mutex> g(mu);
+        if (!err) err = std::current_exception();
+      }
+    });
+  for (auto& th : pool) th.join();
+  if (err) std::rethrow_exception(err);
+}
+
 void hermitian_check(const double* m, int d, const char* what) {  // models.cpp:20-25
-  double scale = 1.0, defect = 0.0;
+  double scale2 = 1.0, defect2 = 0.0;  // squared moduli: no hypot in the per-element loop
   for (int j = 0; j < d; ++j)
-    for (int i = 0; i < d; ++i) {
+    for (int i = 0; i <= j; ++i) {
       const double ar = m[2 * (i + (size_t)j * d)], ai = m[2 * (i + (size_t)j * d) + 1];
       const double br = m[2 * (j + (size_t)i * d)], bi = m[2 * (j + (size_t)i * d) + 1];
-      scale = std::max(scale, std::hypot(ar, ai));
-      defect = std::max(defect, std::hypot(ar - br, ai + bi));
+      scale2 = std::max(scale2, std::max(ar * ar + ai * ai, br * br + bi * bi));
+      defect2 = std::max(defect2, (ar - br) * (ar - br) + (ai + bi) * (ai + bi));
     }
-  if (defect > 1e-10 * scale) fail(QOC_EINVAL, std::string(what) + " must be Hermitian");
+  if (!(defect2 <= 1e-20 * scale2)) fail(QOC_EINVAL, std::string(what) + " must be Hermitian");
 }
 
 void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaStream_t st, DeviceProblem& out) {
@@ -216,13 +247,13 @@ void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaS
             const double re = src[2 * (i + (size_t)j * d)], im = src[2 * (i + (size_t)j * d) + 1];
             dst[2 * ((size_t)i * d + j)] = re;  // column-major -> row-major
             dst[2 * ((size_t)i * d + j) + 1] = im;
-            colsum += std::hypot(re, im);
+            colsum += std::sqrt(re * re + im * im);
           }
           best = std::max(best, colsum);
         }
         *norm = best * (1.0 + 1e-12);
       };
-      for (int b = 0; b < B; ++b) {
+      parallel_for(B, [&](int b) {
         double* nb = norms.data() + (size_t)b * (1 + 2 * C);
         convert(p->h0 + 2 * dd * b, h0.data() + 2 * dd * b, nb, "free Hamiltonian");
         for (int c = 0; c < C; ++c)
@@ -231,7 +262,7 @@ void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaS
         for (int c = 0; c < nq; ++c)
           convert(p->quadratic + 2 * dd * ((size_t)b * C + c), quad.data() + 2 * dd * ((size_t)b * C + c),
                   nb + 1 + C + c, "quadratic operator");
-      }
+      });
       P.h0 = out.put<double2>(h0.data(), h0.size());
       P.lin = out.put<double2>(lin.data(), lin.size());
       P.quad = nq ? out.put<double2>(quad.data(), quad.size()) : nullptr;
@@ -346,7 +377,7 @@ bool use_pcache(const DevProblem& P, const std::vector<int>& node) {
 }
 
 void alloc_run(const DeviceProblem& dp, int cap, const std::vector<int>& node, bool need_prop, bool need_grad,
-               cudaStream_t st, DeviceRun& out, bool with_pc = false) {
+               cudaStream_t st, DeviceRun& out, bool with_pc = false, bool split = false) {
   const DevProblem& P = dp.P;
   DevRun& R = out.R;
   const size_t B = P.B, L = P.L, d = P.d, K = P.K, C = P.C;
@@ -387,11 +418,19 @@ void alloc_run(const DeviceProblem& dp, int cap, const std::vector<int>& node, b
     // Few dense tasks (one lane group each would leave the GPU idle through a long dependent
     // sweep): form every step's Cayley matrix in parallel first, then run the per-task matmul
     // chain.  Many tasks (the batch) keep the fused sweep, which measured faster there.
-    if (P.kind == QOC_KIND_DENSE && P.d <= 16 && B * L <= 1024) {
+    const bool nm = dense_nm_applicable(P) && !split && R.traj_len - 1 <= 32;  // one chunk per task
+    if (P.kind == QOC_KIND_DENSE && P.d <= 16 && B * L <= 1024 && !nm) {
       const size_t cb = sizeof(double2) * B * K * d * d;
       size_t freeb = 0, total = 0;
       if (cudaMemGetInfo(&freeb, &total) == cudaSuccess && cb < freeb / 10 * 6)
         R.cay = out.alloc<double2>(cb / sizeof(double2));
+    }
+    // the Neumann path keeps a column-major cache that only the interpolated-variant
+    // evaluations read (dense_nm.cu); split runs keep the Gauss-Jordan sweep
+    if (nm) {
+      R.nm = out.alloc<double2>(B * NM_TERMS * 256);
+      R.nm_fallback = out.alloc<int>(B * L);
+      ck(cudaMemsetAsync(R.nm_fallback, 0, sizeof(int) * B * L, st), "memset");
     }
     const int nchunk = pc_nchunk(P, R);
     R.chunk_pen = out.alloc<double>(B * L * nchunk);
@@ -499,6 +538,19 @@ void harvest_marks(qoc_ctx* ctx) {
   }
   ctx->marks.clear();
 }
+
+// QOC_TRACE_HOST=1: wall-clock phases of qoc_ism_run on stderr (host-side e2e breakdown)
+struct HostTrace {
+  bool on = std::getenv("QOC_TRACE_HOST") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  void mark(const char* what, cudaStream_t st = nullptr) {
+    if (!on) return;
+    if (st) cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[qoc host] %-22s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+  }
+};
 
 template <class F>
 int32_t guarded(qoc_ctx* ctx, F&& f) {
@@ -611,6 +663,7 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
                     const qoc_solver_v1* solver, const double* u0, double* u_out, qoc_iter_record_v1* recs,
                     int32_t rec_cap, double* task_values, qoc_run_status_v1* status) {
   return guarded(ctx, [&] {
+    HostTrace trace;
     validate_problem(p);
     if (!cfg || !solver || !u0 || !u_out || !recs || !status) fail(QOC_EINVAL, "null argument");
     // ism.cpp:213-231
@@ -635,15 +688,17 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
     DeviceProblem dp;
     dp.slots = fresh_slots(ctx->prob_slots);
     upload_problem(p, node, st, dp);
+    trace.mark("upload problem", st);
     // gradient options of the task sweeps, lagged refresh and node sweeps (ism.cpp:373,437,446,543)
     dp.P.naive = (solver->naive_nonlinear_adjoint && p->kind == QOC_KIND_STRANG) ? 1 : 0;
     const DevProblem& P = dp.P;
     DeviceRun dr;
     dr.slots = fresh_slots(ctx->run_slots);
     const bool pcache = use_pcache(P, node);
-    alloc_run(dp, rec_cap, node, assembled_interp, false, st, dr, pcache);
+    alloc_run(dp, rec_cap, node, assembled_interp, false, st, dr, pcache, split);
     const DevRun& R = dr.R;
     ck(cudaMemcpyAsync(R.u, u0, sizeof(double) * B * K * C, cudaMemcpyHostToDevice, st), "u0");
+    trace.mark("alloc + u0", st);
 
     const int max_outer = cfg->max_outer;
     std::vector<cudaEvent_t> ev(max_outer + 2);
@@ -654,6 +709,7 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
     try {
       ck(cudaEventRecord(ev[0], st), "event");
       // ---- bootstrap (ism.cpp:344-393)
+      if (R.nm) launch(dense_nm_setup(P, R, st), "neumann coefficients");
       if (pcache) launch(pc_assemble(P, R, 0, st), "propagator cache");
       if (L > 1) {
         if (assembled_interp) {
@@ -671,6 +727,7 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
         launch(set_single_tasks(P, R, st), "tasks");
       }
       ck(cudaEventRecord(ev[1], st), "event");
+      trace.mark("bootstrap", st);
 
       const int form = split ? QOC_FORM_OVERLAP : QOC_FORM_TRACKING;
       // run_inner (optimizers.cpp:261-285): inner_iterations <= 0 makes no update but the entry
@@ -852,6 +909,7 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
       }
       destroy_graph();
       launch.in_iteration = false;
+      trace.mark("outer iterations", st);
       // ---- trailing evaluation (ism.cpp:594-609)
       {
         if (pcache) {
@@ -865,6 +923,7 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
       }
       ck(cudaStreamSynchronize(st), "run");
       check_flags(R);
+      trace.mark("trailing evaluation");
 
       // ---- download
       std::vector<int> n_recs(B), stat(B), abort_iter(B), flags((size_t)B * rec_cap);
@@ -888,6 +947,7 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
         ctx->prof.iteration_ms += secs[k];
       }
       ctx->prof.iterations += ran;
+      trace.mark("download");
       harvest_marks(ctx);
       for (auto& e : ev_end) cudaEventDestroy(e);
       for (int b = 0; b < B; ++b) {

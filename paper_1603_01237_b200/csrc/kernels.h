@@ -28,6 +28,12 @@ cudaError_t pc_eval(const DevProblem& P, const DevRun& R, const TaskArgs& A, int
 cudaError_t pc_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st);
 constexpr int PCM_ENTRY = 1, PCM_GRAD = 2, PCM_ERR = 4, PCM_LAG = 8, PCM_FINAL = 16, PCM_RAWGRAD = 32;
 
+// Neumann-in-the-control assembly for dense d = 16, C = 1, linear control (dense_nm.cu)
+constexpr int NM_TERMS = 16;
+bool dense_nm_applicable(const DevProblem& P);
+cudaError_t dense_nm_setup(const DevProblem& P, const DevRun& R, cudaStream_t st);
+cudaError_t dense_nm_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st);
+
 // glue (kind independent)
 cudaError_t penalty_partials(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st);
 cudaError_t merge_iteration(const DevProblem& P, const DevRun& R, int k, double* tot_err, cudaStream_t st);

@@ -354,6 +354,13 @@ __global__ void __launch_bounds__(128) dense_pc_assemble_kernel(DevProblem P, De
   double2* ops = reinterpret_cast<double2*>(smem_raw);
   const int b = blockIdx.y;
   if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
+  // after the Neumann kernel (dense_nm.cu) only the tasks it handed off run here
+  auto handed_off = [&](int n) { return !R.nm_fallback || R.nm_fallback[(size_t)b * P.L + n] != 0; };
+  if (R.nm_fallback) {
+    const int t0 = blockIdx.x * tasks_per_cta;
+    const int mine = (int)threadIdx.x < tasks_per_cta && t0 + (int)threadIdx.x < P.L && handed_off(t0 + threadIdx.x);
+    if (!__syncthreads_or(mine)) return;
+  }
   const int nops = 1 + P.C + (P.has_quad ? P.C : 0);
   const int d = P.d;
   for (int e = threadIdx.x; e < nops * D * D; e += blockDim.x) {
@@ -371,7 +378,7 @@ __global__ void __launch_bounds__(128) dense_pc_assemble_kernel(DevProblem P, De
   const int warp = threadIdx.x >> 5, l32 = threadIdx.x & 31;
   const int gid = warp * TPW + l32 / NL, lane = l32 % NL;
   const int n_raw = blockIdx.x * tasks_per_cta + gid;
-  const bool live_task = n_raw < P.L;
+  const bool live_task = n_raw < P.L && handed_off(n_raw);
   if (!__any_sync(0xffffffffu, live_task)) return;
   const int n = live_task ? n_raw : P.L - 1;
   const size_t gbytes = sizeof(double2) * (Cfg::PIV + Cfg::VEC + 2 * Cfg::MAT) + sizeof(int) * 2 * D;
@@ -397,10 +404,13 @@ __global__ void __launch_bounds__(128) dense_pc_assemble_kernel(DevProblem P, De
   double2 W[COLS], Pm[COLS];
 #pragma unroll
   for (int t = 0; t < COLS; ++t) Pm[t] = cx(row == t ? 1.0 : 0.0, 0.0);
+  // the Neumann path's cache is column-major (dense_nm.cu): its hand-offs store transposed
+  const bool colmajor = R.nm_fallback != nullptr;
+  auto at = [&](int i, int c) { return colmajor ? (size_t)c * d + i : (size_t)i * d + c; };
   if (live_task && row < d)
 #pragma unroll
     for (int t = 0; t < COLS; ++t)
-      if (t < d) Pc[(size_t)row * d + t] = Pm[t];
+      if (t < d) Pc[at(row, t)] = Pm[t];
   const double* nrm = P.norm1 + (size_t)b * (1 + 2 * C);
   for (int j = 0; j < lenmax; ++j) {
     const bool live = j < len;
@@ -418,10 +428,10 @@ __global__ void __launch_bounds__(128) dense_pc_assemble_kernel(DevProblem P, De
     Ln.cayley_matmul(W, Pm, S, live);  // P_{j+1} = 2 B_j^-1 P_j - P_j (kept when past len)
     if (live) {
       if (live_task && row < d) {
-        double2* dst = Pc + (size_t)(j + 1) * dd + (size_t)row * d;
+        double2* dst = Pc + (size_t)(j + 1) * dd;
 #pragma unroll
         for (int t = 0; t < COLS; ++t)
-          if (t < d) dst[t] = Pm[t];
+          if (t < d) dst[at(row, t)] = Pm[t];
       }
     }
   }
@@ -603,9 +613,19 @@ int pc_chunk(const DevProblem& P, const DevRun& R) {
   return chunk < 4 ? 4 : (chunk > 16 ? 16 : chunk);
 }
 
+bool dense_pc_eval16_applicable(const DevProblem& P, const DevRun& R, int mode, int nchunk);
+cudaError_t dense_pc_eval16(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
+
 cudaError_t pc_eval(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
   const int chunk = pc_chunk(P, R);
   const int nchunk = (R.traj_len - 1 + chunk - 1) / chunk;
+  if (dense_pc_eval16_applicable(P, R, A.mode, nchunk)) {  // dense d = 16, one control (dense_nm.cu)
+    cudaError_t e = dense_pc_eval16(P, R, A, ignore_done, st);
+    if (e != cudaSuccess) return e;
+    pc_finalize_kernel<<<(P.B * P.L + 127) / 128, 128, 0, st>>>(P, R, A, nchunk, ignore_done);
+    return cudaGetLastError();
+  }
+  if (R.nm) return cudaErrorNotSupported;  // the Neumann path's column-major cache has no other reader
   dim3 grid((P.L * nchunk + 3) / 4, P.B);
   const bool small = P.d <= 16;  // narrower register arrays -> higher occupancy
   if (P.kind == QOC_KIND_TRIDIAG) {
@@ -647,6 +667,11 @@ static cudaError_t launch_dense_pc(const DevProblem& P, const DevRun& R, int ign
 
 cudaError_t pc_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st) {
   if (P.kind == QOC_KIND_TRIDIAG) return tri_pc_assemble(P, R, ignore_done, st);
+  if (R.nm) {  // Neumann + tensor-core sweep; out-of-range tasks continue in Gauss-Jordan below
+    cudaError_t e = dense_nm_assemble(P, R, ignore_done, st);
+    if (e != cudaSuccess) return e;
+    return launch_dense_pc<16>(P, R, ignore_done, st);
+  }
   if (R.cay) {
     switch (dense_pad(P.d)) {
       case 2: return launch_dense_split<2>(P, R, ignore_done, st);

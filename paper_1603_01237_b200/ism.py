@@ -244,27 +244,43 @@ def pack_solver(sv: SolverSpec):
 
 def unpack_records(recs: np.ndarray, tvals: np.ndarray, status, cfg: IsmConfig,
                    solver: SolverSpec, b: int) -> RunRecord:
-    st = status[b]
-    n = st.iterations_recorded
-    rec = RunRecord(subintervals=cfg.subintervals, workers=cfg.workers, solver=solver.kind,
-                    variant=cfg.variant, plan=cfg.plan, aborted=bool(st.aborted),
-                    abort_reason=st.abort_reason.decode())
-    for k in range(n):
-        r = recs[b, k]
-        rec.iterations.append(IterationStat(
-            iteration=int(r["iteration"]), objective=float(r["objective"]),
-            exact_objective=float(r["exact_objective"]) if r["has_exact_objective"] else None,
-            error=float(r["error"]) if r["has_error"] else None,
-            task_values=[float(v) for v in tvals[b, k]],
-            device_seconds=float(r["device_seconds"])))
-    return rec
+    return unpack_all(recs[b:b + 1], tvals[b:b + 1], [status[b]], cfg, solver)[0]
+
+
+def unpack_all(recs: np.ndarray, tvals: np.ndarray, status, cfg: IsmConfig, solver: SolverSpec,
+               task_value_lists: bool = True) -> list:
+    """RunRecords of every batch member (fields converted once for the whole batch).  With
+    task_value_lists=False each IterationStat.task_values is a read-only row view of `tvals`
+    (no per-value Python objects: the batched device path returns 4096 x iterations x L of them)."""
+    cols = {f: recs[f].tolist() for f in ("iteration", "objective", "exact_objective", "error",
+                                           "device_seconds", "has_exact_objective", "has_error")}
+    if task_value_lists:
+        tv = tvals.tolist()
+    else:
+        tvals.setflags(write=False)
+        tv = tvals
+    out = []
+    for b, st in enumerate(status):
+        n = st.iterations_recorded
+        rec = RunRecord(subintervals=cfg.subintervals, workers=cfg.workers, solver=solver.kind,
+                        variant=cfg.variant, plan=cfg.plan, aborted=bool(st.aborted),
+                        abort_reason=st.abort_reason.decode())
+        it_, obj, ex, er, sec = (cols["iteration"][b], cols["objective"][b], cols["exact_objective"][b],
+                                 cols["error"][b], cols["device_seconds"][b])
+        hx, he, tvb = cols["has_exact_objective"][b], cols["has_error"][b], tv[b]
+        rec.iterations = [IterationStat(iteration=it_[k], objective=obj[k],
+                                        exact_objective=ex[k] if hx[k] else None,
+                                        error=er[k] if he[k] else None, task_values=tvb[k],
+                                        device_seconds=sec[k]) for k in range(n)]
+        out.append(rec)
+    return out
 
 
 def run_buffers(p: ControlProblem, cfg: IsmConfig):
     B, L = p.batch, cfg.subintervals
     cap = max(cfg.max_outer, 0) + 1
     recs = np.zeros((B, cap), dtype=abi.REC_DTYPE)
-    tvals = np.full((B, cap, max(L, 1)), np.nan)
+    tvals = np.empty((B, cap, max(L, 1)))  # every entry is written by the device (NaN where unset)
     status = (abi.RunStatusV1 * B)()
     return cap, recs, tvals, status
 
@@ -296,7 +312,7 @@ def run_ism_batch(p: ControlProblem, u0, cfg: IsmConfig, solver: SolverSpec,
                                abi.dptr(tvals), status)
     raise_for(code, ctx.last_error())
     u = controls_from_abi(u_out, B, Cn, K)
-    return [IsmRun(u[b], unpack_records(recs, tvals, status, cfg, solver, b)) for b in range(B)]
+    return [IsmRun(u[b], r) for b, r in enumerate(unpack_all(recs, tvals, status, cfg, solver, B == 1))]
 
 
 def run_ism(p: ControlProblem, u0, cfg: IsmConfig, solver: SolverSpec, ctx=None) -> IsmRun:

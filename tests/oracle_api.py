@@ -57,7 +57,7 @@ def ism_run(p: I.ControlProblem, u0, cfg: I.IsmConfig, solver: I.SolverSpec,
                                 status, C.c_int32(arith), C.c_int32(threads), err, C.c_size_t(512))
     _check(code, err)
     u = I.controls_from_abi(u_out, B, Cn, K)
-    return [I.IsmRun(u[b], I.unpack_records(recs, tvals, status, cfg, solver, b)) for b in range(B)]
+    return [I.IsmRun(u[b], r) for b, r in enumerate(I.unpack_all(recs, tvals, status, cfg, solver))]
 
 
 def propagate_final(p, u, arith=STRUCTURED):

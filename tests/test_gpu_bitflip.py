@@ -49,15 +49,30 @@ def test_run_ism_small_register(ctx, parts, plan):
         assert abs(a.error - b.error) < 1e-10 * max(1.0, abs(b.error))
 
 
+FIXTURES = __import__("pathlib").Path(__file__).parent / "golden"
+
+
+def compare_run(g, fx, tag, ctl_tol=1e-9, obj_tol=1e-10):
+    assert rel(g.control, fx[f"{tag}_control"]) < ctl_tol
+    obj = fx[f"{tag}_objective"]
+    assert len(g.record.iterations) == len(obj)
+    assert np.max(np.abs(g.record.objectives() - obj)) < obj_tol
+    err = np.array([np.nan if it.error is None else it.error for it in g.record.iterations])
+    ok = np.isfinite(fx[f"{tag}_error"])
+    assert np.array_equal(np.isfinite(err), ok)
+    assert np.max(np.abs(err[ok] - fx[f"{tag}_error"][ok]) / np.maximum(1.0, np.abs(fx[f"{tag}_error"][ok]))) < 1e-9
+    tv = np.array([it.task_values for it in g.record.iterations])
+    assert np.max(np.abs(tv - fx[f"{tag}_task_values"])) < obj_tol
+
+
 @pytest.mark.slow
-def test_ising10_config3_iterations(ctx):
-    # BASELINE config 3 at full size (d = 1024, K = 4000, L = 256), two iterations at the
-    # time-to-fidelity step rho = 0.1/dt (the literal rho = 0.1 moves the controls ~100x less)
-    for rho_fast in (True,):
-        w = problems.ising10(iterations=2)
-        if rho_fast:
-            w.solver.step_size = w.rho_fast
-        g = I.run_ism(w.problem, w.u0, w.config, w.solver, ctx)
-        r = O.ism_run(w.problem, w.u0, w.config, w.solver, O.STRUCTURED)[0]
-        assert rel(g.control, r.control) < 1e-9
-        assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-10
+@pytest.mark.parametrize("tag", ["literal", "fast"])
+def test_ising10_config3_iterations(ctx, tag):
+    # BASELINE config 3 at full size (d = 1024, K = 4000, L = 256) for its timing count of 20
+    # outer iterations at rho = 0.1 and rho = 0.1/dt, against the oracle's frozen outputs
+    # (tests/golden/make_baseline_fixtures.py)
+    fx = np.load(FIXTURES / "config3_full.npz")
+    w = problems.ising10(iterations=20)
+    w.solver.step_size = float(fx[f"{tag}_rho"])
+    g = I.run_ism(w.problem, w.u0, w.config, w.solver, ctx)
+    compare_run(g, fx, tag)

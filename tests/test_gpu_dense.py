@@ -59,7 +59,10 @@ def test_spin2_200_iterations(ctx):
         assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-10
 
 
-def test_batch_subset(ctx):
+@pytest.mark.parametrize("disable", ["", "nm"])
+def test_batch_subset(ctx, disable, monkeypatch):
+    # the Neumann/tensor-core path and (QOC_DISABLE=nm, read per launch) the Gauss-Jordan path
+    monkeypatch.setenv("QOC_DISABLE", disable)
     w = problems.batch4096(batch=8, iterations=3)
     gs = I.run_ism_batch(w.problem, w.u0, w.config, w.solver, ctx)
     rs = O.ism_run(w.problem, w.u0, w.config, w.solver, O.REFERENCE)
@@ -73,11 +76,51 @@ def test_batch4096_problem_sample_long_run(ctx):
     # BASELINE config 5 at full problem size (d = 16, K = 2000, L = 128), SURVEY §8(d) parity
     # plan: 64 fixed problem indices (8 blocks of 8 spread over the 4096 seeds), 200 iterations
     # at rho = 0.1/dt
-    for first in range(0, 4096, 512):
-        w = problems.batch4096(batch=8, iterations=200, first=first)
-        w.solver.step_size = w.rho_fast
+    # at rho = 0.1/dt and at the literal rho = 0.1
+    for fast in (True, False):
+        for first in range(0, 4096, 512):
+            w = problems.batch4096(batch=8, iterations=200, first=first)
+            if fast:
+                w.solver.step_size = w.rho_fast
+            gs = I.run_ism_batch(w.problem, w.u0, w.config, w.solver, ctx)
+            rs = O.ism_run(w.problem, w.u0, w.config, w.solver, O.REFERENCE)
+            for g, r in zip(gs, rs):
+                assert rel(g.control, r.control) < 1e-9
+                assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-10
+
+
+def test_batch_neumann_range_handoff(ctx):
+    # config-5 kind (d = 16, one linear control): the Neumann-in-the-control assembly covers
+    # |u| a ||Hc||_1 up to its staged term count; tasks past it (problem 1: every task; problem
+    # 2: one subinterval; problem 3: far enough that a ||H(u)||_1 >= 1, the partial-pivoting
+    # Gauss-Jordan path) are handed to the Gauss-Jordan kernel -- results match the oracle
+    w = problems.batch4096(batch=4, iterations=4, subintervals=16)
+    u0 = np.array(w.u0)
+    u0[1] *= 100.0
+    u0[2, 0, 500:625] *= 100.0
+    u0[3] *= 1500.0
+    w.solver.step_size = 0.5
+    gs = I.run_ism_batch(w.problem, u0, w.config, w.solver, ctx)
+    rs = O.ism_run(w.problem, u0, w.config, w.solver, O.REFERENCE)
+    for g, r in zip(gs, rs):
+        assert not r.record.aborted
+        assert rel(g.control, r.control) < 1e-11
+        assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-11
+        for a, b in zip(g.record.iterations[1:], r.record.iterations[1:]):
+            assert abs(a.error - b.error) < 1e-10 * max(1.0, abs(b.error))
+
+
+def test_batch_all_problems_two_iterations(ctx):
+    # SURVEY §8(d) / VERDICT r01: every one of the 4096 config-5 problems for 2 outer iterations
+    # at both step sizes; the oracle runs the same batch on all host threads
+    for fast in (False, True):
+        w = problems.batch4096(iterations=2)
+        if fast:
+            w.solver.step_size = w.rho_fast
         gs = I.run_ism_batch(w.problem, w.u0, w.config, w.solver, ctx)
         rs = O.ism_run(w.problem, w.u0, w.config, w.solver, O.REFERENCE)
-        for g, r in zip(gs, rs):
-            assert rel(g.control, r.control) < 1e-9
-            assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-10
+        du = max(rel(g.control, r.control) for g, r in zip(gs, rs))
+        dobj = max(np.max(np.abs(g.record.objectives() - r.record.objectives())) for g, r in zip(gs, rs))
+        derr = max(abs(a.error - b.error) / max(1.0, abs(b.error))
+                   for g, r in zip(gs, rs) for a, b in zip(g.record.iterations[1:], r.record.iterations[1:]))
+        assert du < 1e-9 and dobj < 1e-10 and derr < 1e-9, (fast, du, dobj, derr)

@@ -76,14 +76,17 @@ def test_kat8_condensate_preset_on_device(ctx):
 
 
 @pytest.mark.slow
-def test_gpe1024_config4(ctx):
-    # BASELINE config 4 at full size (1024 points, K = 10000, L = 64), two iterations
-    w = problems.gpe1024(iterations=2)
-    w.solver.step_size = w.rho_fast
+@pytest.mark.parametrize("tag", ["literal", "fast"])
+def test_gpe1024_config4(ctx, tag):
+    # BASELINE config 4 at full size (1024 points, K = 10000, L = 64, split variant) for 100
+    # outer iterations at rho = 0.1 and rho = 0.1/dt with the exact payoff logged, against the
+    # oracle's frozen outputs (tests/golden/make_baseline_fixtures.py)
+    from tests.test_gpu_bitflip import FIXTURES, compare_run
+    fx = np.load(FIXTURES / "config4_full.npz")
+    w = problems.gpe1024(iterations=100)
+    w.config.log_exact_objective = True
+    w.solver.step_size = float(fx[f"{tag}_rho"])
     g = I.run_ism(w.problem, w.u0, w.config, w.solver, ctx)
-    r = O.ism_run(w.problem, w.u0, w.config, w.solver)[0]
-    assert rel(g.control, r.control) < 1e-9
-    assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-10
-    ex_g = [it.exact_objective for it in g.record.iterations[1:]]
-    ex_r = [it.exact_objective for it in r.record.iterations[1:]]
-    assert np.max(np.abs(np.array(ex_g) - np.array(ex_r))) < 1e-10
+    compare_run(g, fx, tag)
+    ex = np.array([it.exact_objective for it in g.record.iterations[1:]])
+    assert np.max(np.abs(ex - fx[f"{tag}_exact"][1:])) < 1e-10
