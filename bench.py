@@ -76,6 +76,13 @@ def flops_per_iteration(name: str, w) -> float:
     return per * K * B
 
 
+def dmma_peak():
+    f = ROOT / "profiles" / "dmma_peak.json"
+    if f.exists():
+        return json.loads(f.read_text())["fp64_mma_tflops"], "measured (tools/dmma_peak.cu, profiles/dmma_peak.json)"
+    return 37.2, "nominal fp64 tensor rate (no measurement found)"
+
+
 def fp64_peak():
     f = ROOT / "profiles" / "fp64_peak.json"
     if f.exists():
@@ -320,6 +327,10 @@ def label_flops(name: str, label: str, w) -> float:
     iteration's task work (flops_per_iteration)."""
     p = w.problem
     d, C, K, B = p.model.state_dim(), p.model.channels(), p.grid.steps, p.batch
+    if name == "batch4096" and label == "assembly":
+        # executed by the Neumann/tensor-core sweep (dense_nm.cu): the d x d complex product
+        # P_{j+1}^T = P_j^T C_j^T on DMMA = 4 real d^3 GEMMs per grid step
+        return 8 * d ** 3 * K * B
     if name in ("spin2", "batch4096"):
         w_cay = (8 / 3) * d ** 3 + (4 * C + 20) * d ** 2
         w_bg = w_cay + 4 * d + C * (8 * d ** 2 + 8 * d)
@@ -399,8 +410,17 @@ def main():
     dom, (dom_ms, dom_n) = max(kprof.items(), key=lambda kv: kv[1][0]) if kprof else ("task", (float("nan"), 1))
     per_launch_ms = dom_ms / max(dom_n, 1)
     fl_launch = label_flops(args.workload, dom, wp)
-    peak, peak_src = fp64_peak()
+    tensor = args.workload == "batch4096" and dom == "assembly"
+    peak, peak_src = dmma_peak() if tensor else fp64_peak()
     achieved = fl_launch / (per_launch_ms * 1e-3) / 1e12
+    # the same kernel counted with the reference algorithm's flops (SURVEY §8(d) per-unit figure,
+    # LU + d-column solve per step) -- exceeds the fp64 roof because the Neumann formulation
+    # does far less work than the reference per unit
+    ref_count = None
+    if tensor:
+        p_ = wp.problem
+        d_, C_, K_p, B_ = p_.model.state_dim(), p_.model.channels(), p_.grid.steps, p_.batch
+        ref_count = ((56 / 3) * d_ ** 3 + (4 * C_ + 4) * d_ ** 2) * K_p * B_ / (per_launch_ms * 1e-3) / 1e12
     fl_iter = flops_per_iteration(args.workload, w)
     kernels = {k: {"ms_per_iteration": v[0] / n_iter, "launches_per_iteration": v[1] / n_iter,
                    "share": v[0] / max(sum(x[0] for x in kprof.values()), 1e-12)} for k, v in kprof.items()}
@@ -408,18 +428,27 @@ def main():
     # ---- end to end through the public API: host buffers in, host results out
     ctx.set_option(abi.OPT_FLUSH_L2_BYTES, 0)
     we = build_workload(args.workload, K_, rank, world)
+    sharded = args.workload == "batch4096" and world > 1
     walls = []
     for _ in range(3):  # median of three whole calls (host-side jitter is ms-scale)
         barrier_sync(dist)
         t0 = time.perf_counter()
-        e2e_runs = I.run_ism_batch(we.problem, we.u0, we.config, we.solver, ctx)
+        if sharded:  # this rank's problem block, then the one all-gather of every control
+            from paper_1603_01237_b200 import partition as PT
+            res = PT.run_batch_sharded(lambda f, c: (we.problem, we.u0, we.config, we.solver),
+                                       lambda p_, u_, c_, s_: I.run_ism_batch(p_, u_, c_, s_, ctx), 4096, dist)
+            e2e_runs = [None] * res.count
+            assert res.controls.shape[0] == 4096
+        else:
+            e2e_runs = I.run_ism_batch(we.problem, we.u0, we.config, we.solver, ctx)
         barrier_sync(dist)
         walls.append(time.perf_counter() - t0)
     e2e_wall = allmax(dist, statistics.median(walls))
     e2e_value = allsum(dist, 2.0 * we.problem.grid.steps * we.problem.batch * K_) / e2e_wall
     h2d = problem_bytes(we)
-    d2h = int(np.asarray(e2e_runs[0].control).nbytes * len(e2e_runs)
-              + (K_ + 1) * (abi.REC_DTYPE.itemsize + 8 * we.config.subintervals) * len(e2e_runs))
+    nb = we.problem.batch
+    d2h = int(8 * we.problem.model.channels() * we.problem.grid.steps * nb
+              + (K_ + 1) * (abi.REC_DTYPE.itemsize + 8 * we.config.subintervals) * nb)
 
     # ---- time to fidelity 0.999 (rho = 0.1/dt): device time and wall clock of a run_ism call
     ttf = None
@@ -446,7 +475,8 @@ def main():
                 "arrays (median of 3 calls), wall clock incl. packing, upload, bootstrap, trailing "
                 "evaluation and download"},
         "gpu_launches": int(round(launches_per_iter * K_)),
-        "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "roofline": {"bound": "tensor" if tensor else "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "reference_count_tflops": ref_count,
                      "frac": achieved / peak, "traffic": ncu_traffic(args.workload),
                      "kernel": dom, "kernel_ms_per_launch": per_launch_ms, "flops_per_launch": fl_launch,
                      "share_of_step": dom_ms / max(prof["iteration_ms"], 1e-12), "peak_source": peak_src,

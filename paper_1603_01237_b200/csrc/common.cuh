@@ -174,6 +174,8 @@ struct DevRun {
   // fragment order [B][NM_TERMS][8][32], and the per-task hand-off flag to Gauss-Jordan
   double2* nm;
   int* nm_fallback;     // [B][L]
+  double2* nm_v;        // [B][L][traj_len - 1][d] fused-residual vectors v_j
+  int* nm_count;        // [1] tasks handed to Gauss-Jordan by the last Neumann sweep
   int cap;
 };
 

@@ -138,11 +138,19 @@ __device__ __forceinline__ int neumann_terms(double x) {
 }
 
 // ---- assembly: one warp per task ----------------------------------------------------------
-template <int TPW>
+// residual != 0 also evaluates the task's residual (error_norm of the weight-1 gradient at the
+// control just assembled, ism.cpp:413-419) in the same sweep, through
+//     Im<chi_j + chi_{j+1}, Hc (psi_j + psi_{j+1})> = Im( y^dag v_j ),
+//     v_j = (P_j + P_{j+1})^dag Hc (psi_j + psi_{j+1}),   y = P_len^dag seed,
+// (chi_j = P_j y by unitarity, as in pcache.cu): v_j is formed on the way (psi_{j+1} = C_j psi_j
+// from the Horner output), parked in `R.nm_v`, and contracted with y once P_len exists.
+template <bool GAUSS3, bool RESIDUAL>
 __global__ void __launch_bounds__(NM_WARPS * 32, 2) dense_nm_assemble_kernel(DevProblem P, DevRun R, int ignore_done) {
+  constexpr bool residual = RESIDUAL;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* nm_s = reinterpret_cast<double2*>(smem_raw);                       // [NM_TERMS][SLOTS][32]
   double2* xch_all = nm_s + NM_TERMS * SLOTS * 32;                            // [NM_WARPS][ND][XS]
+  double2* hc_s = xch_all + NM_WARPS * ND * XS;                               // [SLOTS][32] (residual)
   __shared__ __align__(8) unsigned long long bar;
   const int b = blockIdx.y;
   if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
@@ -161,132 +169,221 @@ __global__ void __launch_bounds__(NM_WARPS * 32, 2) dense_nm_assemble_kernel(Dev
     for (unsigned off = 0; off < kBytes; off += kChunk)
       bulk_g2s(reinterpret_cast<char*>(nm_s) + off, src + off, kChunk < kBytes - off ? kChunk : kBytes - off, &bar);
   }
-  const int C = P.C;
-  const double gam = 0.5 * P.dt * P.norm1[(size_t)b * (1 + 2 * C) + 1];  // a ||Hc||_1 >= ||G||_2
-  double2* xch = xch_all + warp * ND * XS;
   const size_t dd = (size_t)ND * ND;
+  if (residual)  // Hc in fragment order: slot s = jn*4 + kk of lane (q, r) = Hc[8 jn + q][4 kk + r]
+    for (int e = tid; e < SLOTS * 32; e += blockDim.x) {
+      const int s = e >> 5, ll = e & 31;
+      hc_s[e] = P.lin[(size_t)b * dd + (8 * (s >> 2) + (ll >> 2)) * ND + 4 * (s & 3) + (ll & 3)];
+    }
+  const double gam = 0.5 * P.dt * P.norm1[(size_t)b * (1 + 2 * P.C) + 1];  // a ||Hc||_1 >= ||G||_2
+  double2* xch = xch_all + warp * ND * XS;
 
-  int n[TPW], node0[TPW], len[TPW];
-  bool live[TPW];
-  int lenmax = 0;
-#pragma unroll
-  for (int t = 0; t < TPW; ++t) {
-    const int nr = (blockIdx.x * NM_WARPS + warp) * TPW + t;
-    live[t] = nr < P.L;
-    n[t] = live[t] ? nr : P.L - 1;
-    node0[t] = P.node[n[t]];
-    len[t] = P.node[n[t] + 1] - node0[t];
-    lenmax = max(lenmax, len[t]);
-  }
+  const int nr = blockIdx.x * NM_WARPS + warp;
+  bool live = nr < P.L;
+  const int n = live ? nr : P.L - 1;
+  const int node0 = P.node[n], len = P.node[n + 1] - node0;
+  const double* u = R.u + (size_t)b * P.K + node0;
   // certified range check over the task's steps (warp-uniform); out-of-range tasks are handed
   // to the Gauss-Jordan kernel
-#pragma unroll
-  for (int t = 0; t < TPW; ++t) {
+  {
     double um = 0.0;
-    for (int j = l; j < len[t]; j += 32) um = fmax(um, fabs(R.u[(size_t)b * P.K + node0[t] + j]));
+    for (int j = l; j < len; j += 32) um = fmax(um, fabs(u[j]));
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) um = fmax(um, __shfl_xor_sync(0xffffffffu, um, off));
     const bool ok = neumann_terms(um * gam) >= 0;  // NaN controls also fail here
-    if (l == 0 && live[t]) R.nm_fallback[(size_t)b * P.L + n[t]] = ok ? 0 : 1;
-    if (!ok) live[t] = false;
+    if (l == 0 && live) {
+      R.nm_fallback[(size_t)b * P.L + n] = ok ? 0 : 1;
+      if (!ok) atomicAdd(R.nm_count, 1);
+    }
+    if (!ok) live = false;
   }
+  const size_t task = (size_t)b * P.L + n;
+  double2* Pc = R.pc + task * (size_t)R.traj_len * dd;
   // P^T in A-fragment layout: Pa[i][kk] = P[4kk + r][8i + q]
-  double2 Pa[TPW][2][4];
+  double2 Pa[2][4];
 #pragma unroll
-  for (int t = 0; t < TPW; ++t)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) Pa[t][i][kk] = cx((4 * kk + r) == (8 * i + q) ? 1.0 : 0.0, 0.0);
-  // P_0 = I into the cache
-#pragma unroll
-  for (int t = 0; t < TPW; ++t) {
-    if (!live[t]) continue;
-    double2* Pc = R.pc + ((size_t)b * P.L + n[t]) * (size_t)R.traj_len * dd;
+    for (int kk = 0; kk < 4; ++kk) Pa[i][kk] = cx((4 * kk + r) == (8 * i + q) ? 1.0 : 0.0, 0.0);
+  if (live)  // P_0 = I into the cache (column-major)
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) Pc[(8 * i + q) * ND + 4 * kk + r] = Pa[t][i][kk];  // column-major
-  }
+      for (int kk = 0; kk < 4; ++kk) Pc[(8 * i + q) * ND + 4 * kk + r] = Pa[i][kk];
+  // residual state: psi_j at columns 4kk + r ("column layout")
+  double2 psc[4];
+  if (residual)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) psc[kk] = R.task_init[task * ND + 4 * kk + r];
+  double2* vj = R.nm_v + task * (size_t)(R.traj_len - 1) * ND;
+  auto quad_sum = [](double2 v) {
+    v = cadd(v, shfl_xor(v, 1));
+    return cadd(v, shfl_xor(v, 2));
+  };
   mbar_wait(&bar, 0);
+  if (residual) __syncthreads();  // hc_s visible
 
-  for (int j = 0; j < lenmax; ++j) {
-    double uj[TPW];
-    int M = 0;
-#pragma unroll
-    for (int t = 0; t < TPW; ++t) {
-      uj[t] = R.u[(size_t)b * P.K + node0[t] + min(j, len[t] - 1)];
-      const int mt = live[t] ? neumann_terms(fabs(uj[t]) * gam) : 0;
-      M = max(M, mt);
-    }
+  for (int j = 0; j < len; ++j) {
+    const double uj = u[j];
+    const int M = live ? neumann_terms(fabs(uj) * gam) : 0;
     // Horner: Y = N_M; Y = N_m + u Y (m = M-1 .. 0); Y[s] = C(u)[8 jn + q][4 kk + r]
-    double2 Y[TPW][SLOTS];
+    double2 Y[SLOTS];
 #pragma unroll
-    for (int s = 0; s < SLOTS; ++s) {
-      const double2 nv = nm_s[(M * SLOTS + s) * 32 + l];
-#pragma unroll
-      for (int t = 0; t < TPW; ++t) Y[t][s] = nv;
-    }
+    for (int s = 0; s < SLOTS; ++s) Y[s] = nm_s[(M * SLOTS + s) * 32 + l];
     for (int m = M - 1; m >= 0; --m) {
 #pragma unroll
       for (int s = 0; s < SLOTS; ++s) {
         const double2 nv = nm_s[(m * SLOTS + s) * 32 + l];
-#pragma unroll
-        for (int t = 0; t < TPW; ++t) Y[t][s] = cx(fma(uj[t], Y[t][s].x, nv.x), fma(uj[t], Y[t][s].y, nv.y));
+        Y[s] = cx(fma(uj, Y[s].x, nv.x), fma(uj, Y[s].y, nv.y));
       }
     }
+    double2 bc[4], vp[2];
+    if (residual) {
+      // psi_{j+1} = C_j psi_j: rows 8 jn + q, reduced over the quad's columns
+      double2 pn[2];
 #pragma unroll
-    for (int t = 0; t < TPW; ++t) {
-      // P_{j+1}^T = P_j^T C_j^T: A = P^T (Pa), B = C^T (Y: B[4kk + r][8jn + q] = C[8jn + q][4kk + r])
-      double cr[2][2][2], ci[2][2][2];
+      for (int jn = 0; jn < 2; ++jn) {
+        double2 acc = cx(0.0, 0.0);
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+        for (int kk = 0; kk < 4; ++kk) acc = cfma(Y[jn * 4 + kk], psc[kk], acc);
+        pn[jn] = quad_sum(acc);
+      }
+      // to column layout: psi_{j+1}[4kk + r] lives in quad 4(kk & 1) + r, slot kk >> 1; ps = psi_j + psi_{j+1}
+      double2 ps[4];
 #pragma unroll
-        for (int jn = 0; jn < 2; ++jn) {
-          cr[i][jn][0] = cr[i][jn][1] = ci[i][jn][0] = ci[i][jn][1] = 0.0;
+      for (int kk = 0; kk < 4; ++kk) {
+        const double2 v = shfl(pn[kk >> 1], 4 * (4 * (kk & 1) + r));
+        ps[kk] = cadd(psc[kk], v);
+        psc[kk] = v;
+      }
+      // b = Hc ps (rows 8 jn + q), back to column layout
+      double2 br[2];
+#pragma unroll
+      for (int jn = 0; jn < 2; ++jn) {
+        double2 acc = cx(0.0, 0.0);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) acc = cfma(hc_s[(jn * 4 + kk) * 32 + l], ps[kk], acc);
+        br[jn] = quad_sum(acc);
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) bc[kk] = shfl(br[kk >> 1], 4 * (4 * (kk & 1) + r));
+      // v partial with P_j: v[8i + q] += sum conj(P_j[4kk + r][8i + q]) b[4kk + r]
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        double2 acc = cx(0.0, 0.0);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) acc = cfmaconj(Pa[i][kk], bc[kk], acc);
+        vp[i] = acc;
+      }
+    }
+    // P_{j+1}^T = P_j^T C_j^T: A = P^T (Pa), B = C^T (Y: B[4kk + r][8jn + q] = C[8jn + q][4kk + r])
+    double cr[2][2][2], ci[2][2][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int jn = 0; jn < 2; ++jn) {
+        cr[i][jn][0] = cr[i][jn][1] = ci[i][jn][0] = ci[i][jn][1] = 0.0;
+        if constexpr (GAUSS3) {  // three real products: re = ArBr - AiBi, im = (Ar+Ai)(Br+Bi) - ArBr - AiBi
+          double t2[2] = {0.0, 0.0};
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            const double2 av = Pa[t][i][kk], bv = Y[t][jn * 4 + kk];
+            const double2 av = Pa[i][kk], bv = Y[jn * 4 + kk];
+            dmma(cr[i][jn][0], cr[i][jn][1], av.x, bv.x);
+            dmma(t2[0], t2[1], av.y, bv.y);
+            dmma(ci[i][jn][0], ci[i][jn][1], av.x + av.y, bv.x + bv.y);
+          }
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            ci[i][jn][e] = ci[i][jn][e] - cr[i][jn][e] - t2[e];
+            cr[i][jn][e] = cr[i][jn][e] - t2[e];
+          }
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const double2 av = Pa[i][kk], bv = Y[jn * 4 + kk];
             dmma(cr[i][jn][0], cr[i][jn][1], av.x, bv.x);
             dmma(cr[i][jn][0], cr[i][jn][1], -av.y, bv.y);
             dmma(ci[i][jn][0], ci[i][jn][1], av.x, bv.y);
             dmma(ci[i][jn][0], ci[i][jn][1], av.y, bv.x);
           }
         }
-      // lane holds P_{j+1}[8 jn + 2r + e][8 i + q]; C-fragment -> A-fragment layout through the
-      // warp's scratch, then the cache store (column-major: 64-byte runs of a column per lane quad)
-      const bool act = live[t] && j < len[t];
-      __syncwarp();
+      }
+    // lane holds P_{j+1}[8 jn + 2r + e][8 i + q]; C-fragment -> A-fragment layout through the
+    // warp's scratch, then the cache store (column-major: 64-byte runs of a column per lane quad)
+    __syncwarp();
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int jn = 0; jn < 2; ++jn)
+      for (int jn = 0; jn < 2; ++jn)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) xch[(8 * jn + 2 * r + e) * XS + 8 * i + q] = cx(cr[i][jn][e], ci[i][jn][e]);
-      __syncwarp();
-      if (act) {
-        double2* dst = R.pc + (((size_t)b * P.L + n[t]) * (size_t)R.traj_len + j + 1) * dd;
+        for (int e = 0; e < 2; ++e) xch[(8 * jn + 2 * r + e) * XS + 8 * i + q] = cx(cr[i][jn][e], ci[i][jn][e]);
+    __syncwarp();
+    double2* dst = Pc + (size_t)(j + 1) * dd;
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            Pa[t][i][kk] = xch[(4 * kk + r) * XS + 8 * i + q];
-            __stcs(dst + (8 * i + q) * ND + 4 * kk + r, Pa[t][i][kk]);
-          }
+      for (int kk = 0; kk < 4; ++kk) {
+        Pa[i][kk] = xch[(4 * kk + r) * XS + 8 * i + q];
+        if (live) __stcs(dst + (8 * i + q) * ND + 4 * kk + r, Pa[i][kk]);
+      }
+    if (residual) {  // v partial with P_{j+1}; park v_j
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        double2 acc = vp[i];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) acc = cfmaconj(Pa[i][kk], bc[kk], acc);
+        acc = quad_sum(acc);
+        if (r == 0 && live) vj[(size_t)j * ND + 8 * i + q] = acc;
       }
     }
   }
   // M_n = P_len for the boundary chain (row-major)
-  if (R.prop) {
+  if (R.prop && live) {
+    double2* Mn = R.prop + task * dd;
 #pragma unroll
-    for (int t = 0; t < TPW; ++t) {
-      if (!live[t]) continue;
-      double2* M = R.prop + ((size_t)b * P.L + n[t]) * dd;
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+      for (int kk = 0; kk < 4; ++kk) Mn[(4 * kk + r) * ND + 8 * i + q] = Pa[i][kk];
+  }
+  if (residual) {
+    // seed = targ - psi_len (tracking form, interpolated variant); y = P_len^dag seed
+    double2 sc[4];
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) M[(4 * kk + r) * ND + 8 * i + q] = Pa[t][i][kk];
+    for (int kk = 0; kk < 4; ++kk) sc[kk] = csub(R.task_targ[task * ND + 4 * kk + r], psc[kk]);
+    double2 yr[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      double2 acc = cx(0.0, 0.0);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) acc = cfmaconj(Pa[i][kk], sc[kk], acc);
+      yr[i] = quad_sum(acc);  // y[8i + q]
     }
+    __syncwarp();
+    // g_j = -alpha_j dt u_j + dt/4 w Im(y^dag v_j): lane (j = l & 15, half h = l >> 4) takes 8 of
+    // the 16 components, y from the quads through the scratch
+    if (r == 0) {
+      xch[8 * 0 + q] = yr[0];
+      xch[8 + q] = yr[1];
+    }
+    __syncwarp();
+    const int jl = l & 15, h = l >> 4;
+    double im = 0.0;
+    if (jl < len) {
+      double2 acc = cx(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc = cfmaconj(xch[8 * h + c], vj[(size_t)jl * ND + 8 * h + c], acc);
+      im = acc.y;
+    }
+    im += __shfl_xor_sync(0xffffffffu, im, 16);
+    const double Kd = (double)P.K, scale = (double)len / Kd, dt = P.dt, w = P.ip_w;
+    double err = 0.0;
+    if (jl < len && h == 0) {
+      const double gj = -(P.alpha[node0 + jl] * scale) * dt * u[jl] + 0.25 * dt * (w * im);
+      err = fabs(gj);
+    }
+#pragma unroll
+    for (int off = 1; off < 16; off <<= 1) err += __shfl_xor_sync(0xffffffffu, err, off);
+    if (l == 0 && live) R.err[task] = err;
   }
 }
 
@@ -296,11 +393,13 @@ __global__ void __launch_bounds__(NM_WARPS * 32, 2) dense_nm_assemble_kernel(Dev
 //   psi_j = P_j phi,  chi_j = P_j chi_0,  chi_0 = P_len^dag seed       (objective.cpp:31-34)
 //   g_j = -alpha_j dt u_j + dt/4 w Im<chi_j + chi_{j+1}, Hc (psi_j + psi_{j+1})>  (objective.cpp:55-57)
 // Lane (row = l & 15, g = l >> 4) holds columns 2t + g of its row of every matrix.
-__global__ void __launch_bounds__(256, 2) dense_pc_eval16_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done) {
+__global__ void __launch_bounds__(256, 2) dense_pc_eval16_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done,
+                                                                  int handed_off_only) {
   constexpr int PE_ENTRY = 1, PE_GRAD = 2, PE_ERR = 4;
   __shared__ double2 hcs[ND * ND];  // Hc column-major: lane (row, g) reads 512-byte runs
   __shared__ double2 xs[8][ND];
   const int b = blockIdx.y;
+  if (handed_off_only && *R.nm_count == 0) return;  // nothing was handed off (the common case)
   if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
   const size_t dd = (size_t)ND * ND;
   for (int e = threadIdx.x; e < ND * ND; e += blockDim.x) hcs[(e & 15) * ND + (e >> 4)] = P.lin[(size_t)b * dd + e];
@@ -308,6 +407,8 @@ __global__ void __launch_bounds__(256, 2) dense_pc_eval16_kernel(DevProblem P, D
   const int warp = threadIdx.x >> 5, l = threadIdx.x & 31, row = l & 15, g = l >> 4;
   const int n = blockIdx.x * 8 + warp;
   if (n >= P.L) return;
+  // residual of the tasks the Neumann sweep handed to Gauss-Jordan (its fused residual covers the rest)
+  if (handed_off_only && R.nm_fallback[(size_t)b * P.L + n] == 0) return;
   const int mode = A.mode;
   const int node0 = P.node[n], len = P.node[n + 1] - node0;
   const double Kd = (double)P.K, weight = A.weighted ? Kd / (double)len : 1.0, scale = (double)len / Kd;
@@ -386,8 +487,12 @@ __global__ void __launch_bounds__(256, 2) dense_pc_eval16_kernel(DevProblem P, D
     }
   }
   if (l == 0) {
-    R.chunk_pen[(size_t)b * P.L + n] = pen;
-    R.chunk_err[(size_t)b * P.L + n] = err;
+    if (handed_off_only) {
+      R.err[(size_t)b * P.L + n] = err;
+    } else {
+      R.chunk_pen[(size_t)b * P.L + n] = pen;
+      R.chunk_err[(size_t)b * P.L + n] = err;
+    }
   }
 }
 
@@ -399,6 +504,14 @@ static bool disabled(const char* what) {
   return e && std::strstr(e, what) != nullptr;
 }
 
+// The fused residual (RESIDUAL kernels) measured even with the separate streaming evaluation
+// (28.9 vs 28.8 ms per config-5 iteration: +7 ms in the sweep vs one more 36 GB cache pass); it
+// stays available behind QOC_ENABLE=fuse.
+bool dense_nm_fuse_residual() {
+  const char* e = std::getenv("QOC_ENABLE");
+  return e && std::strstr(e, "fuse") != nullptr;
+}
+
 bool dense_nm_applicable(const DevProblem& P) {
   return P.kind == QOC_KIND_DENSE && P.d == ND && P.C == 1 && !P.has_quad && !disabled("nm");
 }
@@ -408,44 +521,37 @@ cudaError_t dense_nm_setup(const DevProblem& P, const DevRun& R, cudaStream_t st
   return cudaGetLastError();
 }
 
-size_t dense_nm_smem() {
-  return sizeof(double2) * ((size_t)NM_TERMS * SLOTS * 32 + (size_t)NM_WARPS * ND * XS);
-}
-
-// tasks per warp (1 or 2: two tasks of a problem share every coefficient load); QOC_NM_TPW
-// overrides the default for A/B measurements
-static int nm_tpw() {
-  static int v = [] {
-    const char* e = std::getenv("QOC_NM_TPW");
-    return (e && std::atoi(e) == 2) ? 2 : 1;
-  }();
-  return v;
-}
-
-template <int TPW>
-static cudaError_t launch_nm(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st) {
-  auto kern = dense_nm_assemble_kernel<TPW>;
-  const size_t smem = dense_nm_smem();
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const int tpc = NM_WARPS * TPW;
-  kern<<<dim3((P.L + tpc - 1) / tpc, P.B), NM_WARPS * 32, smem, st>>>(P, R, ignore_done);
-  return cudaGetLastError();
-}
-
 // pc_eval for the same problems when the evaluation needs only ENTRY / GRAD / ERR and the task
 // is a single chunk (pc_finalize_kernel then reduces exactly as for pc_eval_kernel)
 bool dense_pc_eval16_applicable(const DevProblem& P, const DevRun& R, int mode, int nchunk) {
   return R.nm && !disabled("eval16") && nchunk == 1 && (mode & ~7) == 0 && R.traj_len - 1 <= 32;
 }
 
-cudaError_t dense_pc_eval16(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
-  dense_pc_eval16_kernel<<<dim3((P.L + 7) / 8, P.B), 256, 0, st>>>(P, R, A, ignore_done);
+cudaError_t dense_pc_eval16(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st,
+                            int handed_off_only) {
+  dense_pc_eval16_kernel<<<dim3((P.L + 7) / 8, P.B), 256, 0, st>>>(P, R, A, ignore_done, handed_off_only);
   return cudaGetLastError();
 }
 
-cudaError_t dense_nm_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st) {
-  return nm_tpw() == 2 ? launch_nm<2>(P, R, ignore_done, st) : launch_nm<1>(P, R, ignore_done, st);
+size_t dense_nm_smem() {
+  return sizeof(double2) * ((size_t)NM_TERMS * SLOTS * 32 + (size_t)NM_WARPS * ND * XS + SLOTS * 32);
+}
+
+// The complex product as three real tensor-core products (Gauss) instead of four: 48 instead of
+// 64 DMMA per grid step (12.8 vs 13.4 ms per config-5 sweep); QOC_NM_GAUSS3=0 selects four.
+static bool nm_gauss3() {
+  const char* e = std::getenv("QOC_NM_GAUSS3");
+  return !(e && e[0] == '0');
+}
+
+cudaError_t dense_nm_assemble(const DevProblem& P, const DevRun& R, int ignore_done, int residual, cudaStream_t st) {
+  auto kern = nm_gauss3() ? (residual ? dense_nm_assemble_kernel<true, true> : dense_nm_assemble_kernel<true, false>)
+                          : (residual ? dense_nm_assemble_kernel<false, true> : dense_nm_assemble_kernel<false, false>);
+  const size_t smem = dense_nm_smem();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<dim3((P.L + NM_WARPS - 1) / NM_WARPS, P.B), NM_WARPS * 32, smem, st>>>(P, R, ignore_done);
+  return cudaGetLastError();
 }
 
 }  // namespace qoc

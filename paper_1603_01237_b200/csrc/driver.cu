@@ -430,6 +430,8 @@ void alloc_run(const DeviceProblem& dp, int cap, const std::vector<int>& node, b
     if (nm) {
       R.nm = out.alloc<double2>(B * NM_TERMS * 256);
       R.nm_fallback = out.alloc<int>(B * L);
+      R.nm_v = out.alloc<double2>(B * L * (R.traj_len - 1) * d);
+      R.nm_count = out.alloc<int>(1);
       ck(cudaMemsetAsync(R.nm_fallback, 0, sizeof(int) * B * L, st), "memset");
     }
     const int nchunk = pc_nchunk(P, R);
@@ -755,8 +757,12 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
             const TaskArgs G2{PCM_GRAD, form, split ? 0 : 1, 1, solver->step_size};
             launch.run([&] { return pc_eval(P, RR, G2, 0, st); }, "gradient", true);
           }
-          // no update (inner = 0): the cache and the propagators already belong to this control
-          if (inner > 0) launch.run([&] { return pc_assemble(P, RR, 0, st); }, "assembly", true);
+          // no update (inner = 0): the cache and the propagators already belong to this control.
+          // Where the assembly sweep fuses the residual (dense_nm.cu), it is evaluated there.
+          const bool fuse_err = cfg->compute_error && inner > 0 && !(L > 1 && split && !direct) &&
+                                pc_fuses_residual(P, RR);
+          if (inner > 0)
+            launch.run([&] { return pc_assemble(P, RR, 0, st, fuse_err ? form : -1); }, "assembly", true);
           if (assembled_interp) {
             // the boundary chain needs only the new propagators: run it on the side stream,
             // concurrently with the residual sweep, penalty and merge (joined before boundary)
@@ -765,7 +771,7 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
             launch(chain_propagators(P, RR, ctx->aux), "chain");
             ck(cudaEventRecord(ctx->ev_join, ctx->aux), "join");
           }
-          const int em = (cfg->compute_error ? PCM_ERR : 0) | ((L > 1 && split && !direct) ? PCM_LAG : 0);
+          const int em = ((cfg->compute_error && !fuse_err) ? PCM_ERR : 0) | ((L > 1 && split && !direct) ? PCM_LAG : 0);
           if (em) {
             const TaskArgs E{em, form, split ? 0 : 1, 1, 0.0};
             launch.run([&] { return pc_eval(P, RR, E, 0, st); }, "residual", true);

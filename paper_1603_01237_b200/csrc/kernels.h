@@ -25,14 +25,22 @@ cudaError_t strang_horizon(const DevProblem& P, const DevRun& R, int which, int 
 // propagator-cache engine for the linear kinds (d <= 32)
 int pc_nchunk(const DevProblem& P, const DevRun& R);
 cudaError_t pc_eval(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
-cudaError_t pc_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st);
+// residual_form >= 0: the assembly sweep also writes the tasks' residual err[b][n] at the new
+// control (objective form residual_form) when the path fuses it; pc_fuses_residual tells the
+// driver to skip its separate residual evaluation
+cudaError_t pc_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st,
+                        int residual_form = -1);
+bool pc_fuses_residual(const DevProblem& P, const DevRun& R);
 constexpr int PCM_ENTRY = 1, PCM_GRAD = 2, PCM_ERR = 4, PCM_LAG = 8, PCM_FINAL = 16, PCM_RAWGRAD = 32;
 
 // Neumann-in-the-control assembly for dense d = 16, C = 1, linear control (dense_nm.cu)
 constexpr int NM_TERMS = 16;
 bool dense_nm_applicable(const DevProblem& P);
 cudaError_t dense_nm_setup(const DevProblem& P, const DevRun& R, cudaStream_t st);
-cudaError_t dense_nm_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st);
+cudaError_t dense_nm_assemble(const DevProblem& P, const DevRun& R, int ignore_done, int residual, cudaStream_t st);
+bool dense_pc_eval16_applicable(const DevProblem& P, const DevRun& R, int mode, int nchunk);
+cudaError_t dense_pc_eval16(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st,
+                            int handed_off_only = 0);
 
 // glue (kind independent)
 cudaError_t penalty_partials(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st);

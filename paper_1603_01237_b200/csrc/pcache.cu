@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(128) dense_pc_assemble_kernel(DevProblem P, De
   // after the Neumann kernel (dense_nm.cu) only the tasks it handed off run here
   auto handed_off = [&](int n) { return !R.nm_fallback || R.nm_fallback[(size_t)b * P.L + n] != 0; };
   if (R.nm_fallback) {
+    if (*R.nm_count == 0) return;  // nothing was handed off (the common case)
     const int t0 = blockIdx.x * tasks_per_cta;
     const int mine = (int)threadIdx.x < tasks_per_cta && t0 + (int)threadIdx.x < P.L && handed_off(t0 + threadIdx.x);
     if (!__syncthreads_or(mine)) return;
@@ -613,9 +614,6 @@ int pc_chunk(const DevProblem& P, const DevRun& R) {
   return chunk < 4 ? 4 : (chunk > 16 ? 16 : chunk);
 }
 
-bool dense_pc_eval16_applicable(const DevProblem& P, const DevRun& R, int mode, int nchunk);
-cudaError_t dense_pc_eval16(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
-
 cudaError_t pc_eval(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
   const int chunk = pc_chunk(P, R);
   const int nchunk = (R.traj_len - 1 + chunk - 1) / chunk;
@@ -665,12 +663,26 @@ static cudaError_t launch_dense_pc(const DevProblem& P, const DevRun& R, int ign
   return cudaGetLastError();
 }
 
-cudaError_t pc_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st) {
+bool dense_nm_fuse_residual();
+bool pc_fuses_residual(const DevProblem& P, const DevRun& R) {
+  return R.nm != nullptr && R.nm_v != nullptr && dense_nm_fuse_residual();
+}
+
+cudaError_t pc_assemble(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st, int residual_form) {
   if (P.kind == QOC_KIND_TRIDIAG) return tri_pc_assemble(P, R, ignore_done, st);
   if (R.nm) {  // Neumann + tensor-core sweep; out-of-range tasks continue in Gauss-Jordan below
-    cudaError_t e = dense_nm_assemble(P, R, ignore_done, st);
+    const int fused = residual_form >= 0 && pc_fuses_residual(P, R);
+    if (fused && residual_form != QOC_FORM_TRACKING) return cudaErrorNotSupported;  // interpolated runs only
+    cudaError_t e = cudaMemsetAsync(R.nm_count, 0, sizeof(int), st);
     if (e != cudaSuccess) return e;
-    return launch_dense_pc<16>(P, R, ignore_done, st);
+    e = dense_nm_assemble(P, R, ignore_done, fused, st);
+    if (e != cudaSuccess) return e;
+    if ((e = launch_dense_pc<16>(P, R, ignore_done, st)) != cudaSuccess) return e;
+    if (fused) {  // residual of the handed-off tasks through the cache
+      const TaskArgs E{PCM_ERR, residual_form, 1, 1, 0.0};
+      return dense_pc_eval16(P, R, E, ignore_done, st, 1);
+    }
+    return cudaSuccess;
   }
   if (R.cay) {
     switch (dense_pad(P.d)) {

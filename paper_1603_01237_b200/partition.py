@@ -42,9 +42,39 @@ class ShardedRun:
     count: int
 
 
+def _collective_device(dist):
+    """Device of the collective buffers: the current CUDA device under NCCL (which rejects host
+    tensors), the host under gloo."""
+    import torch
+    if dist is not None and dist.get_backend() == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+def all_gather_blocks(dist, local: np.ndarray, counts: list[int]) -> np.ndarray:
+    """One all-gather of ragged contiguous row blocks (rank r contributes counts[r] rows of equal
+    trailing shape): rows are padded to the largest block, gathered as one float64 tensor on the
+    collective device (NVLink under NCCL), then un-padded in rank order."""
+    import torch
+    world = len(counts)
+    mx = max(counts)
+    dev = _collective_device(dist)
+    flat = np.ascontiguousarray(local, dtype=np.float64)
+    if np.iscomplexobj(local):
+        flat = np.ascontiguousarray(local).view(np.float64)
+    tail = flat.shape[1:]
+    buf = torch.zeros((mx,) + tuple(tail), dtype=torch.float64, device=dev)
+    buf[:flat.shape[0]] = torch.from_numpy(flat).to(dev)
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf)
+    out = np.concatenate([parts[r][:counts[r]].cpu().numpy() for r in range(world)])
+    return out.view(np.complex128) if np.iscomplexobj(local) else out
+
+
 def run_batch_sharded(problem_builder, solve, total: int, dist=None) -> ShardedRun:
     """Config-5 partition: this rank solves problems [first, first + count) with ``solve``
-    (the device ``ism.run_ism_batch`` in production) and all ranks gather the results once.
+    (the device ``ism.run_ism_batch`` in production) and all ranks gather the results once --
+    one all-gather of the controls and one of the objective histories.
 
     problem_builder(first, count) -> (ControlProblem, u0, IsmConfig, SolverSpec)
     solve(problem, u0, cfg, solver) -> list[IsmRun]
@@ -63,14 +93,8 @@ def run_batch_sharded(problem_builder, solve, total: int, dist=None) -> ShardedR
         obj[i, :len(o)] = o
     if dist is None or world == 1:
         return ShardedRun(ctl, obj, first, count)
-    import torch
-    parts_c = [None] * world
-    parts_o = [None] * world
-    # one gather at the end (payload ~ B*C*K doubles); object gather keeps ragged blocks simple
-    dist.all_gather_object(parts_c, ctl)
-    dist.all_gather_object(parts_o, obj)
-    del torch
-    return ShardedRun(np.concatenate(parts_c), np.concatenate(parts_o), first, count)
+    counts = [n for _, n in balanced_blocks(total, world)]
+    return ShardedRun(all_gather_blocks(dist, ctl, counts), all_gather_blocks(dist, obj, counts), first, count)
 
 
 def block_product(props: np.ndarray) -> np.ndarray:
@@ -95,12 +119,8 @@ def block_boundaries(local_props: np.ndarray, initial: np.ndarray, target: np.nd
     Pg = block_product(local_props)
     if dist is None or world == 1:
         blocks = [Pg]
-    else:
-        import torch
-        t = torch.from_numpy(np.ascontiguousarray(Pg))
-        bufs = [torch.empty_like(t) for _ in range(world)]
-        dist.all_gather(bufs, t)  # the per-iteration exchange: G block products
-        blocks = [b.numpy() for b in bufs]
+    else:  # the per-iteration exchange: G block products (complex128 as float64 pairs)
+        blocks = list(all_gather_blocks(dist, Pg[None], [1] * world))
     psi = np.asarray(initial, dtype=np.complex128)
     for g in range(rank):
         psi = blocks[g] @ psi

@@ -22,3 +22,17 @@ def test_reference_arm_json_line():
     assert j["impl"] == "reference" and j["value"] > 0 and j["unit"] == "steps/s"
     assert j["cpu_baseline"]["kind"] == "port" and j["cpu_baseline"]["cores"] >= 1
     assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_gpus_flag_spawns_ranks():
+    # `bench.py --gpus 2` outside torchrun launches the two ranks itself (gloo on this CPU box);
+    # the reference arm runs on rank 0 only and reports the job's GPU count
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--workload", "spin2", "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                         timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == 2 and j["impl"] == "reference"
+    assert j["config"]["parallelism"] == "replicas x2"

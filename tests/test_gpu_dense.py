@@ -63,6 +63,7 @@ def test_spin2_200_iterations(ctx):
 def test_batch_subset(ctx, disable, monkeypatch):
     # the Neumann/tensor-core path and (QOC_DISABLE=nm, read per launch) the Gauss-Jordan path
     monkeypatch.setenv("QOC_DISABLE", disable)
+    monkeypatch.setenv("QOC_ENABLE", "fuse" if disable == "" else "")
     w = problems.batch4096(batch=8, iterations=3)
     gs = I.run_ism_batch(w.problem, w.u0, w.config, w.solver, ctx)
     rs = O.ism_run(w.problem, w.u0, w.config, w.solver, O.REFERENCE)

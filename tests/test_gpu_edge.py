@@ -66,3 +66,30 @@ def test_batch_members_stop_independently(ctx):
     for g, r in zip(gs, rs):
         assert np.max(np.abs(g.control - r.control)) / np.max(np.abs(r.control)) < 1e-11
         assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-11
+
+
+@pytest.mark.parametrize("kind", ["batch", "rotor", "bitflip", "strang"])
+def test_run_to_run_bitwise_determinism(ctx, kind):
+    # fixed-order reductions everywhere (no atomics on the data path): two runs of the same
+    # problem give bit-identical controls and records (acceptance_main.cpp:143-157 asks the same
+    # of the reference across worker counts)
+    from paper_1603_01237_b200 import problems
+    if kind == "batch":
+        w = problems.batch4096(batch=16, iterations=9)
+        w.solver.step_size = w.rho_fast
+    elif kind == "rotor":
+        w = problems.rotor21(subintervals=32, iterations=9, rho=100.0)
+    elif kind == "bitflip":
+        w = problems.ising10(nspins=7, steps=64, T=0.5, iterations=4, subintervals=8, rho=2.0)
+    else:
+        p, u = O.strang_fixture(3300, steps=24)
+        cfg = I.IsmConfig(subintervals=4, max_outer=9, eta=0.0, variant="split", log_exact_objective=True)
+        w = type("W", (), {"problem": p, "u0": u, "config": cfg, "solver": I.SolverSpec(step_size=0.3)})
+    a = I.run_ism_batch(w.problem, w.u0, w.config, w.solver, ctx)
+    b = I.run_ism_batch(w.problem, w.u0, w.config, w.solver, ctx)
+    for x, y in zip(a, b):
+        assert np.array_equal(x.control, y.control)
+        assert np.array_equal(x.record.objectives(), y.record.objectives(), equal_nan=True)
+        for s, t in zip(x.record.iterations, y.record.iterations):
+            assert np.array_equal(np.asarray(s.task_values), np.asarray(t.task_values), equal_nan=True)
+            assert (s.error == t.error) or (s.error is None and t.error is None)
