@@ -1,0 +1,126 @@
+// dropin_check.cpp -- the drop-in exercised end to end, in one process: the reference's own
+// problem builders and run_ism (compiled from /root/reference by oracle/Makefile `ref`) against
+// run_ism_gpu (ism_gpu.cpp -> libqoc_b200.so) on the same inputs.  Prints one JSON line per case
+// and exits non-zero on any mismatch.  Built here (integration/Makefile); run on the GPU box by
+// tests/test_gpu_dropin.py.
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <stdexcept>
+#include <string>
+
+#include "ism_gpu.hpp"
+#include "qoc/models.hpp"
+
+using namespace qoc;
+
+static bool compare(const char* name, const IsmRun& ref, const IsmRun& gpu, double ctl_tol, double obj_tol) {
+  const RMat& a = ref.control.samples();
+  const RMat& b = gpu.control.samples();
+  double du = 0.0, scale = 1e-300, dobj = 0.0, dex = 0.0;
+  for (Eigen::Index i = 0; i < a.size(); ++i) {
+    du = std::max(du, std::abs(a.data()[i] - b.data()[i]));
+    scale = std::max(scale, std::abs(a.data()[i]));
+  }
+  const size_t n = std::min(ref.record.iterations.size(), gpu.record.iterations.size());
+  for (size_t k = 0; k < n; ++k) {
+    const auto& x = ref.record.iterations[k];
+    const auto& y = gpu.record.iterations[k];
+    // absolute for O(1) payoffs, relative once the penalty term dominates
+    if (std::isfinite(x.objective))
+      dobj = std::max(dobj, std::abs(x.objective - y.objective) / std::max(1.0, std::abs(x.objective)));
+    if (x.exact_objective && y.exact_objective)
+      dex = std::max(dex, std::abs(*x.exact_objective - *y.exact_objective) / std::max(1.0, std::abs(*x.exact_objective)));
+  }
+  const bool same_len = ref.record.iterations.size() == gpu.record.iterations.size();
+  const bool meta = ref.record.solver == gpu.record.solver && ref.record.variant == gpu.record.variant &&
+                    ref.record.plan == gpu.record.plan && ref.record.subintervals == gpu.record.subintervals;
+  const bool ok = same_len && meta && du / scale <= ctl_tol && dobj <= obj_tol && dex <= obj_tol;
+  std::printf("{\"case\": \"%s\", \"iterations\": %zu, \"control_rel\": %.3e, \"objective_abs\": %.3e, "
+              "\"exact_abs\": %.3e, \"record_metadata_equal\": %s, \"ok\": %s}\n",
+              name, ref.record.iterations.size(), du / scale, dobj, dex, meta ? "true" : "false", ok ? "true" : "false");
+  return ok;
+}
+
+template <class F>
+static bool throws_logic(const char* name, F&& f) {
+  bool ok = false;
+  std::string what;
+  try {
+    f();
+  } catch (const std::logic_error& e) {
+    ok = dynamic_cast<const std::invalid_argument*>(&e) == nullptr;
+    what = e.what();
+  } catch (const std::exception& e) {
+    what = e.what();
+  }
+  std::printf("{\"case\": \"%s\", \"throws\": \"std::logic_error\", \"what\": \"%s\", \"ok\": %s}\n", name,
+              what.c_str(), ok ? "true" : "false");
+  return ok;
+}
+
+int main() {
+  bool all = true;
+  {  // BASELINE config 1 physics from the reference's spin operators (sigma/2): two spins
+    ControlProblem p;
+    const CMat h0 = 2.0 * std::acos(-1.0) * (spin_operator(2, 0, 'z') * spin_operator(2, 1, 'z'));
+    const CMat hc = spin_operator(2, 0, 'x') + spin_operator(2, 1, 'x');
+    p.model = std::make_shared<DenseModel>(PropagatorKind::cn_dense, h0, std::vector<CMat>{hc});
+    p.grid = TimeGrid::over(0.0, 10.0, 1000);
+    p.initial = CMat::Zero(4, 1);
+    p.initial(0, 0) = 1.0;
+    p.target = CMat::Zero(4, 1);
+    p.target(3, 0) = 1.0;
+    p.penalty = PenaltySchedule::constant(0.0, 1000);
+    const ControlField u0 = random_control(p.grid, 1, 7u, 0.3);
+    IsmConfig cfg;
+    cfg.subintervals = 8;
+    cfg.max_outer = 200;
+    cfg.eta = 0.0;
+    SolverSpec sv;
+    sv.step_size = 10.0;
+    all &= compare("spin2_config1_200it", run_ism(p, u0, cfg, sv), run_ism_gpu(p, u0, cfg, sv), 1e-9, 1e-10);
+    cfg.plan = IsmConfig::BoundaryPlan::direct;
+    cfg.max_outer = 20;
+    all &= compare("spin2_direct_plan", run_ism(p, u0, cfg, sv), run_ism_gpu(p, u0, cfg, sv), 1e-9, 1e-10);
+    SolverSpec mono = sv;
+    mono.kind = SolverSpec::Kind::monotonic;
+    all &= throws_logic("monotonic_solver_rejected", [&] { run_ism_gpu(p, u0, cfg, mono); });
+  }
+  {  // the reference's HCN-style rotor preset: dense, quadratic polarizability, t-dependent penalty
+    ControlProblem p = rotor_problem(20, 1.0, 1.0, 0.5, 0.3, 5.0, 1024, 100.0, 1e-3);
+    const ControlField u0 = random_control(p.grid, 1, 11u, 0.5);
+    IsmConfig cfg;
+    cfg.subintervals = 8;
+    cfg.max_outer = 20;
+    cfg.eta = 0.0;
+    SolverSpec sv;
+    sv.step_size = 0.5;
+    all &= compare("rotor_preset_quadratic", run_ism(p, u0, cfg, sv), run_ism_gpu(p, u0, cfg, sv), 1e-9, 1e-10);
+  }
+  {  // the reference's condensate preset (KAT-8 configuration): split variant, exact payoff logged
+    ControlProblem p = condensate_problem(50, -10.0, 10.0, 6.0, 1.0, 8.0, 512);
+    const ControlField u0 = ramp_control(p.grid, 1.0, 0.0);
+    IsmConfig cfg;
+    cfg.subintervals = 4;
+    cfg.max_outer = 10;
+    cfg.eta = 0.0;
+    cfg.variant = IsmConfig::Variant::split;
+    cfg.log_exact_objective = true;
+    SolverSpec sv;
+    sv.step_size = 0.1;
+    all &= compare("condensate_preset_kat8", run_ism(p, u0, cfg, sv), run_ism_gpu(p, u0, cfg, sv), 1e-9, 1e-10);
+    sv.gradient.naive_nonlinear_adjoint = true;
+    all &= compare("condensate_naive_adjoint", run_ism(p, u0, cfg, sv), run_ism_gpu(p, u0, cfg, sv), 1e-9, 1e-10);
+  }
+  {  // the density-matrix spin chain (cn_conjugation) is not on the device path
+    ControlProblem p = spin_chain_problem(3, {{1, 2}, {2, 3}}, 1.0, 1.0, 64, 0.0);
+    const ControlField u0 = random_control(p.grid, p.model->channels(), 3u, 0.2);
+    IsmConfig cfg;
+    cfg.subintervals = 2;
+    cfg.max_outer = 1;
+    all &= throws_logic("density_matrix_kind_rejected", [&] { run_ism_gpu(p, u0, cfg, SolverSpec{}); });
+  }
+  std::printf("{\"all_ok\": %s}\n", all ? "true" : "false");
+  return all ? 0 : 1;
+}

@@ -216,3 +216,37 @@ class Rng:
 
     def hermitian(self, n, scale=1.0):
         return self._draw(2, n, scale, n * n).reshape(n, n).T.copy()
+
+
+# ---- the reference itself (oracle/_ref/libqocref.so: /root/reference's run_ism compiled
+# against the Eigen-subset shim by `make -C oracle ref`; absent on the GPU box) ------------------
+REF_LIBPATH = ROOT / "oracle" / "_ref" / "libqocref.so"
+_ref = None
+
+
+def ref_available() -> bool:
+    if not REF_LIBPATH.exists() and Path("/root/reference/proj/core/src/ism.cpp").exists():
+        subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "ref"], check=True)
+    return REF_LIBPATH.exists()
+
+
+def ref_ism_run(p: I.ControlProblem, u0, cfg: I.IsmConfig, solver: I.SolverSpec) -> list[I.IsmRun]:
+    """qoc::run_ism of the reference (ism.cpp:211-612), one problem at a time."""
+    global _ref
+    if _ref is None:
+        _ref = C.CDLL(str(REF_LIBPATH))
+        _ref.ref_ism_run.restype = C.c_int32
+    packed = I.pack_problem(p)
+    B, Cn, K = p.batch, p.model.channels(), p.grid.steps
+    u_in = I.controls_to_abi(u0, B, Cn, K)
+    u_out = np.empty_like(u_in)
+    c, keep = I.pack_config(cfg)
+    s = I.pack_solver(solver)
+    cap, recs, tvals, status = I.run_buffers(p, cfg)
+    err = _err()
+    code = _ref.ref_ism_run(packed.ref, C.byref(c), C.byref(s), abi.dptr(u_in), abi.dptr(u_out),
+                            recs.ctypes.data_as(C.c_void_p), C.c_int32(cap), abi.dptr(tvals), status, err,
+                            C.c_size_t(512))
+    _check(code, err)
+    u = I.controls_from_abi(u_out, B, Cn, K)
+    return [I.IsmRun(u[b], r) for b, r in enumerate(I.unpack_all(recs, tvals, status, cfg, solver))]
