@@ -113,14 +113,36 @@ class SolverSpec:
 
 
 @dataclass
+class TaskStat:
+    """runtime.hpp:38-42.  On the device every task of an iteration runs concurrently inside
+    the same kernels: compute_seconds is the device time of the iteration's task kernels (an
+    upper bound on each task), nothing is serialised (serialize_seconds = bytes_sent = 0)."""
+    compute_seconds: float = 0.0
+    serialize_seconds: float = 0.0
+    bytes_sent: int = 0
+
+
+@dataclass
 class IterationStat:
-    """runtime.hpp:44-63."""
+    """runtime.hpp:44-63.  critical_path_seconds / wall_seconds are the device time of the
+    iteration (CUDA events bracketing its launch sequence); events carry the reference's abort
+    text at the iteration that stopped the run (ism.cpp:387,529-530,558)."""
     iteration: int
     objective: float
     exact_objective: Optional[float] = None
     error: Optional[float] = None
     task_values: list = field(default_factory=list)
     device_seconds: float = 0.0
+    tasks: list = field(default_factory=list)
+    events: list = field(default_factory=list)
+
+    @property
+    def critical_path_seconds(self) -> float:
+        return self.device_seconds
+
+    @property
+    def wall_seconds(self) -> float:
+        return self.device_seconds
 
 
 @dataclass
@@ -137,6 +159,12 @@ class RunRecord:
 
     def objectives(self) -> np.ndarray:
         return np.array([it.objective for it in self.iterations])
+
+    def total_wall_seconds(self) -> float:  # runtime.cpp:104-108
+        return float(sum(it.wall_seconds for it in self.iterations))
+
+    def total_critical_path_seconds(self) -> float:  # runtime.cpp:110-114
+        return float(sum(it.critical_path_seconds for it in self.iterations))
 
 
 @dataclass
@@ -272,6 +300,8 @@ def unpack_all(recs: np.ndarray, tvals: np.ndarray, status, cfg: IsmConfig, solv
                                         exact_objective=ex[k] if hx[k] else None,
                                         error=er[k] if he[k] else None, task_values=tvb[k],
                                         device_seconds=sec[k]) for k in range(n)]
+        if rec.aborted and rec.iterations:  # the stopping iteration carries the reason
+            rec.iterations[-1].events.append(rec.abort_reason)
         out.append(rec)
     return out
 

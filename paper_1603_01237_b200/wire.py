@@ -19,6 +19,7 @@ import io
 import json
 import math
 import struct
+from dataclasses import dataclass
 from pathlib import Path
 
 import numpy as np
@@ -130,13 +131,14 @@ def iteration_json(it) -> dict:
         j["exact_objective"] = it.exact_objective
     if it.error is not None:
         j["error"] = it.error
-    j["task_values"] = list(it.task_values)
-    j["tasks"] = []
+    j["task_values"] = [float(v) for v in it.task_values]
+    j["tasks"] = [{"compute_seconds": t.compute_seconds, "serialize_seconds": t.serialize_seconds,
+                   "bytes_sent": t.bytes_sent} for t in getattr(it, "tasks", [])]
     j["coordinator_seconds"] = 0.0
     j["critical_path_seconds"] = it.device_seconds
     j["instrumentation_seconds"] = 0.0
     j["wall_seconds"] = it.device_seconds
-    j["events"] = []
+    j["events"] = list(getattr(it, "events", []))
     return j
 
 
@@ -175,3 +177,95 @@ def write_run_artifacts(directory, problem: ControlProblem, run: IsmRun, config:
     if secs:
         prof["bootstrap_seconds"] = secs[0]
     (d / "profiling.json").write_text(json.dumps(prof, indent=2) + "\n")
+
+
+# ---- speedup / efficiency reporting (runtime.cpp:117-174, tools/main.cpp:304-375) ------------
+@dataclass
+class EfficiencyRow:
+    """runtime.hpp:83-89."""
+    subintervals: int
+    t_seconds: float = 0.0
+    speedup: float = 0.0
+    efficiency_percent: float = 0.0
+    reached: bool = False
+
+
+def _critical_path(it) -> float:
+    v = getattr(it, "critical_path_seconds", None)
+    return it.device_seconds if v is None else v
+
+
+def time_to_target(record, limit_value: float, eps: float):
+    """time_to_target (runtime.cpp:117-124): earliest cumulative critical-path time at which the
+    recorded objective came within eps of limit_value; None if never."""
+    cumulative = 0.0
+    for it in record.iterations:
+        cumulative += _critical_path(it)
+        if limit_value - it.objective < eps:
+            return cumulative
+    return None
+
+
+def efficiency_table(runs, limit_value: float, eps: float) -> list:
+    """efficiency_table (runtime.cpp:126-153): runs = [(N, RunRecord)], speedups relative to
+    the N = 1 entry, which must be present and reach the target."""
+    base = None
+    for n, rec in runs:
+        if n == 1:
+            base = time_to_target(rec, limit_value, eps)
+            break
+    if base is None:
+        raise ValueError("efficiency table needs an N=1 run that reaches the target")
+    rows = []
+    for n, rec in runs:
+        row = EfficiencyRow(subintervals=n)
+        t = time_to_target(rec, limit_value, eps)
+        row.reached = t is not None
+        if t is not None:
+            row.t_seconds = t
+            row.speedup = base / t
+            row.efficiency_percent = 100.0 * row.speedup / n
+        rows.append(row)
+    return rows
+
+
+def format_percent(value: float) -> str:
+    """format_percent (runtime.cpp:155-159): printf "%.1f%%"."""
+    return "%.1f%%" % value
+
+
+def efficiency_csv(rows) -> str:
+    """efficiency_csv (runtime.cpp:161-174)."""
+    out = "N,t_seconds,speedup,efficiency\n"
+    for r in rows:
+        if r.reached:
+            out += "%d,%.6f,%.6f,%s\n" % (r.subintervals, r.t_seconds, r.speedup, format_percent(r.efficiency_percent))
+        else:
+            out += "%d,,,unreached\n" % r.subintervals
+    return out
+
+
+def bench_efficiency_csv(runs, eps_list) -> str:
+    """The `qoc bench` efficiency.csv (tools/main.cpp:339-372): limit = best finite N = 1
+    objective, one block of rows per eps ("eps,N,t_seconds,speedup,efficiency")."""
+    limit = -math.inf
+    for n, rec in runs:
+        if n == 1:
+            for it in rec.iterations:
+                if math.isfinite(it.objective):
+                    limit = max(limit, it.objective)
+    if not math.isfinite(limit):
+        raise ValueError("bench needs an N=1 run with a finite objective")
+    csv = "eps,N,t_seconds,speedup,efficiency\n"
+    for eps in eps_list:
+        try:
+            rows = efficiency_table(runs, limit, eps)
+        except ValueError:
+            continue
+        for r in rows:
+            if r.reached:
+                csv += "%g,%d,%.6e,%.3f,%s\n" % (eps, r.subintervals, r.t_seconds, r.speedup,
+                                                 format_percent(r.efficiency_percent))
+            else:
+                csv += "%g,%d,,,unreached\n" % (eps, r.subintervals)
+    return csv

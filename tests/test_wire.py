@@ -57,3 +57,47 @@ def test_run_artifacts(tmp_path):
     assert s["format_version"] == 1 and s["result"]["iterations"] == 3 and s["problem"]["steps"] == p.grid.steps
     assert np.allclose(W.read_control_csv((tmp_path / "control.csv").read_text(), p.grid), run.control,
                        rtol=0, atol=0)
+
+
+def test_kat7_efficiency_formulas_and_csv():
+    # acceptance_main.cpp:541-575 (criterion 10) and runtime_test.cpp:143-170, exact strings
+    from paper_1603_01237_b200 import ism as I
+    from paper_1603_01237_b200 import wire as W
+
+    def record_with(objectives, times):
+        r = I.RunRecord()
+        r.iterations = [I.IterationStat(iteration=k, objective=o, device_seconds=t)
+                        for k, (o, t) in enumerate(zip(objectives, times))]
+        return r
+
+    serial = record_with([0.0, 0.2, 0.5, 1.0], [249.25] * 4)
+    eight = record_with([0.4, 1.0], [62.5, 62.5])
+    stuck = record_with([0.1, 0.2], [10.0, 10.0])
+    rows = W.efficiency_table([(1, serial), (8, eight), (16, stuck)], 1.0, 0.25)
+    assert len(rows) == 3
+    assert rows[0].reached and rows[0].t_seconds == 997.0 and rows[0].speedup == 1.0
+    assert rows[0].efficiency_percent == 100.0
+    assert rows[1].reached and rows[1].t_seconds == 125.0 and rows[1].speedup == 997.0 / 125.0
+    assert rows[1].efficiency_percent == 100.0 * (997.0 / 125.0) / 8.0
+    assert not rows[2].reached
+    assert W.format_percent(rows[1].efficiency_percent) == "99.7%"
+    assert W.format_percent(rows[0].efficiency_percent) == "100.0%"
+    assert W.efficiency_csv(rows) == ("N,t_seconds,speedup,efficiency\n"
+                                      "1,997.000000,1.000000,100.0%\n"
+                                      "8,125.000000,7.976000,99.7%\n"
+                                      "16,,,unreached\n")
+    a = W.EfficiencyRow(1, 8.0, 1.0, 100.0, True)
+    b = W.EfficiencyRow(2, 2.5, 3.2, 160.0, True)
+    c = W.EfficiencyRow(4)
+    assert W.efficiency_csv([a, b, c]) == ("N,t_seconds,speedup,efficiency\n"
+                                           "1,8.000000,1.000000,100.0%\n"
+                                           "2,2.500000,3.200000,160.0%\n"
+                                           "4,,,unreached\n")
+    assert W.format_percent(12.34) == "12.3%" and W.format_percent(99.96) == "100.0%"
+    assert W.format_percent(0.0) == "0.0%"
+    try:
+        W.efficiency_table([(2, eight)], 1.0, 0.25)
+    except ValueError:
+        pass
+    else:
+        raise AssertionError("an N=1 run is required")
