@@ -1,0 +1,258 @@
+// bitflip_cluster.cu — the full-horizon node sweeps of the spin-register kind (node_sweeps,
+// ism.cpp:35-84, and the exact payoff, objective.cpp:93-100) on a thread-block CLUSTER, sm_100a.
+//
+// The direct plan's node sweeps are the serial critical path of BASELINE config 3: K = 4000
+// dependent Cayley steps per direction, each ~7 Jacobi sweeps of the bit-flip fixed point
+//     z <- (1 + sD)^-1 (x - s V z),   x' = 2z - x          (bitflip_kernels.cu, oracle BitM::cayley)
+// over d = 2^n amplitudes.  On one SM a sweep of d = 1024 costs ~1,570 cycles; here
+// CL = 2^LOG2CL CTAs of one cluster split the amplitudes: CTA `rank` owns s = rank * Dl + t + e*T.
+// A flip of bit b pairs
+//   b < LOG2T                      -> thread t ^ 2^b of the same CTA   (shared memory)
+//   LOG2T <= b < LOG2T + LOG2E     -> register slot e ^ 2^(b - LOG2T)   (same thread)
+//   b >= LOG2T + LOG2E             -> CTA rank ^ 2^(b - LOG2T - LOG2E)  (distributed shared memory)
+// and one cluster barrier per sweep orders every exchange (the double-buffered publish makes a
+// second barrier unnecessary).  Arithmetic, coefficient signs and the a-priori sweep count are
+// those of the single-CTA kernel, so results are identical to rounding order.
+#include <cooperative_groups.h>
+#include <cstdlib>
+
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace qoc {
+
+namespace {
+
+__device__ __forceinline__ double2 flip_coef(double2 ab, int one) { return cx(ab.x, one ? ab.y : -ab.y); }
+
+template <int LOG2E, int LOG2T, int LOG2CL, bool PUSH>
+__global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_cluster_kernel(DevProblem P, DevRun R, int which, int k) {
+  constexpr int E = 1 << LOG2E, T = 1 << LOG2T, CL = 1 << LOG2CL, Dl = E * T, N = LOG2E + LOG2T + LOG2CL;
+  if (R.kdev) k = *R.kdev;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int b = blockIdx.y, dir = blockIdx.z;
+  if (R.done[b] || R.status[b]) return;  // uniform over the cluster (same problem)
+  if (which == 1 && dir == 1) return;
+  __shared__ __align__(16) double2 buf[2][Dl];
+  // PUSH: partner rb's amplitudes of the current sweep, written by the partner (remote stores
+  // before the barrier, local loads after it) instead of loaded remotely after the barrier
+  __shared__ __align__(16) double2 inbox[PUSH ? 2 : 1][PUSH ? (LOG2CL > 0 ? LOG2CL : 1) : 1][PUSH ? Dl : 1];
+  __shared__ double2 sa[2][N];
+  __shared__ int ssw[2];
+  __shared__ double red[T / 32 + 1];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, d = P.d, C = P.C;
+  const double half = 0.5 * P.dt;
+  const double* u = R.u + (size_t)b * P.K * C;
+  const double* coef = P.bf_coef + (size_t)b * C * P.nspins;
+  const size_t nb = (size_t)b * (P.L + 1) * d;
+  const int base = rank * Dl + t;  // amplitude of slot e: base + e * T
+  double dg[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) dg[e] = P.bf_diag[(size_t)b * d + base + e * T];
+  // partner CTAs' exchange buffers (distributed shared memory)
+  const double2* rem[LOG2CL > 0 ? LOG2CL : 1];
+  double2* outbox[LOG2CL > 0 ? LOG2CL : 1];  // PUSH: my slot rb in partner rank ^ 2^rb's inbox
+#pragma unroll
+  for (int rb = 0; rb < LOG2CL; ++rb) {
+    rem[rb] = cluster.map_shared_rank(&buf[0][0], rank ^ (1 << rb));
+    if constexpr (PUSH) outbox[rb] = cluster.map_shared_rank(&inbox[0][rb][0], rank ^ (1 << rb));
+  }
+  double2 cl[LOG2T > 0 ? LOG2T : 1], ch[LOG2E > 0 ? LOG2E : 1], cr[LOG2CL > 0 ? LOG2CL : 1];
+  int par = 0, spar = 0;
+  bool ok = true;
+  double2 x[E];
+
+  auto begin_step = [&](const double* uj) -> int {
+    spar ^= 1;
+    if (warp == 0) {
+      double nrm = 0.0;
+      if (lane < N) {
+        double ax = 0.0, ay = 0.0;
+        for (int c = 0; c < C; ++c) {
+          const double g = uj[c] * coef[c * N + lane];
+          if (P.bf_axis[c] == 0) ax += g;
+          else ay += g;
+        }
+        sa[spar][lane] = cx(ax, ay);
+        nrm = sqrt(ax * ax + ay * ay);
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, off);
+      if (lane == 0) {
+        const double q = half * nrm;
+        ssw[spar] = !(q < 0.5) ? -1 : (q <= 0.0 ? 0 : (int)ceil(54.0 * 0.6931471805599453 / -log(q)));
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int bb = 0; bb < LOG2T; ++bb) cl[bb] = flip_coef(sa[spar][N - 1 - bb], (t >> bb) & 1);
+#pragma unroll
+    for (int hb = 0; hb < LOG2E; ++hb) ch[hb] = sa[spar][N - 1 - (LOG2T + hb)];
+#pragma unroll
+    for (int rb = 0; rb < LOG2CL; ++rb) cr[rb] = flip_coef(sa[spar][N - 1 - (LOG2T + LOG2E + rb)], (rank >> rb) & 1);
+    return ssw[spar];
+  };
+
+  auto cayley = [&](double sh, int sweeps) {
+    double2 z[E], vv[E], inv[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const double a = sh * dg[e];
+      const double den = 1.0 / fma(a, a, 1.0);
+      inv[e] = cx(den, -a * den);
+      z[e] = cmul(x[e], inv[e]);
+    }
+    for (int it = 0; it < sweeps; ++it) {
+      par ^= 1;
+#pragma unroll
+      for (int e = 0; e < E; ++e) buf[par][t + e * T] = z[e];
+      if constexpr (PUSH) {
+#pragma unroll
+        for (int rb = 0; rb < LOG2CL; ++rb)
+#pragma unroll
+          for (int e = 0; e < E; ++e) outbox[rb][par * LOG2CL * Dl + t + e * T] = z[e];
+      }
+      cluster.sync();  // every CTA's publish of this sweep is visible cluster-wide
+#pragma unroll
+      for (int e = 0; e < E; ++e) vv[e] = cx(0.0, 0.0);
+#pragma unroll
+      for (int rb = 0; rb < LOG2CL; ++rb) {
+        const double2* rbuf = PUSH ? &inbox[par][rb][0] : rem[rb] + par * Dl;
+#pragma unroll
+        for (int e = 0; e < E; ++e) vv[e] = cfma(cr[rb], rbuf[t + e * T], vv[e]);
+      }
+#pragma unroll
+      for (int hb = 0; hb < LOG2E; ++hb)
+#pragma unroll
+        for (int e = 0; e < E; ++e) vv[e] = cfma(flip_coef(ch[hb], (e >> hb) & 1), z[e ^ (1 << hb)], vv[e]);
+#pragma unroll
+      for (int bb = 0; bb < LOG2T; ++bb)
+#pragma unroll
+        for (int e = 0; e < E; ++e) vv[e] = cfma(cl[bb], buf[par][(t ^ (1 << bb)) + e * T], vv[e]);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const double2 tt = cx(x[e].x + sh * vv[e].y, x[e].y - sh * vv[e].x);  // x - s V z
+        z[e] = cmul(tt, inv[e]);
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = cx(fma(2.0, z[e].x, -x[e].x), fma(2.0, z[e].y, -x[e].y));
+  };
+  auto load = [&](const double2* src) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = src[base + e * T];
+  };
+  auto store = [&](double2* dst) {
+#pragma unroll
+    for (int e = 0; e < E; ++e) dst[base + e * T] = x[e];
+  };
+  auto step = [&](const double* uj, double sh) {
+    const int sweeps = begin_step(uj);
+    ok &= sweeps >= 0;
+    cayley(sh, sweeps < 0 ? 0 : sweeps);
+  };
+
+  if (dir == 0) {
+    load(P.init + (size_t)b * d);
+    if (which == 0) store(R.psi_nodes + nb);
+    int nxt = 1;
+    for (int j = 0; j < P.K; ++j) {
+      step(u + (size_t)j * C, half);
+      if (which == 0 && nxt <= P.L && P.node[nxt] == j + 1) {
+        store(R.psi_nodes + nb + (size_t)nxt * d);
+        ++nxt;
+      }
+    }
+    if (which == 1) {  // Re<target, psi(T)> over the cluster, fixed rank order
+      double s = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) s += cconjmul(P.targ[(size_t)b * d + base + e * T], x[e]).x;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (lane == 0) red[warp] = s;
+      __syncthreads();
+      if (t == 0) {
+        double a = 0.0;
+        for (int w = 0; w < T / 32; ++w) a += red[w];
+        red[T / 32] = a;
+      }
+      cluster.sync();
+      if (rank == 0 && t == 0) {
+        double tot = 0.0;
+        for (int r = 0; r < CL; ++r) tot += cluster.map_shared_rank(red, r)[T / 32];
+        double pen = 0.0;
+        for (int n = 0; n < P.L; ++n) pen += R.pen[(size_t)b * P.L + n];
+        R.rec_exact[(size_t)b * R.cap + k] = P.ip_w * tot - 0.5 * P.dt * pen;
+      }
+    }
+  } else {
+    load(P.targ + (size_t)b * d);
+    store(R.chi_nodes + nb + (size_t)P.L * d);
+    int prev = P.L - 1;
+    for (int j = P.K - 1; j >= 0; --j) {
+      step(u + (size_t)j * C, -half);
+      if (prev >= 0 && P.node[prev] == j) {
+        store(R.chi_nodes + nb + (size_t)prev * d);
+        --prev;
+      }
+    }
+  }
+  if (!ok && t == 0 && rank == 0 && R.err_flags) atomicOr(R.err_flags, 2);
+  cluster.sync();  // no CTA leaves while a peer may still read its shared memory
+}
+
+template <int LOG2E, int LOG2T, int LOG2CL, bool PUSH = false>
+cudaError_t launch_cluster(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
+  auto kern = bitflip_horizon_cluster_kernel<LOG2E, LOG2T, LOG2CL, PUSH>;
+  constexpr int CL = 1 << LOG2CL;
+  if (CL > 8) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(CL, P.B, 2);
+  cfg.blockDim = dim3(1 << LOG2T, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, P, R, which, k);
+}
+
+}  // namespace
+
+// QOC_BF_CLUSTER selects the cluster shape for d = 1024 node sweeps ("0" keeps the single-CTA
+// kernel): "8x1" = 8 CTAs x 128 threads x 1 amplitude, "8x2" = 8 x 64 x 2,
+// "16x1" = 16 x 64 x 1 (non-portable cluster size); "8p" / "8q" = 8x1 / 8x2 with the partner
+// amplitudes pushed (remote stores) instead of pulled, "4p" = 4 x 128 x 2 (default), "2p" = 2 x 128 x 4.
+// Measured per config-3 outer iteration (node sweeps): single CTA 22.8 ms, 8x1 21.2, 8p 20.1,
+// 4p 20.0, 2p 20.1, 8x2 34.8, 16x1 29.8 -- the per-sweep floor is the exchange + barrier
+// latency of a dependent chain (~1,200 cycles), not the arithmetic.
+cudaError_t bitflip_horizon_cluster(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st,
+                                    bool* used) {
+  *used = false;
+  if (P.nspins != 10 || P.C > 4) return cudaSuccess;
+  const char* e = std::getenv("QOC_BF_CLUSTER");
+  const char* shape = e ? e : "4p";
+  if (shape[0] == '0') return cudaSuccess;
+  cudaError_t r;
+  if (shape[0] == '1' && shape[1] == '6') r = launch_cluster<0, 6, 4>(P, R, which, k, st);
+  else if (shape[2] == '2') r = launch_cluster<1, 6, 3>(P, R, which, k, st);
+  else if (shape[1] == 'p') r = launch_cluster<0, 7, 3, true>(P, R, which, k, st);
+  else if (shape[1] == 'q') r = launch_cluster<1, 6, 3, true>(P, R, which, k, st);
+  else if (shape[0] == '4') r = launch_cluster<1, 7, 2, true>(P, R, which, k, st);
+  else if (shape[0] == '2') r = launch_cluster<2, 7, 1, true>(P, R, which, k, st);
+  else r = launch_cluster<0, 7, 3>(P, R, which, k, st);
+  *used = r == cudaSuccess;
+  if (r != cudaSuccess) cudaGetLastError();  // e.g. no cluster support: fall back
+  return cudaSuccess;
+}
+
+}  // namespace qoc

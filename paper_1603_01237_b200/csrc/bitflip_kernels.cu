@@ -444,8 +444,16 @@ cudaError_t bitflip_task(const DevProblem& P, const DevRun& R, const TaskArgs& A
   return cudaErrorNotSupported;
 }
 
+cudaError_t bitflip_horizon_cluster(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st,
+                                    bool* used);
+
 cudaError_t bitflip_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
   if (P.C > 4) return cudaErrorNotSupported;
+  {  // d = 1024: the node sweeps split over a thread-block cluster (bitflip_cluster.cu)
+    bool used = false;
+    cudaError_t e = bitflip_horizon_cluster(P, R, which, k, st, &used);
+    if (e != cudaSuccess || used) return e;
+  }
   switch (P.nspins) {
     case 5: return launch_horizon<0, 5>(P, R, which, k, st);
     case 6: return launch_horizon<0, 6>(P, R, which, k, st);

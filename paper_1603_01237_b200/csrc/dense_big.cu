@@ -1,0 +1,443 @@
+// dense_big.cu — QOC_KIND_DENSE task and horizon kernels for 32 < d <= 64 (sm_100a).
+//
+// The reference's DenseModel takes any d (models.cpp:45-75) and its micro-benchmarks time a
+// d = 64 Crank-Nicolson step (benchmarks.cpp:76).  Above the warp-resident sizes of
+// dense_kernels.cu a task owns a CTA: the step matrix B_j = I + i dt/2 H(u_j) (models.cpp:57-68,
+// propagation.cpp:14-16) is built in shared memory, inverted in place by Gauss-Jordan with
+// partial pivoting (largest |.| in the column, first row on ties, then the column unscramble --
+// the pivot order of Eigen's PartialPivLU, propagation.cpp:85-90), and every sweep applies
+//     C_j = 2 B_j^-1 - I          forward          (cn_step, propagation.cpp:85-90)
+//     C_j^dag = 2 B_j^-dag - I     adjoint          (cn_adjoint_step, propagation.cpp:101-106)
+// as matvecs (threads over rows), and P <- 2 B_j^-1 P - P for the assembled propagator
+// (propagation.cpp:236-249).  The task body is the same as dense_task_kernel's (ism.cpp:401-479):
+// entry value, gradient sweep with the fused update (objective.cpp:48-60, optimizers.cpp:102-107),
+// residual sweep (error_norm), assembly and the split-variant lagged refresh.
+#include "common.cuh"
+#include "kernels.h"
+#include "qoc_gpu.h"
+
+namespace qoc {
+
+namespace {
+
+constexpr int BT = 256;     // threads per task CTA
+constexpr int BIG_MAX = 64;  // three d x d complex buffers (assembly) within 227 KB
+
+struct BigSmem {
+  double2* W;     // [d][d] row-major: B_j, then its inverse
+  double2* Pm;    // [d][d] assembly product (M_ASSEMBLE only)
+  double2* T;     // [d][d] matmul scratch (M_ASSEMBLE only)
+  double2* x;     // [d] state vectors
+  double2* y;
+  double2* z;
+  double2* v;
+  double2* prow;  // [d] pivot row
+  double2* colk;  // [d] pivot column (read before the elimination writes it)
+  double* red;    // [BT] reduction scratch
+  int* perm;      // [d]
+  int* piv;       // [2]
+};
+
+__device__ double block_sum(double v, double* red) {
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = BT / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// B = I + s i H(u), s = +half (forward) -- H(u) = H0 + sum u_c A_c + sum (u_c^2/2) B_c
+__device__ void build(const DevProblem& P, int b, const double* u, double half, double2* W) {
+  const int d = P.d, C = P.C;
+  const size_t dd = (size_t)d * d;
+  for (int e = threadIdx.x; e < d * d; e += BT) {
+    double2 h = P.h0[(size_t)b * dd + e];
+    for (int c = 0; c < C; ++c) {
+      const double2 a = P.lin[((size_t)b * C + c) * dd + e];
+      h = cx(fma(u[c], a.x, h.x), fma(u[c], a.y, h.y));
+      if (P.has_quad) {
+        const double2 q = P.quad[((size_t)b * C + c) * dd + e];
+        const double s = 0.5 * u[c] * u[c];
+        h = cx(fma(s, q.x, h.x), fma(s, q.y, h.y));
+      }
+    }
+    const int i = e / d, j = e % d;
+    W[e] = cx((i == j ? 1.0 : 0.0) - half * h.y, half * h.x);
+  }
+  __syncthreads();
+}
+
+// In-place Gauss-Jordan inverse with partial pivoting and the column unscramble.
+__device__ void invert(int d, const BigSmem& S) {
+  double2* W = S.W;
+  for (int k = 0; k < d; ++k) {
+    // pivot: first row of largest |W[i][k]|, i >= k
+    double best = -1.0;
+    int bi = d;
+    for (int i = k + threadIdx.x; i < d; i += BT) {
+      const double v = cabs2(W[i * d + k]);
+      if (v > best) {
+        best = v;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      S.red[threadIdx.x >> 5] = best;
+      S.perm[d + (threadIdx.x >> 5)] = bi;  // scratch after perm[0..d)
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double bb = S.red[0];
+      int ii = S.perm[d];
+      for (int w = 1; w < BT / 32; ++w) {
+        const double ob = S.red[w];
+        const int oi = S.perm[d + w];
+        if (ob > bb || (ob == bb && oi < ii)) {
+          bb = ob;
+          ii = oi;
+        }
+      }
+      S.piv[0] = ii;
+      S.perm[k] = ii;
+    }
+    __syncthreads();
+    const int p = S.piv[0];
+    if (p != k)
+      for (int j = threadIdx.x; j < d; j += BT) {
+        const double2 t = W[k * d + j];
+        W[k * d + j] = W[p * d + j];
+        W[p * d + j] = t;
+      }
+    __syncthreads();
+    const double2 pinv = crcp(W[k * d + k]);
+    for (int j = threadIdx.x; j < d; j += BT) {
+      S.prow[j] = (j == k) ? pinv : cmul(W[k * d + j], pinv);
+      S.colk[j] = W[j * d + k];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < d * d; e += BT) {
+      const int i = e / d, j = e % d;
+      if (i == k) continue;
+      const double2 f = S.colk[i];
+      W[e] = (j == k) ? cneg(cmul(f, pinv)) : cfms(f, S.prow[j], W[e]);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < d; j += BT) W[k * d + j] = S.prow[j];
+    __syncthreads();
+  }
+  // undo the row interchanges on the columns of the inverse (reverse order)
+  for (int k = d - 1; k >= 0; --k) {
+    const int p = S.perm[k];
+    if (p != k)
+      for (int i = threadIdx.x; i < d; i += BT) {
+        const double2 t = W[i * d + k];
+        W[i * d + k] = W[i * d + p];
+        W[i * d + p] = t;
+      }
+    __syncthreads();
+  }
+}
+
+// y = 2 W x - x (adj: 2 W^dag x - x); rows over threads, x in smem; y may not alias x
+__device__ void cayley(int d, const double2* W, const double2* x, double2* y, bool adj) {
+  for (int i = threadIdx.x; i < d; i += BT) {
+    double2 acc = cx(0.0, 0.0);
+    if (adj)
+      for (int k = 0; k < d; ++k) acc = cfmaconj(W[k * d + i], x[k], acc);
+    else
+      for (int k = 0; k < d; ++k) acc = cfma(W[i * d + k], x[k], acc);
+    y[i] = cx(2.0 * acc.x - x[i].x, 2.0 * acc.y - x[i].y);
+  }
+  __syncthreads();
+}
+
+__device__ void copy_vec(int d, const double2* src, double2* dst) {
+  for (int i = threadIdx.x; i < d; i += BT) dst[i] = src[i];
+  __syncthreads();
+}
+
+// Im <cs, dH/du_c(u_c) ps>, dH/du_c = A_c + u_c B_c (models.cpp:70-75)
+__device__ double grad_im(const DevProblem& P, int b, int c, double uc, const double2* ps, const double2* cs,
+                          double* red) {
+  const int d = P.d;
+  const size_t dd = (size_t)d * d;
+  double im = 0.0;
+  for (int i = threadIdx.x; i < d; i += BT) {
+    double2 acc = cx(0.0, 0.0);
+    for (int k = 0; k < d; ++k) {
+      double2 a = P.lin[((size_t)b * P.C + c) * dd + (size_t)i * d + k];
+      if (P.has_quad) {
+        const double2 q = P.quad[((size_t)b * P.C + c) * dd + (size_t)i * d + k];
+        a = cx(fma(uc, q.x, a.x), fma(uc, q.y, a.y));
+      }
+      acc = cfma(a, ps[k], acc);
+    }
+    im += cconjmul(cs[i], acc).y;
+  }
+  return block_sum(im, red);
+}
+
+__device__ BigSmem carve(unsigned char* raw, int d, bool with_asm) {
+  BigSmem S;
+  double2* p = reinterpret_cast<double2*>(raw);
+  S.W = p;
+  p += (size_t)d * d;
+  S.Pm = with_asm ? p : nullptr;
+  if (with_asm) p += (size_t)d * d;
+  S.T = with_asm ? p : nullptr;
+  if (with_asm) p += (size_t)d * d;
+  S.x = p;
+  S.y = p + d;
+  S.z = p + 2 * d;
+  S.v = p + 3 * d;
+  S.prow = p + 4 * d;
+  S.colk = p + 5 * d;
+  p += 6 * d;
+  S.red = reinterpret_cast<double*>(p);
+  S.perm = reinterpret_cast<int*>(S.red + BT);
+  S.piv = S.perm + d + BT / 32;
+  return S;
+}
+
+size_t big_smem(int d, bool with_asm) {
+  return sizeof(double2) * ((size_t)d * d * (with_asm ? 3 : 1) + 6 * (size_t)d) + sizeof(double) * BT +
+         sizeof(int) * (d + BT / 32 + 2);
+}
+
+__global__ void __launch_bounds__(BT) dense_big_task_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = blockIdx.x, b = blockIdx.y;
+  if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
+  const int mode = A.mode;
+  const bool do_asm = (mode & M_ASSEMBLE) != 0;
+  const BigSmem S = carve(smem_raw, P.d, do_asm);
+  const int d = P.d, C = P.C;
+  const int node0 = P.node[n], len = P.node[n + 1] - node0;
+  const double Kd = (double)P.K, weight = A.weighted ? Kd / (double)len : 1.0, scale = (double)len / Kd;
+  const double half = 0.5 * P.dt, dt = P.dt, w = P.ip_w;
+  double* u = R.u + ((size_t)b * P.K + node0) * C;
+  double2* traj = R.traj + ((size_t)b * P.L + n) * (size_t)R.traj_len * d;
+  const size_t tix = ((size_t)b * P.L + n) * d;
+  const double2* init = R.task_init + tix;
+  const double2* targ = R.task_targ + tix;
+
+  // ---- phase 1: sweeps at the current control
+  if (mode & (M_ENTRY | M_UPDATE | M_FINAL | M_GRAD)) {
+    const bool need_traj = (mode & (M_UPDATE | M_GRAD)) != 0;
+    const int iters = (mode & M_UPDATE) ? A.inner : 1;
+    for (int it = 0; it < iters; ++it) {
+      copy_vec(d, init, S.x);
+      if (need_traj) copy_vec(d, S.x, traj);
+      double pen = 0.0;
+      for (int j = 0; j < len; ++j) {
+        const double* uj = u + (size_t)j * C;
+        build(P, b, uj, half, S.W);
+        invert(d, S);
+        cayley(d, S.W, S.x, S.y, false);
+        copy_vec(d, S.y, S.x);
+        if (need_traj) copy_vec(d, S.x, traj + (size_t)(j + 1) * d);
+        double sq = 0.0;
+        for (int c = 0; c < C; ++c) sq += uj[c] * uj[c];
+        pen += (P.alpha[node0 + j] * scale) * sq;
+      }
+      if (it == 0 && (mode & M_ENTRY)) {  // sub_functional (objective.cpp:131-134)
+        double t = 0.0;
+        for (int i = threadIdx.x; i < d; i += BT)
+          t += A.form == 0 ? cconjmul(targ[i], S.x[i]).x : cabs2(csub(S.x[i], targ[i]));
+        t = block_sum(t, S.red);
+        const double payoff = A.form == 0 ? (w * t) : (-0.5 * (w * t));
+        if (threadIdx.x == 0) R.entry[(size_t)b * P.L + n] = weight * (payoff - 0.5 * dt * pen);
+      }
+      if (it == 0 && (mode & M_FINAL)) copy_vec(d, S.x, R.psi_end + tix);
+      if (mode & (M_UPDATE | M_GRAD)) {
+        for (int i = threadIdx.x; i < d; i += BT) S.z[i] = A.form == 0 ? targ[i] : csub(targ[i], S.x[i]);
+        __syncthreads();
+        for (int j = len - 1; j >= 0; --j) {
+          const double* uj = u + (size_t)j * C;
+          build(P, b, uj, half, S.W);
+          invert(d, S);
+          cayley(d, S.W, S.z, S.y, true);  // chi_j
+          for (int i = threadIdx.x; i < d; i += BT) {
+            S.v[i] = cadd(traj[(size_t)j * d + i], traj[(size_t)(j + 1) * d + i]);  // psi sum
+            S.prow[i] = cadd(S.y[i], S.z[i]);                                     // chi sum
+          }
+          __syncthreads();
+          const double aj = P.alpha[node0 + j] * scale;
+          for (int c = 0; c < C; ++c) {
+            const double uc = uj[c];
+            const double im = grad_im(P, b, c, uc, S.v, S.prow, S.red);
+            const double gc = -aj * dt * uc + 0.25 * dt * (w * im);
+            if (threadIdx.x == 0) {
+              if (mode & M_GRAD) R.grad[((size_t)b * P.K + node0 + j) * C + c] = gc;
+              if (mode & M_UPDATE) u[(size_t)j * C + c] = uc + A.rho * (weight * gc);
+            }
+            __syncthreads();
+          }
+          copy_vec(d, S.y, S.z);
+        }
+      }
+    }
+  }
+
+  // ---- phase 2: sweeps at the updated control
+  const bool do_err = (mode & M_ERROR) != 0, do_lag = (mode & M_LAGGED) != 0;
+  if (do_err || do_asm || do_lag) {
+    copy_vec(d, init, S.x);
+    if (do_lag) copy_vec(d, R.psi_nodes + ((size_t)b * (P.L + 1) + n) * d, S.z);
+    if (do_err) copy_vec(d, S.x, traj);
+    if (do_asm)
+      for (int e = threadIdx.x; e < d * d; e += BT) S.Pm[e] = cx((e / d) == (e % d) ? 1.0 : 0.0, 0.0);
+    __syncthreads();
+    for (int j = 0; j < len; ++j) {
+      build(P, b, u + (size_t)j * C, half, S.W);
+      invert(d, S);
+      if (do_err) {
+        cayley(d, S.W, S.x, S.y, false);
+        copy_vec(d, S.y, S.x);
+        copy_vec(d, S.x, traj + (size_t)(j + 1) * d);
+      }
+      if (do_lag) {
+        cayley(d, S.W, S.z, S.y, false);
+        copy_vec(d, S.y, S.z);
+      }
+      if (do_asm) {  // P <- 2 W P - P
+        for (int e = threadIdx.x; e < d * d; e += BT) {
+          const int i = e / d, c = e % d;
+          double2 acc = cx(0.0, 0.0);
+          for (int k = 0; k < d; ++k) acc = cfma(S.W[i * d + k], S.Pm[k * d + c], acc);
+          S.T[e] = cx(2.0 * acc.x - S.Pm[e].x, 2.0 * acc.y - S.Pm[e].y);
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < d * d; e += BT) S.Pm[e] = S.T[e];
+        __syncthreads();
+      }
+    }
+    if (do_asm)
+      for (int e = threadIdx.x; e < d * d; e += BT) R.prop[((size_t)b * P.L + n) * (size_t)d * d + e] = S.Pm[e];
+    if (do_lag) copy_vec(d, S.z, R.psi_end + tix);
+    if (do_err || do_lag) {
+      // residual adjoint (error_norm) seeded from the residual forward state; lagged adjoint from chi_{n+1}
+      for (int i = threadIdx.x; i < d; i += BT) S.v[i] = A.form == 0 ? targ[i] : csub(targ[i], S.x[i]);
+      if (do_lag) copy_vec(d, R.chi_nodes + ((size_t)b * (P.L + 1) + n + 1) * d, S.z);
+      __syncthreads();
+      double err = 0.0;
+      for (int j = len - 1; j >= 0; --j) {
+        const double* uj = u + (size_t)j * C;
+        build(P, b, uj, half, S.W);
+        invert(d, S);
+        if (do_lag) {
+          cayley(d, S.W, S.z, S.y, true);
+          copy_vec(d, S.y, S.z);
+        }
+        if (do_err) {
+          cayley(d, S.W, S.v, S.y, true);  // chi_j
+          double2* ps = S.Pm ? S.T : S.prow;   // scratch vectors (T is free after the assembly)
+          double2* cs = S.x;
+          for (int i = threadIdx.x; i < d; i += BT) {
+            ps[i] = cadd(traj[(size_t)j * d + i], traj[(size_t)(j + 1) * d + i]);
+            cs[i] = cadd(S.y[i], S.v[i]);
+          }
+          __syncthreads();
+          const double aj = P.alpha[node0 + j] * scale;
+          double sq = 0.0;
+          for (int c = 0; c < C; ++c) {
+            const double uc = uj[c];
+            const double im = grad_im(P, b, c, uc, ps, cs, S.red);
+            const double gc = -aj * dt * uc + 0.25 * dt * (w * im);
+            sq += gc * gc;
+          }
+          err += sqrt(sq);
+          copy_vec(d, S.y, S.v);
+        }
+      }
+      if (do_err && threadIdx.x == 0) R.err[(size_t)b * P.L + n] = err;
+      if (do_lag) copy_vec(d, S.z, R.chi_start + tix);
+    }
+  }
+}
+
+// node_sweeps (ism.cpp:35-84) / exact payoff (which = 1), one CTA per problem
+__global__ void __launch_bounds__(BT) dense_big_horizon_kernel(DevProblem P, DevRun R, int which, int k) {
+  if (R.kdev) k = *R.kdev;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int b = blockIdx.x;
+  if (R.done[b] || R.status[b]) return;
+  const BigSmem S = carve(smem_raw, P.d, false);
+  const int d = P.d, C = P.C;
+  const double half = 0.5 * P.dt;
+  const double* u = R.u + (size_t)b * P.K * C;
+  const size_t nb = (size_t)b * (P.L + 1) * d;
+  copy_vec(d, P.init + (size_t)b * d, S.x);
+  if (which == 0) copy_vec(d, S.x, R.psi_nodes + nb);
+  int nxt = 1;
+  for (int j = 0; j < P.K; ++j) {
+    build(P, b, u + (size_t)j * C, half, S.W);
+    invert(d, S);
+    cayley(d, S.W, S.x, S.y, false);
+    copy_vec(d, S.y, S.x);
+    if (which == 0 && nxt <= P.L && P.node[nxt] == j + 1) {
+      copy_vec(d, S.x, R.psi_nodes + nb + (size_t)nxt * d);
+      ++nxt;
+    }
+  }
+  if (which == 1) {
+    double t = 0.0;
+    for (int i = threadIdx.x; i < d; i += BT) t += cconjmul(P.targ[(size_t)b * d + i], S.x[i]).x;
+    t = block_sum(t, S.red);
+    if (threadIdx.x == 0) {
+      double pen = 0.0;
+      for (int n = 0; n < P.L; ++n) pen += R.pen[(size_t)b * P.L + n];
+      R.rec_exact[(size_t)b * R.cap + k] = P.ip_w * t - 0.5 * P.dt * pen;
+    }
+    return;
+  }
+  copy_vec(d, P.targ + (size_t)b * d, S.x);
+  copy_vec(d, S.x, R.chi_nodes + nb + (size_t)P.L * d);
+  int prev = P.L - 1;
+  for (int j = P.K - 1; j >= 0; --j) {
+    build(P, b, u + (size_t)j * C, half, S.W);
+    invert(d, S);
+    cayley(d, S.W, S.x, S.y, true);
+    copy_vec(d, S.y, S.x);
+    if (prev >= 0 && P.node[prev] == j) {
+      copy_vec(d, S.x, R.chi_nodes + nb + (size_t)prev * d);
+      --prev;
+    }
+  }
+}
+
+}  // namespace
+
+bool dense_big_supported(int d) { return d > 32 && d <= BIG_MAX; }
+
+cudaError_t dense_big_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
+  const size_t smem = big_smem(P.d, (A.mode & M_ASSEMBLE) != 0);
+  cudaError_t e = cudaFuncSetAttribute(dense_big_task_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dense_big_task_kernel<<<dim3(P.L, P.B), BT, smem, st>>>(P, R, A, ignore_done);
+  return cudaGetLastError();
+}
+
+cudaError_t dense_big_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
+  const size_t smem = big_smem(P.d, false);
+  cudaError_t e =
+      cudaFuncSetAttribute(dense_big_horizon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dense_big_horizon_kernel<<<P.B, BT, smem, st>>>(P, R, which, k);
+  return cudaGetLastError();
+}
+
+}  // namespace qoc

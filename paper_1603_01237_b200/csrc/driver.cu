@@ -231,8 +231,9 @@ void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaS
   switch (p->kind) {
     case QOC_KIND_DENSE: {
       if (!p->h0 || !p->linear) fail(QOC_EINVAL, "dense model needs h0 and linear operators");
-      if (dense_pad(d) < 0) fail(QOC_ELOGIC, "dense device kernels support d <= 32; use a structured kind");
-      out.stride = dense_pad(d);
+      if (dense_pad(d) < 0 && !dense_big_supported(d))
+        fail(QOC_ELOGIC, "dense device kernels support d <= 64; use a structured kind");
+      out.stride = dense_pad(d) > 0 ? dense_pad(d) : d;
       const size_t dd = (size_t)d * d;
       P.has_quad = p->quadratic != nullptr;
       const int nq = P.has_quad ? C : 0;
@@ -459,7 +460,8 @@ void alloc_run(const DeviceProblem& dp, int cap, const std::vector<int>& node, b
 // Kind dispatch ------------------------------------------------------------------------
 cudaError_t task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
   switch (P.kind) {
-    case QOC_KIND_DENSE: return dense_task(P, R, A, ignore_done, st);
+    case QOC_KIND_DENSE:
+      return P.d > 32 ? dense_big_task(P, R, A, ignore_done, st) : dense_task(P, R, A, ignore_done, st);
     case QOC_KIND_TRIDIAG: return tridiag_task(P, R, A, ignore_done, st);
     case QOC_KIND_BITFLIP: return bitflip_task(P, R, A, ignore_done, st);
     case QOC_KIND_STRANG: return strang_task(P, R, A, ignore_done, st);
@@ -468,7 +470,8 @@ cudaError_t task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ig
 }
 cudaError_t horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
   switch (P.kind) {
-    case QOC_KIND_DENSE: return dense_horizon(P, R, which, k, st);
+    case QOC_KIND_DENSE:
+      return P.d > 32 ? dense_big_horizon(P, R, which, k, st) : dense_horizon(P, R, which, k, st);
     case QOC_KIND_TRIDIAG: return tridiag_horizon(P, R, which, k, st);
     case QOC_KIND_BITFLIP: return bitflip_horizon(P, R, which, k, st);
     case QOC_KIND_STRANG: return strang_horizon(P, R, which, k, st);

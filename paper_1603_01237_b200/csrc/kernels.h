@@ -10,6 +10,11 @@ int dense_pad(int d);
 cudaError_t dense_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
 cudaError_t dense_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st);
 
+// dense 32 < d <= 64 (CTA per task, dense_big.cu)
+bool dense_big_supported(int d);
+cudaError_t dense_big_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
+cudaError_t dense_big_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st);
+
 // tridiagonal (d <= 32)
 cudaError_t tridiag_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
 cudaError_t tridiag_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st);

@@ -113,7 +113,9 @@ def ising10(subintervals: int = 256, iterations: int = 20, rho: float = 0.1, nsp
     u0 = (0.1 + 0.05 * z).reshape(2, steps)  # channel x then channel y
     grid = TimeGrid.over(0.0, T, steps)
     p = ControlProblem(model, grid, psi_i, psi_t, np.zeros(steps))
-    cfg = IsmConfig(subintervals=subintervals, workers=8, eta=0.0, max_outer=iterations)
+    # direct plan: the spin register never forms its d x d one-step matrices (16 MB each at
+    # d = 1024) on one GPU; direct and assembled agree to rounding (ism_test.cpp:248-265)
+    cfg = IsmConfig(subintervals=subintervals, workers=8, eta=0.0, max_outer=iterations, plan="direct")
     return Workload("ising10", p, u0, cfg, SolverSpec(step_size=rho), 0.1 / grid.dt)
 
 

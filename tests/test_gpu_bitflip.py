@@ -52,8 +52,12 @@ def test_run_ism_small_register(ctx, parts, plan):
 FIXTURES = __import__("pathlib").Path(__file__).parent / "golden"
 
 
-def compare_run(g, fx, tag, ctl_tol=1e-9, obj_tol=1e-10):
+def compare_run(g, fx, tag, ctl_tol=1e-9, obj_tol=1e-10, u0=None, upd_tol=1e-5):
     assert rel(g.control, fx[f"{tag}_control"]) < ctl_tol
+    if u0 is not None:  # the update itself (config 3's gradient is ~1e-9: u moves ~1e-8 in 20 iterations)
+        du_ref = fx[f"{tag}_control"] - np.asarray(u0)
+        assert np.max(np.abs(du_ref)) > 0
+        assert rel(g.control - np.asarray(u0), du_ref) < upd_tol
     obj = fx[f"{tag}_objective"]
     assert len(g.record.iterations) == len(obj)
     assert np.max(np.abs(g.record.objectives() - obj)) < obj_tol
@@ -75,4 +79,4 @@ def test_ising10_config3_iterations(ctx, tag):
     w = problems.ising10(iterations=20)
     w.solver.step_size = float(fx[f"{tag}_rho"])
     g = I.run_ism(w.problem, w.u0, w.config, w.solver, ctx)
-    compare_run(g, fx, tag)
+    compare_run(g, fx, tag, u0=w.u0)

@@ -15,7 +15,7 @@ def rel(a, b):
 
 
 @pytest.mark.parametrize("quad", [False, True])
-@pytest.mark.parametrize("dim", [2, 4, 7, 16, 21])
+@pytest.mark.parametrize("dim", [2, 4, 7, 16, 21, 33, 48, 64])
 def test_propagate_gradient_assemble(ctx, quad, dim):
     p, u = O.dense_fixture(100 + dim + 2 * quad, dim=dim, steps=16, quadratic=quad, random_penalty=True)
     fin = I.propagate_final(p, u, ctx)
@@ -125,3 +125,27 @@ def test_batch_all_problems_two_iterations(ctx):
         derr = max(abs(a.error - b.error) / max(1.0, abs(b.error))
                    for g, r in zip(gs, rs) for a, b in zip(g.record.iterations[1:], r.record.iterations[1:]))
         assert du < 1e-9 and dobj < 1e-10 and derr < 1e-9, (fast, du, dobj, derr)
+
+
+@pytest.mark.parametrize("dim", [48, 64])
+@pytest.mark.parametrize("variant,plan", [("interpolated", "assembled"), ("interpolated", "direct"),
+                                          ("split", "assembled")])
+def test_run_ism_large_dense(ctx, dim, variant, plan):
+    # DenseModel beyond the warp-resident sizes (CTA-per-task kernels, dense_big.cu); the
+    # reference benchmarks a d = 64 Crank-Nicolson step (benchmarks.cpp:76)
+    p, u = O.dense_fixture(2650 + dim, dim=dim, steps=12, channels=2, quadratic=True, random_penalty=True)
+    cfg = I.IsmConfig(subintervals=3, max_outer=9, eta=0.0, variant=variant, plan=plan,
+                      log_exact_objective=(variant == "split"))
+    sv = I.SolverSpec(step_size=0.5)
+    g = I.run_ism(p, u, cfg, sv, ctx)
+    r = O.ism_run(p, u, cfg, sv, O.REFERENCE)[0]
+    assert rel(g.control, r.control) < 1e-12
+    assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-12
+    for a, b in zip(g.record.iterations[1:], r.record.iterations[1:]):
+        assert abs(a.error - b.error) < 1e-11 * max(1.0, abs(b.error))
+
+
+def test_dense_above_64_rejected(ctx):
+    p, u = O.dense_fixture(2690, dim=65, steps=4, channels=1)
+    with pytest.raises(I.LogicError):
+        I.run_ism(p, u, I.IsmConfig(subintervals=2, max_outer=1), I.SolverSpec(step_size=0.1), ctx)
