@@ -339,6 +339,14 @@ def label_flops(name: str, label: str, w) -> float:
     elif name == "rotor21":
         per = {"assembly": 41 * d * d + 23 * d, "gradient": 64 * d + 64 * d + 24 * d,
                "residual": 64 * d + 64 * d + 24 * d}.get(label)
+    elif name == "ising10":
+        # bit-flip Cayley step (1 + m)(8n + 12) d with m from the contraction bound at u0
+        n = p.model.nspins
+        u = np.asarray(w.u0).reshape(C, K)
+        q = 0.5 * p.grid.dt * np.max(np.sqrt((np.abs(u[0]) * 0.5 * n) ** 2 + (np.abs(u[1]) * 0.5 * n) ** 2))
+        cay = (1 + int(np.ceil(53 * np.log(2) / -np.log(q)))) * (8 * n + 12) * d
+        per = {"node sweeps": 2 * cay,  # forward + adjoint full-horizon sweeps
+               "task": 5 * cay + 2 * C * n * 16 * d}.get(label)
     else:
         per = None
     if per is None:

@@ -93,3 +93,42 @@ def test_run_to_run_bitwise_determinism(ctx, kind):
         for s, t in zip(x.record.iterations, y.record.iterations):
             assert np.array_equal(np.asarray(s.task_values), np.asarray(t.task_values), equal_nan=True)
             assert (s.error == t.error) or (s.error is None and t.error is None)
+
+
+def test_checkpoint_stride_gives_identical_results(ctx):
+    # CheckpointedTrajectory (propagation.cpp:202-234) only trades memory for recomputation: the
+    # reference requires bit-identical results for any stride; the device keeps trajectories in
+    # HBM/L2 and accepts the stride, and the oracle run with the same stride agrees
+    p, u = O.strang_fixture(3000)
+    base = I.IsmConfig(subintervals=4, max_outer=4, eta=0.0, variant="split", log_exact_objective=True)
+    strided = I.IsmConfig(subintervals=4, max_outer=4, eta=0.0, variant="split", log_exact_objective=True,
+                          checkpoint_stride=3)
+    sv = I.SolverSpec(step_size=0.3, checkpoint_stride=3)
+    a = I.run_ism(p, u, base, I.SolverSpec(step_size=0.3), ctx)
+    b = I.run_ism(p, u, strided, sv, ctx)
+    assert np.array_equal(a.control, b.control)
+    r = O.ism_run(p, u, strided, sv)[0]
+    assert np.max(np.abs(b.control - r.control)) < 1e-12
+
+
+def test_run_artifacts_from_a_device_run(ctx, tmp_path):
+    # `qoc run` artifacts (tools/main.cpp:178-200) written from a device run, and the `qoc bench`
+    # efficiency.csv (main.cpp:339-372) over device runs at L = 1, 2, 4
+    import json
+    from paper_1603_01237_b200 import problems, wire
+    w = problems.spin2(iterations=30, rho=10.0)
+    run = I.run_ism(w.problem, w.u0, w.config, w.solver, ctx)
+    wire.write_run_artifacts(tmp_path / "run", w.problem, run, {"preset": "spin2"})
+    lines = (tmp_path / "run" / "iterations.jsonl").read_text().splitlines()
+    assert len(lines) == 31 and json.loads(lines[5])["iteration"] == 5
+    summary = json.loads((tmp_path / "run" / "summary.json").read_text())
+    assert summary["result"]["iterations"] == 30 and summary["result"]["solver"] == "gradient"
+    assert (tmp_path / "run" / "control.csv").read_text().startswith("t,")
+    runs = []
+    for L in (1, 2, 4):
+        w.config.subintervals = L
+        runs.append((L, I.run_ism(w.problem, w.u0, w.config, w.solver, ctx).record))
+    csv = wire.bench_efficiency_csv(runs, [0.1, 0.01])
+    rows = csv.splitlines()
+    assert rows[0] == "eps,N,t_seconds,speedup,efficiency" and len(rows) == 7
+    assert all(r.split(",")[0] in ("0.1", "0.01") for r in rows[1:])

@@ -1,17 +1,45 @@
 #!/usr/bin/env bash
-# Round-end evidence on one GPU (run under gpurun from the repo root): default bench line
-# (with cpu_baseline), the reference arm, every workload's bench line, the ncu launch list of
-# the default bench command and one --set full capture of its dominant kernel.
+# Round evidence on one GPU (run under gpurun from the repo root):
+#   * the default bench line (config 5, with cpu_baseline) and the reference arm;
+#   * every other workload's bench line with its cpu_baseline;
+#   * the ncu launch list of the default bench command (cold, serialised per-launch times);
+#   * one `ncu --set full` capture of each workload's dominant kernel(s);
+#   * compute-sanitizer memcheck and racecheck on the smoke workloads (one tool per run).
+# usage: tools/round_evidence.sh TAG [SECTION...]   sections: bench ncu sanitize (default: all)
 set -u
 out=gpurun_out/${1:-evidence}
+shift || true
+sections=${*:-"bench ncu sanitize"}
 mkdir -p "$out"
 nproc > "$out/nproc.txt"; lscpu > "$out/lscpu.txt" 2>&1
-timeout 900 python bench.py > "$out/bench_default.json" 2> "$out/bench_default.err"; echo "default rc=$?"
-timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > "$out/bench_reference.json" 2> "$out/bench_reference.err"; echo "reference rc=$?"
-for wl in spin2 batch4096 ising10 gpe1024; do
-  timeout 900 python bench.py --workload $wl --steps 5 --warmup 3 --no-cpu-baseline > "$out/bench_$wl.json" 2> "$out/bench_$wl.err"; echo "$wl rc=$?"
-done
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file "$out/launches_default.csv" \
-  python bench.py --steps 2 --warmup 3 --no-cpu-baseline > "$out/ncu_launch.log" 2>&1; echo "launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:tri_pc_assemble|pc_eval|chain_small" -c 3 \
-  -o "$out/full_default" python bench.py --steps 1 --warmup 3 --no-cpu-baseline > "$out/ncu_full.log" 2>&1; echo "full rc=$?"
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > "$out/gpu.txt" 2>&1
+if [[ " $sections " == *" bench "* ]]; then
+  timeout 900 python bench.py > "$out/bench_default.json" 2> "$out/bench_default.err"; echo "default rc=$?"
+  timeout 900 python bench.py --impl reference > "$out/bench_reference.json" 2> "$out/bench_reference.err"; echo "reference rc=$?"
+  for wl in spin2 rotor21 ising10 gpe1024; do
+    timeout 900 python bench.py --workload $wl --steps 10 --warmup 3 > "$out/bench_$wl.json" 2> "$out/bench_$wl.err"
+    echo "$wl rc=$?"
+  done
+fi
+if [[ " $sections " == *" ncu "* ]]; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file "$out/launches_default.csv" \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-ttf > "$out/ncu_launch.log" 2>&1; echo "launches rc=$?"
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:dense_nm_assemble|dense_pc_eval16" -c 3 \
+    -o "$out/full_batch4096" python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-ttf > "$out/ncu_full_batch.log" 2>&1
+  echo "full batch rc=$?"
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:bitflip_horizon_cluster|bitflip_task" -c 2 \
+    -o "$out/full_ising10" python bench.py --workload ising10 --steps 1 --warmup 3 --no-cpu-baseline --no-ttf \
+    > "$out/ncu_full_ising.log" 2>&1; echo "full ising rc=$?"
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:strang_task" -c 2 \
+    -o "$out/full_gpe1024" python bench.py --workload gpe1024 --steps 1 --warmup 3 --no-cpu-baseline --no-ttf \
+    > "$out/ncu_full_gpe.log" 2>&1; echo "full gpe rc=$?"
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:tri_pc_assemble|pc_eval|chain_small" -c 3 \
+    -o "$out/full_rotor21" python bench.py --workload rotor21 --steps 1 --warmup 3 --no-cpu-baseline --no-ttf \
+    > "$out/ncu_full_rotor.log" 2>&1; echo "full rotor rc=$?"
+fi
+if [[ " $sections " == *" sanitize "* ]]; then
+  timeout 1200 compute-sanitizer --tool memcheck --leak-check full python __graft_entry__.py > "$out/memcheck.log" 2>&1
+  echo "memcheck rc=$?"
+  timeout 1500 compute-sanitizer --tool racecheck python __graft_entry__.py > "$out/racecheck.log" 2>&1
+  echo "racecheck rc=$?"
+fi
