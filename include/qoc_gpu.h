@@ -67,7 +67,15 @@ enum qoc_status_code {
  *             significant as in spin_operator, models.cpp:296-318).
  *   STRANG  - periodic-grid condensate, split-step Fourier (propagation.cpp:131-170),
  *             TrappedCondensateModel-style potentials (models.cpp:77-127). */
-enum qoc_kind { QOC_KIND_DENSE = 0, QOC_KIND_TRIDIAG = 1, QOC_KIND_BITFLIP = 2, QOC_KIND_STRANG = 3 };
+enum qoc_kind { QOC_KIND_DENSE = 0, QOC_KIND_TRIDIAG = 1, QOC_KIND_BITFLIP = 2, QOC_KIND_STRANG = 3,
+                QOC_KIND_DENSITY = 4 };
+/* QOC_KIND_DENSITY - DenseModel with PropagatorKind::cn_conjugation (propagation.cpp:92-129):
+ *             the same H0 / A_c / B_c payload as DENSE (dim = d <= 32), but every state is a
+ *             d x d matrix rho (initial / target: [B][d*d] complex, column-major) stepped as
+ *             rho' = A rho A^dag, A = (I + L)^-1 (I - L); channel count up to QOC_MAX_DENSITY_CHANNELS.
+ *             The boundary refresh always runs as direct node sweeps (assembled and direct agree
+ *             to rounding, ism_test.cpp:248-265). */
+#define QOC_MAX_DENSITY_CHANNELS 32
 
 /* Sampled potentials for QOC_KIND_STRANG.
  *   TRAP    : models.cpp:95-127, pot_params = {trap_distance}

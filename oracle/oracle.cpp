@@ -256,6 +256,108 @@ struct DenseM : Model {
   }
 };
 
+// Density-matrix kind: DenseModel with PropagatorKind::cn_conjugation (models.cpp:45-75,
+// propagation.cpp:92-129).  A state is a dm x dm matrix held as a dm^2 column-major vector
+// (Model::d = dm^2), stepped rho' = A rho A^dag with A = (I+L)^-1 (I-L); the adjoint is
+// X' = A^dag X A.  The same LU solves, in the same order, as the reference.
+struct ConjM : Model {
+  int dm = 0;
+  CMat h0;
+  std::vector<CMat> lin, quad;
+  CMat hamiltonian(const double* u) const {  // models.cpp:57-68
+    CMat h = h0;
+    for (int c = 0; c < C; ++c)
+      for (size_t e = 0; e < h.v.size(); ++e) h.v[e] += u[c] * lin[static_cast<size_t>(c)].v[e];
+    for (size_t c = 0; c < quad.size(); ++c) {
+      const double s = 0.5 * u[c] * u[c];
+      for (size_t e = 0; e < h.v.size(); ++e) h.v[e] += s * quad[c].v[e];
+    }
+    return h;
+  }
+  CMat derivative(int c, const double* u) const {  // models.cpp:70-75
+    CMat a = lin[static_cast<size_t>(c)];
+    if (!quad.empty())
+      for (size_t e = 0; e < a.v.size(); ++e) a.v[e] += u[c] * quad[static_cast<size_t>(c)].v[e];
+    return a;
+  }
+  void plus_minus(const double* u, double dt, CMat& plus, CMat& minus) const {
+    const CMat h = hamiltonian(u);
+    const cd half(0.0, 0.5 * dt);  // half_step_matrix, propagation.cpp:14-16
+    plus = CMat::identity(dm);
+    minus = CMat::identity(dm);
+    for (size_t e = 0; e < h.v.size(); ++e) {
+      plus.v[e] += half * h.v[e];
+      minus.v[e] -= half * h.v[e];
+    }
+  }
+  static CMat mat_of(const cd* x, int n) {
+    CMat r(n, n);
+    for (size_t e = 0; e < r.v.size(); ++e) r.v[e] = x[e];
+    return r;
+  }
+  void cayley(const double* u, double dt, CMat& X, bool adj) const override {
+    CMat plus, minus;
+    plus_minus(u, dt, plus, minus);
+    const PivLU lu(adj ? minus : plus);
+    for (int col = 0; col < X.cols; ++col) {
+      cd* x = &X(0, col);
+      const CMat r = mat_of(x, dm);
+      CMat out;
+      if (!adj) {  // cn_conjugation_step (92-99): g = A rho, out = (A g^dag)^dag
+        CMat g = matmul(minus, r);
+        lu.solve_inplace(g);
+        CMat t = matmul(minus, adjoint(g));
+        lu.solve_inplace(t);
+        out = adjoint(t);
+      } else {  // cn_conjugation_adjoint_step (108-115): b = A^dag X, out = (A^dag b^dag)^dag
+        CMat s0 = r;
+        lu.solve_inplace(s0);
+        const CMat b = matmul(plus, s0);
+        CMat t = adjoint(b);
+        lu.solve_inplace(t);
+        out = adjoint(matmul(plus, t));
+      }
+      for (size_t e = 0; e < out.v.size(); ++e) x[e] = out.v[e];
+    }
+  }
+  // cn_conjugation_backward_stage (117-129) and the gradient row of objective.cpp:61-71:
+  // chi <- X_j; g[c] = 2 dt Im tr(r1^dag dH_c r2), r1 = (I-L)^-1 X_{j+1}, r2 = (I-L)^-1 rho_{j+1}
+  void backward(const double* u, double dt, CV& chi, const CV& rho_next, double* trace_im) const {
+    CMat plus, minus;
+    plus_minus(u, dt, plus, minus);
+    const PivLU lm(minus);
+    CMat r1 = mat_of(chi.data(), dm), r2 = mat_of(rho_next.data(), dm);
+    lm.solve_inplace(r1);
+    lm.solve_inplace(r2);
+    const CMat b = matmul(plus, r1);
+    CMat t = adjoint(b);
+    lm.solve_inplace(t);
+    const CMat xj = adjoint(matmul(plus, t));
+    chi = xj.v;
+    const CMat r1h = adjoint(r1);
+    for (int c = 0; c < C; ++c) {
+      const CMat m = matmul(matmul(r1h, derivative(c, u)), r2);
+      cd tr = 0.0;
+      for (int i = 0; i < dm; ++i) tr += m(i, i);
+      trace_im[c] = tr.imag();
+    }
+  }
+  CMat assemble_dm(const double* u, int len, double dt) const {  // propagation.cpp:236-249
+    CMat prod = CMat::identity(dm);
+    for (int j = 0; j < len; ++j) {
+      CMat plus, minus;
+      plus_minus(u + static_cast<size_t>(j) * C, dt, plus, minus);
+      CMat rhs = matmul(minus, prod);
+      PivLU(plus).solve_inplace(rhs);
+      prod = std::move(rhs);
+    }
+    return prod;
+  }
+  void dH(int, const double*, const cd*, cd*) const override {
+    throw LogicErr("the conjugation kind has its own gradient row");
+  }
+};
+
 // Hermitian tridiagonal operators, Thomas elimination.  I + i dt/2 H is strictly diagonally
 // dominant for the rotor (|diag| >= 1 > off-diagonal), so Eigen's partial pivoting never
 // swaps and the LU it forms is exactly this elimination; a swap is detected and refused.
@@ -561,7 +663,8 @@ static Prob make_prob(const qoc_problem_v1* p, int b, int arith) {
   validate(p);
   Prob P;
   const int d = p->dim, C = p->channels;
-  P.d = d;
+  const int slen = p->kind == QOC_KIND_DENSITY ? d * d : d;  // state length
+  P.d = slen;
   P.C = C;
   P.K = p->steps;
   P.t0 = p->t_start;
@@ -588,6 +691,18 @@ static Prob make_prob(const qoc_problem_v1* p, int b, int arith) {
       hermitian(m->h0, "free Hamiltonian");
       for (const CMat& a : m->lin) hermitian(a, "control operator");
       for (const CMat& a : m->quad) hermitian(a, "quadratic operator");
+      P.m = m;
+      break;
+    }
+    case QOC_KIND_DENSITY: {
+      if (!p->h0 || !p->linear) throw InvalidArg("density model needs h0 and linear operators");
+      auto m = std::make_shared<ConjM>();
+      m->dm = d;
+      m->h0 = load_cmat(p->h0 + 2 * dd * b, d);
+      for (int c = 0; c < C; ++c) m->lin.push_back(load_cmat(p->linear + 2 * dd * (static_cast<size_t>(b) * C + c), d));
+      if (p->quadratic)
+        for (int c = 0; c < C; ++c)
+          m->quad.push_back(load_cmat(p->quadratic + 2 * dd * (static_cast<size_t>(b) * C + c), d));
       P.m = m;
       break;
     }
@@ -664,11 +779,11 @@ static Prob make_prob(const qoc_problem_v1* p, int b, int arith) {
       throw InvalidArg("unknown model kind");
   }
   P.m->kind = p->kind;
-  P.m->d = d;
+  P.m->d = slen;
   P.m->C = C;
   P.m->w = p->ip_weight;
-  P.init = load_cvec(p->initial + 2 * static_cast<size_t>(b) * d, static_cast<size_t>(d));
-  P.targ = load_cvec(p->target + 2 * static_cast<size_t>(b) * d, static_cast<size_t>(d));
+  P.init = load_cvec(p->initial + 2 * static_cast<size_t>(b) * slen, static_cast<size_t>(slen));
+  P.targ = load_cvec(p->target + 2 * static_cast<size_t>(b) * slen, static_cast<size_t>(slen));
   P.alpha.assign(static_cast<size_t>(P.K), 0.0);
   if (p->penalty) P.alpha.assign(p->penalty, p->penalty + P.K);
   return P;
@@ -799,7 +914,11 @@ static RV sweep(const Model& m, const double* u, int len, double dt,
   CV tmp(static_cast<size_t>(m.d));
   for (int j = len - 1; j >= 0; --j) {
     const double* uj = u + static_cast<size_t>(j) * C;
-    if (m.kind == QOC_KIND_STRANG) {
+    if (m.kind == QOC_KIND_DENSITY) {  // objective.cpp:61-71
+      double tr[64];
+      static_cast<const ConjM&>(m).backward(uj, dt, chi, state_at(j + 1), tr);
+      for (int c = 0; c < C; ++c) g[c + static_cast<size_t>(j) * C] = -alpha[j] * dt * uj[c] + 2.0 * dt * tr[c];
+    } else if (m.kind == QOC_KIND_STRANG) {
       CV cj, pb, cb;
       const auto& sm = static_cast<const StrangM&>(m);
       sm.backward(uj, dt, state_at(j), chi, naive, cj, pb, cb);
@@ -845,6 +964,7 @@ static RV gradient(const Model& m, const double* u, int len, double dt, const CV
 
 static CMat assemble(const Model& m, const double* u, int len, double dt) {  // 236-249
   if (!m.linear()) throw LogicErr("no dense one-step matrices to assemble for this propagator kind");
+  if (m.kind == QOC_KIND_DENSITY) return static_cast<const ConjM&>(m).assemble_dm(u, len, dt);
   CMat prod = CMat::identity(m.d);
   for (int j = 0; j < len; ++j) m.cayley(u + static_cast<size_t>(j) * m.C, dt, prod, false);
   return prod;
@@ -1088,7 +1208,9 @@ static RunOut run_ism(const Prob& P, const double* u0, const qoc_ism_config_v1& 
   if (sv.kind != QOC_SOLVER_GRADIENT) throw LogicErr("only the gradient solver is on this path");
   const int parts = cfg.subintervals;
   const std::vector<int> node = decomposition(P.K, parts, cfg.partition, cfg.node_index);
-  const bool direct = cfg.plan == QOC_PLAN_DIRECT;
+  // the density kind refreshes its boundaries by direct node sweeps (as the device does;
+  // assembled and direct agree to rounding, ism_test.cpp:248-265)
+  const bool direct = cfg.plan == QOC_PLAN_DIRECT || m.kind == QOC_KIND_DENSITY;
   const int stride = cfg.checkpoint_stride > 0 ? cfg.checkpoint_stride : sv.checkpoint_stride;
   const bool naive = sv.naive_nonlinear_adjoint != 0;
   const int C = P.C;
@@ -1473,7 +1595,7 @@ extern "C" int32_t oracle_assemble_propagator(const qoc_problem_v1* p, const dou
     for (int b = 0; b < p->batch; ++b) {
       const Prob P = make_prob(p, b, arith);
       const CMat M = assemble(*P.m, u + CK * b, P.K, P.dt);
-      store(M.v, prop_out + 2 * static_cast<size_t>(b) * P.d * P.d);
+      store(M.v, prop_out + 2 * static_cast<size_t>(b) * p->dim * p->dim);
     }
   });
 }

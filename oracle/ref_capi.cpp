@@ -94,6 +94,14 @@ std::shared_ptr<const qoc::HamiltonianModel> make_model(const qoc_problem_v1* p,
         for (int c = 0; c < C; ++c) quad.push_back(load_cmat(p->quadratic + 2 * dd * ((size_t)b * C + c), d));
       return std::make_shared<qoc::DenseModel>(qoc::PropagatorKind::cn_dense, h0, lin, quad);
     }
+    case QOC_KIND_DENSITY: {  // the same payload, PropagatorKind::cn_conjugation (propagation.cpp:92-129)
+      CMat h0 = load_cmat(p->h0 + 2 * dd * b, d);
+      std::vector<CMat> lin, quad;
+      for (int c = 0; c < C; ++c) lin.push_back(load_cmat(p->linear + 2 * dd * ((size_t)b * C + c), d));
+      if (p->quadratic)
+        for (int c = 0; c < C; ++c) quad.push_back(load_cmat(p->quadratic + 2 * dd * ((size_t)b * C + c), d));
+      return std::make_shared<qoc::DenseModel>(qoc::PropagatorKind::cn_conjugation, h0, lin, quad);
+    }
     case QOC_KIND_TRIDIAG: {
       const int nops = 1 + C + (p->tri_has_quadratic ? C : 0);
       std::vector<CMat> ops;
@@ -157,8 +165,13 @@ extern "C" int32_t ref_ism_run(const qoc_problem_v1* p, const qoc_ism_config_v1*
       qoc::ControlProblem prob;
       prob.model = make_model(p, b);
       prob.grid = qoc::TimeGrid{p->t_start, p->dt, K};
-      prob.initial = load_state(p->initial + 2 * (size_t)d * b, d);
-      prob.target = load_state(p->target + 2 * (size_t)d * b, d);
+      if (p->kind == QOC_KIND_DENSITY) {  // d x d matrix states, column-major
+        prob.initial = load_cmat(p->initial + 2 * (size_t)d * d * b, d);
+        prob.target = load_cmat(p->target + 2 * (size_t)d * d * b, d);
+      } else {
+        prob.initial = load_state(p->initial + 2 * (size_t)d * b, d);
+        prob.target = load_state(p->target + 2 * (size_t)d * b, d);
+      }
       prob.penalty.values.assign(K, 0.0);
       if (p->penalty) prob.penalty.values.assign(p->penalty, p->penalty + K);
       qoc::RMat samples(C, K);

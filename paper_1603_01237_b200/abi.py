@@ -15,7 +15,7 @@ import numpy as np
 QOC_ABI_VERSION = 1
 
 QOC_OK, QOC_EINVAL, QOC_ELOGIC, QOC_ECUDA, QOC_ENCCL, QOC_ERUNTIME = range(6)
-KIND_DENSE, KIND_TRIDIAG, KIND_BITFLIP, KIND_STRANG = range(4)
+KIND_DENSE, KIND_TRIDIAG, KIND_BITFLIP, KIND_STRANG, KIND_DENSITY = range(5)
 POT_TRAP, POT_LATTICE = range(2)
 VARIANT_INTERPOLATED, VARIANT_SPLIT = range(2)
 PLAN_ASSEMBLED, PLAN_DIRECT = range(2)

@@ -177,8 +177,14 @@ class IsmRun:
 # ----------------------------------------------------------------------------------------
 # Packing into the C ABI (shared with the test-side oracle wrapper).
 # ----------------------------------------------------------------------------------------
-def _states(a, B: int, d: int, what: str) -> np.ndarray:
+def _states(a, B: int, d: int, what: str, square: bool = False) -> np.ndarray:
     a = np.asarray(a, dtype=np.complex128)
+    if square:  # d x d matrix states (density kind): column-major, like Eigen's MatrixXcd
+        if a.ndim == 2:
+            a = np.broadcast_to(a[None], (B,) + a.shape)
+        if a.shape != (B, d, d):
+            raise InvalidArgument(f"{what} state has shape {a.shape}, expected ({B}, {d}, {d})")
+        return np.ascontiguousarray(np.swapaxes(a, 1, 2)).reshape(B, d * d)
     if a.ndim == 2 and a.shape[1] == 1 and B == 1 and a.shape[0] == d:
         a = a[:, 0]
     if a.ndim == 1:
@@ -204,8 +210,9 @@ def pack_problem(p: ControlProblem) -> abi.PackedProblem:
     s.dt = p.grid.dt
     s.ip_weight = m.ip_weight()
     m.pack_into(s, keep)
-    ini = abi.cplx(_states(p.initial, m.batch, s.dim, "initial"))
-    tgt = abi.cplx(_states(p.target, m.batch, s.dim, "target"))
+    sq = m.kind == abi.KIND_DENSITY
+    ini = abi.cplx(_states(p.initial, m.batch, s.dim, "initial", sq))
+    tgt = abi.cplx(_states(p.target, m.batch, s.dim, "target", sq))
     keep += [ini, tgt]
     s.initial, s.target = abi.dptr(ini), abi.dptr(tgt)
     if p.penalty is not None:
@@ -352,17 +359,32 @@ def run_ism(p: ControlProblem, u0, cfg: IsmConfig, solver: SolverSpec, ctx=None)
     return run_ism_batch(p, u0, cfg, solver, ctx)[0]
 
 
+def state_shape(model) -> tuple:
+    """Shape of one state: (d,) vectors, or (d, d) matrices for the density kind."""
+    d = model.state_dim()
+    return (d, d) if model.kind == abi.KIND_DENSITY else (d,)
+
+
+def unpack_states(flat: np.ndarray, model, lead: tuple) -> np.ndarray:
+    """Interleaved complex states (column-major matrices for the density kind) -> numpy."""
+    z = flat.view(np.complex128)
+    shp = state_shape(model)
+    if len(shp) == 2:
+        return np.swapaxes(z.reshape(lead + (shp[1], shp[0])), -1, -2)
+    return z.reshape(lead + shp)
+
+
 def propagate_final(p: ControlProblem, u, ctx=None) -> np.ndarray:
-    """propagation.cpp:194-200, on the device: (B, d) final states."""
+    """propagation.cpp:194-200, on the device: (B,) + state shape final states."""
     from . import _native
     packed = pack_problem(p)
-    B, Cn, K, d = p.batch, p.model.channels(), p.grid.steps, p.model.state_dim()
+    B, Cn, K = p.batch, p.model.channels(), p.grid.steps
     u_in = controls_to_abi(u, B, Cn, K)
-    out = np.empty(2 * B * d)
+    out = np.empty(2 * B * int(np.prod(state_shape(p.model))))
     ctx = ctx or _native.default_context()
     raise_for(ctx.lib.qoc_propagate_final(ctx.handle, packed.ref, abi.dptr(u_in), abi.dptr(out)),
               ctx.last_error())
-    return out.view(np.complex128).reshape(B, d)
+    return unpack_states(out, p.model, (B,))
 
 
 def objective_gradient(p: ControlProblem, u, form: str = "tracking", naive: bool = False, ctx=None):

@@ -109,6 +109,17 @@ class DenseModel(HamiltonianModel):
             s.quadratic = abi.dptr(q)
 
 
+class DensityModel(DenseModel):
+    """DenseModel with PropagatorKind::cn_conjugation (propagation.cpp:92-129): the states are
+    d x d matrices stepped rho' = A rho A^dag (the reference's `spins` preset, models.cpp:320-347).
+    state_dim() is the edge size d (propagation.hpp:25); the packed states are d*d long."""
+
+    kind = abi.KIND_DENSITY
+
+    def state_len(self) -> int:
+        return self.state_dim() ** 2
+
+
 class TridiagonalModel(HamiltonianModel):
     """DenseModel whose H0, A_c (and B_c) are Hermitian tridiagonal (rotor, models.cpp:349-359).
 

@@ -17,7 +17,7 @@ import numpy as np
 
 from . import abi
 from .ism import ControlProblem, IsmConfig, SolverSpec, TimeGrid
-from .models import CondensateModel, DenseModel, SpinRegisterModel, TridiagonalModel
+from .models import CondensateModel, DenseModel, DensityModel, SpinRegisterModel, TridiagonalModel
 
 SX = np.array([[0, 1], [1, 0]], dtype=np.complex128)
 SY = np.array([[0, -1j], [1j, 0]], dtype=np.complex128)
@@ -117,6 +117,48 @@ def ising10(subintervals: int = 256, iterations: int = 20, rho: float = 0.1, nsp
     # d = 1024) on one GPU; direct and assembled agree to rounding (ism_test.cpp:248-265)
     cfg = IsmConfig(subintervals=subintervals, workers=8, eta=0.0, max_outer=iterations, plan="direct")
     return Workload("ising10", p, u0, cfg, SolverSpec(step_size=rho), 0.1 / grid.dt)
+
+
+# --------------------------------------------------------------------------------------
+# The reference's `spins` preset: density-matrix (conjugation) transfer on a coupled chain
+# (models.cpp:320-347, config.cpp:128-146; the paper's 5-spin benchmark).
+# --------------------------------------------------------------------------------------
+def spin_operator(n: int, k: int, axis: str) -> np.ndarray:
+    """sigma_axis / 2 on spin k of n (spin 0 = most significant factor, models.cpp:296-318)."""
+    s = {"x": SX, "y": SY, "z": SZ}[axis] / 2
+    op = np.eye(1, dtype=np.complex128)
+    for i in range(n):
+        op = np.kron(op, s if i == k else I2)
+    return op
+
+
+def default_couplings(n: int):  # config.cpp:79-93
+    if n == 5:
+        return [(1, 2), (1, 3), (2, 3), (2, 5), (3, 4)]
+    if n == 3:
+        return [(1, 2), (1, 3), (2, 3)]
+    return [(a, a + 1) for a in range(1, n)]
+
+
+def spins_preset(quick: bool = True, subintervals: int = 4, iterations=None, steps=None, seed: int = 7) -> Workload:
+    """spin_chain_problem (models.cpp:320-347) with the preset parameters (config.cpp:132-146;
+    SpinsParams defaults config.hpp:21-28): n = 3 (quick) or 5 spins, J = 140, duration 0.14 or
+    14, 2^10 or 2^15 steps, alpha = 0, gradient rho = 1e4, interpolated variant, initial control
+    uniform in [-1, 1] (the reference draws it with std::mt19937 seed 7; here numpy PCG64 seed 7)."""
+    n = 3 if quick else 5
+    J, T = 140.0, (0.14 if quick else 14.0)
+    K = steps or (1 << 10 if quick else 1 << 15)
+    h0 = sum(2.0 * np.pi * J * (spin_operator(n, a - 1, "z") @ spin_operator(n, b - 1, "z"))
+             for a, b in default_couplings(n))
+    ctl = []
+    for k in range(n):
+        ctl += [spin_operator(n, k, "x"), spin_operator(n, k, "y")]
+    grid = TimeGrid.over(0.0, T, K)
+    p = ControlProblem(DensityModel(h0, np.stack(ctl)), grid, spin_operator(n, 0, "x"),
+                       spin_operator(n, n - 1, "x"), np.zeros(K))
+    u0 = np.random.default_rng(seed).uniform(-1.0, 1.0, (2 * n, K))
+    cfg = IsmConfig(subintervals=subintervals, workers=8, eta=0.0, max_outer=iterations or (25 if quick else 50))
+    return Workload("spins", p, u0, cfg, SolverSpec(step_size=1e4), 0.1 / grid.dt)
 
 
 # --------------------------------------------------------------------------------------

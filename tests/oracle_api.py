@@ -62,13 +62,13 @@ def ism_run(p: I.ControlProblem, u0, cfg: I.IsmConfig, solver: I.SolverSpec,
 
 def propagate_final(p, u, arith=STRUCTURED):
     packed = I.pack_problem(p)
-    B, d = p.batch, p.model.state_dim()
+    B, d = p.batch, int(np.prod(I.state_shape(p.model)))
     u_in = I.controls_to_abi(u, B, p.model.channels(), p.grid.steps)
     out = np.empty(2 * B * d)
     err = _err()
     _check(lib().oracle_propagate_final(packed.ref, abi.dptr(u_in), abi.dptr(out), C.c_int32(arith),
                                         err, C.c_size_t(512)), err)
-    return out.view(np.complex128).reshape(B, d)
+    return I.unpack_states(out, p.model, (B,))
 
 
 def propagate(p, u, arith=STRUCTURED):

@@ -156,3 +156,23 @@ def test_integration_shim_compiles():
     root = Path(__file__).resolve().parents[1]
     subprocess.run(["make", "-s", "-C", str(root / "integration"), "_build/ism_gpu.o"], check=True)
     assert (root / "integration" / "_build" / "ism_gpu.o").exists()
+
+
+@pytest.mark.parametrize("plan", ["assembled", "direct"])
+@pytest.mark.parametrize("parts", [1, 4])
+def test_density_matrix_spins_preset(plan, parts):
+    # the reference's `spins` preset (density-matrix conjugation kind, models.cpp:320-347,
+    # propagation.cpp:92-129, objective.cpp:61-71), quick size: 3 spins, 2^10 steps, rho = 1e4
+    w = problems.spins_preset(quick=True, subintervals=parts, iterations=5)
+    w.config.plan = plan
+    w.config.partition = "uniform"
+    compare(O.ref_ism_run(w.problem, w.u0, w.config, w.solver)[0],
+            O.ism_run(w.problem, w.u0, w.config, w.solver, O.REFERENCE)[0], ctl_abs=1e-12, obj_abs=1e-12)
+
+
+def test_density_matrix_five_spins():
+    # the paper's 5-spin chain (d = 32, ten x/y channels) on a shortened grid
+    w = problems.spins_preset(quick=False, subintervals=4, iterations=3, steps=128)
+    w.config.partition = "uniform"
+    compare(O.ref_ism_run(w.problem, w.u0, w.config, w.solver)[0],
+            O.ism_run(w.problem, w.u0, w.config, w.solver, O.REFERENCE)[0], ctl_abs=1e-11, obj_abs=1e-11)
