@@ -105,6 +105,7 @@ enum TaskMode : int {
 // ---- problem + run state as seen by kernels ------------------------------------------
 struct DevProblem {
   int kind, d, C, K, B, L;
+  int dm;  // matrix edge of the density kind (its states are dm x dm, d = dm^2); = d otherwise
   int has_quad;
   double dt, ip_w;
   // DENSE: row-major [B][d][d]; quad may be null.  Column 1-norms for the pivot bound.

@@ -51,8 +51,8 @@ __device__ double block_sum(double v, double* red) {
 }
 
 // B = I + s i H(u), s = +half (forward) -- H(u) = H0 + sum u_c A_c + sum (u_c^2/2) B_c
-__device__ void build(const DevProblem& P, int b, const double* u, double half, double2* W) {
-  const int d = P.d, C = P.C;
+__device__ void build(const DevProblem& P, int b, const double* u, double half, double2* W, int dmat = 0) {
+  const int d = dmat ? dmat : P.d, C = P.C;
   const size_t dd = (size_t)d * d;
   for (int e = threadIdx.x; e < d * d; e += BT) {
     double2 h = P.h0[(size_t)b * dd + e];
@@ -419,6 +419,290 @@ __global__ void __launch_bounds__(BT) dense_big_horizon_kernel(DevProblem P, Dev
   }
 }
 
+// ---- density-matrix (conjugation) kind: CTA per task --------------------------------------
+// States are dm x dm matrices held column-major (the packed ABI layout, state length P.d = dm^2);
+// W = B_j^-1 is row-major (build + invert above).  With A = 2W - I (propagation.cpp:92-129):
+//   forward   rho' = A rho A^dag : G = 2 W rho - rho,  rho' = 2 G W^dag - G
+//   adjoint   X'   = A^dag X A   : b = 2 W^dag X - X,  X'   = 2 b W - b
+//   gradient  g_c  = -alpha dt u_c + 2 dt Im tr(r1^dag dH_c r2),  r1 = W^dag X_{j+1},
+//             r2 = W^dag rho_{j+1}  (cn_conjugation_backward_stage + objective.cpp:61-71), and
+//             b = 2 r1 - X_{j+1}.
+constexpr int DENS_MAX = 32;
+
+// C = op(A) op(B), dm x dm; A/B/C accessors select layout and conjugate-transpose
+enum MOp { ROW = 0, ROW_H = 1, COL = 2, COL_H = 3 };
+__device__ __forceinline__ double2 at(const double2* M, int dm, int i, int j, MOp op) {
+  switch (op) {
+    case ROW: return M[i * dm + j];
+    case ROW_H: return cconj(M[j * dm + i]);
+    case COL: return M[i + j * dm];
+    default: return cconj(M[j + i * dm]);
+  }
+}
+// out (column-major) = alpha * op(A) op(B) + beta * Cin (column-major, may alias out only if beta == 0)
+__device__ void mm(int dm, const double2* A, MOp oa, const double2* Bm, MOp ob, double alpha, const double2* Cin,
+                   double beta, double2* out) {
+  for (int e = threadIdx.x; e < dm * dm; e += BT) {
+    const int i = e % dm, j = e / dm;
+    double2 acc = cx(0.0, 0.0);
+    for (int k = 0; k < dm; ++k) acc = cfma(at(A, dm, i, k, oa), at(Bm, dm, k, j, ob), acc);
+    double2 r = cx(alpha * acc.x, alpha * acc.y);
+    if (beta != 0.0) r = cx(fma(beta, Cin[e].x, r.x), fma(beta, Cin[e].y, r.y));
+    out[e] = r;
+  }
+  __syncthreads();
+}
+
+struct DensSmem {
+  double2 *W, *S, *G, *T, *X;  // W row-major; states column-major
+  BigSmem lin;                 // vectors / reduction scratch of invert
+};
+
+__device__ DensSmem carve_dens(unsigned char* raw, int dm) {
+  DensSmem D;
+  double2* p = reinterpret_cast<double2*>(raw);
+  const size_t mm2 = (size_t)dm * dm;
+  D.W = p;
+  D.S = p + mm2;
+  D.G = p + 2 * mm2;
+  D.T = p + 3 * mm2;
+  D.X = p + 4 * mm2;
+  BigSmem& S = D.lin;
+  S.W = D.W;
+  S.Pm = S.T = nullptr;
+  double2* v = p + 5 * mm2;
+  S.x = v;
+  S.y = v + dm;
+  S.z = v + 2 * dm;
+  S.v = v + 3 * dm;
+  S.prow = v + 4 * dm;
+  S.colk = v + 5 * dm;
+  S.red = reinterpret_cast<double*>(v + 6 * dm);
+  S.perm = reinterpret_cast<int*>(S.red + BT);
+  S.piv = S.perm + dm + BT / 32;
+  return D;
+}
+
+size_t dens_smem(int dm) {
+  return sizeof(double2) * (5 * (size_t)dm * dm + 6 * (size_t)dm) + sizeof(double) * BT +
+         sizeof(int) * (dm + BT / 32 + 2);
+}
+
+// W = B_j^-1 at control uj
+__device__ void dens_inverse(const DevProblem& P, int b, const double* uj, DensSmem& D) {
+  build(P, b, uj, 0.5 * P.dt, D.W, P.dm);
+  invert(P.dm, D.lin);
+}
+// rho (column-major in/out) <- A rho A^dag ; uses G
+__device__ void dens_forward(int dm, DensSmem& D, double2* rho) {
+  mm(dm, D.W, ROW, rho, COL, 2.0, rho, -1.0, D.G);     // G = 2 W rho - rho
+  mm(dm, D.G, COL, D.W, ROW_H, 2.0, D.G, -1.0, rho);   // rho' = 2 G W^dag - G
+}
+// X (column-major in/out) <- A^dag X A ; uses G
+__device__ void dens_adjoint(int dm, DensSmem& D, double2* X) {
+  mm(dm, D.W, ROW_H, X, COL, 2.0, X, -1.0, D.G);       // b = 2 W^dag X - X
+  mm(dm, D.G, COL, D.W, ROW, 2.0, D.G, -1.0, X);       // X' = 2 b W - b
+}
+__device__ void dens_copy(int n, const double2* src, double2* dst) {
+  for (int i = threadIdx.x; i < n; i += BT) dst[i] = src[i];
+  __syncthreads();
+}
+// Im tr(r1^dag dH_c r2) summed into trace_im[c]; r1 in T, r2 in G (column-major); uses S? no: scratch X2
+__device__ double dens_trace_im(const DevProblem& P, int b, int c, double uc, const double2* r1, const double2* r2,
+                                double* red) {
+  const int dm = P.dm;
+  const size_t dd = (size_t)dm * dm;
+  double im = 0.0;
+  for (int e = threadIdx.x; e < dm * dm; e += BT) {
+    const int i = e % dm, j = e / dm;  // (dH r2)(i, j)
+    double2 acc = cx(0.0, 0.0);
+    for (int k = 0; k < dm; ++k) {
+      double2 a = P.lin[((size_t)b * P.C + c) * dd + (size_t)i * dm + k];
+      if (P.has_quad) {
+        const double2 q = P.quad[((size_t)b * P.C + c) * dd + (size_t)i * dm + k];
+        a = cx(fma(uc, q.x, a.x), fma(uc, q.y, a.y));
+      }
+      acc = cfma(a, r2[k + j * dm], acc);
+    }
+    im += cconjmul(r1[e], acc).y;  // tr(r1^dag Y) = sum conj(r1_ij) Y_ij
+  }
+  return block_sum(im, red);
+}
+
+__global__ void __launch_bounds__(BT) density_task_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = blockIdx.x, b = blockIdx.y;
+  if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
+  DensSmem D = carve_dens(smem_raw, P.dm);
+  const int dm = P.dm, sl = P.d, C = P.C, mode = A.mode;
+  const int node0 = P.node[n], len = P.node[n + 1] - node0;
+  const double Kd = (double)P.K, weight = A.weighted ? Kd / (double)len : 1.0, scale = (double)len / Kd;
+  const double dt = P.dt, w = P.ip_w;
+  double* u = R.u + ((size_t)b * P.K + node0) * C;
+  double2* traj = R.traj + ((size_t)b * P.L + n) * (size_t)R.traj_len * sl;
+  const size_t tix = ((size_t)b * P.L + n) * sl;
+  const double2* init = R.task_init + tix;
+  const double2* targ = R.task_targ + tix;
+  double* red = D.lin.red;
+
+  if (mode & (M_ENTRY | M_UPDATE | M_FINAL | M_GRAD)) {
+    const bool need_traj = (mode & (M_UPDATE | M_GRAD)) != 0;
+    const int iters = (mode & M_UPDATE) ? A.inner : 1;
+    for (int it = 0; it < iters; ++it) {
+      dens_copy(sl, init, D.S);
+      if (need_traj) dens_copy(sl, D.S, traj);
+      double pen = 0.0;
+      for (int j = 0; j < len; ++j) {
+        const double* uj = u + (size_t)j * C;
+        dens_inverse(P, b, uj, D);
+        dens_forward(dm, D, D.S);
+        if (need_traj) dens_copy(sl, D.S, traj + (size_t)(j + 1) * sl);
+        double sq = 0.0;
+        for (int c = 0; c < C; ++c) sq += uj[c] * uj[c];
+        pen += (P.alpha[node0 + j] * scale) * sq;
+      }
+      if (it == 0 && (mode & M_ENTRY)) {
+        double t = 0.0;
+        for (int i = threadIdx.x; i < sl; i += BT)
+          t += A.form == 0 ? cconjmul(targ[i], D.S[i]).x : cabs2(csub(D.S[i], targ[i]));
+        t = block_sum(t, red);
+        const double payoff = A.form == 0 ? (w * t) : (-0.5 * (w * t));
+        if (threadIdx.x == 0) R.entry[(size_t)b * P.L + n] = weight * (payoff - 0.5 * dt * pen);
+      }
+      if (it == 0 && (mode & M_FINAL)) dens_copy(sl, D.S, R.psi_end + tix);
+      if (mode & (M_UPDATE | M_GRAD)) {
+        for (int i = threadIdx.x; i < sl; i += BT) D.X[i] = A.form == 0 ? targ[i] : csub(targ[i], D.S[i]);
+        __syncthreads();
+        for (int j = len - 1; j >= 0; --j) {
+          const double* uj = u + (size_t)j * C;
+          dens_inverse(P, b, uj, D);
+          mm(dm, D.W, ROW_H, D.X, COL, 1.0, nullptr, 0.0, D.T);                          // r1 = W^dag X
+          mm(dm, D.W, ROW_H, traj + (size_t)(j + 1) * sl, COL, 1.0, nullptr, 0.0, D.S);  // r2 = W^dag rho_{j+1}
+          const double aj = P.alpha[node0 + j] * scale;
+          for (int c = 0; c < C; ++c) {
+            const double uc = uj[c];
+            const double im = dens_trace_im(P, b, c, uc, D.T, D.S, red);
+            const double gc = -aj * dt * uc + 2.0 * dt * im;
+            if (threadIdx.x == 0) {
+              if (mode & M_GRAD) R.grad[((size_t)b * P.K + node0 + j) * C + c] = gc;
+              if (mode & M_UPDATE) u[(size_t)j * C + c] = uc + A.rho * (weight * gc);
+            }
+            __syncthreads();
+          }
+          for (int i = threadIdx.x; i < sl; i += BT)  // b = 2 r1 - X
+            D.G[i] = cx(2.0 * D.T[i].x - D.X[i].x, 2.0 * D.T[i].y - D.X[i].y);
+          __syncthreads();
+          mm(dm, D.G, COL, D.W, ROW, 2.0, D.G, -1.0, D.X);  // X_j = 2 b W - b
+        }
+      }
+    }
+  }
+
+  const bool do_err = (mode & M_ERROR) != 0, do_asm = (mode & M_ASSEMBLE) != 0, do_lag = (mode & M_LAGGED) != 0;
+  if (do_asm) {  // product of the one-step A's (row-major dm x dm; assemble_propagator, 236-249)
+    for (int e = threadIdx.x; e < dm * dm; e += BT) D.S[e] = cx((e / dm) == (e % dm) ? 1.0 : 0.0, 0.0);
+    __syncthreads();
+    for (int j = 0; j < len; ++j) {
+      dens_inverse(P, b, u + (size_t)j * C, D);
+      // S (row-major) <- 2 W S - S  : via column-major views of the transposes
+      mm(dm, D.S, COL, D.W, COL, 2.0, D.S, -1.0, D.T);  // (2 W S - S)^T = 2 S^T W^T - S^T as column-major
+      dens_copy(dm * dm, D.T, D.S);
+    }
+    for (int e = threadIdx.x; e < dm * dm; e += BT) R.prop[((size_t)b * P.L + n) * (size_t)dm * dm + e] = D.S[e];
+  }
+  if (do_err || do_lag) {
+    // residual: forward at the updated control (trajectory), then the adjoint with its gradient
+    if (do_err) {
+      dens_copy(sl, init, D.S);
+      dens_copy(sl, D.S, traj);
+      for (int j = 0; j < len; ++j) {
+        dens_inverse(P, b, u + (size_t)j * C, D);
+        dens_forward(dm, D, D.S);
+        dens_copy(sl, D.S, traj + (size_t)(j + 1) * sl);
+      }
+      for (int i = threadIdx.x; i < sl; i += BT) D.X[i] = A.form == 0 ? targ[i] : csub(targ[i], D.S[i]);
+      __syncthreads();
+      double err = 0.0;
+      for (int j = len - 1; j >= 0; --j) {
+        const double* uj = u + (size_t)j * C;
+        dens_inverse(P, b, uj, D);
+        mm(dm, D.W, ROW_H, D.X, COL, 1.0, nullptr, 0.0, D.T);
+        mm(dm, D.W, ROW_H, traj + (size_t)(j + 1) * sl, COL, 1.0, nullptr, 0.0, D.S);
+        const double aj = P.alpha[node0 + j] * scale;
+        double sq = 0.0;
+        for (int c = 0; c < C; ++c) {
+          const double uc = uj[c];
+          const double gc = -aj * dt * uc + 2.0 * dt * dens_trace_im(P, b, c, uc, D.T, D.S, red);
+          sq += gc * gc;
+        }
+        err += sqrt(sq);
+        for (int i = threadIdx.x; i < sl; i += BT) D.G[i] = cx(2.0 * D.T[i].x - D.X[i].x, 2.0 * D.T[i].y - D.X[i].y);
+        __syncthreads();
+        mm(dm, D.G, COL, D.W, ROW, 2.0, D.G, -1.0, D.X);
+      }
+      if (threadIdx.x == 0) R.err[(size_t)b * P.L + n] = err;
+    }
+    if (do_lag) {  // lagged boundary refresh (ism.cpp:424-459)
+      dens_copy(sl, R.psi_nodes + ((size_t)b * (P.L + 1) + n) * sl, D.S);
+      for (int j = 0; j < len; ++j) {
+        dens_inverse(P, b, u + (size_t)j * C, D);
+        dens_forward(dm, D, D.S);
+      }
+      dens_copy(sl, D.S, R.psi_end + tix);
+      dens_copy(sl, R.chi_nodes + ((size_t)b * (P.L + 1) + n + 1) * sl, D.X);
+      for (int j = len - 1; j >= 0; --j) {
+        dens_inverse(P, b, u + (size_t)j * C, D);
+        dens_adjoint(dm, D, D.X);
+      }
+      dens_copy(sl, D.X, R.chi_start + tix);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(BT) density_horizon_kernel(DevProblem P, DevRun R, int which, int k) {
+  if (R.kdev) k = *R.kdev;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int b = blockIdx.x;
+  if (R.done[b] || R.status[b]) return;
+  DensSmem D = carve_dens(smem_raw, P.dm);
+  const int dm = P.dm, sl = P.d, C = P.C;
+  const double* u = R.u + (size_t)b * P.K * C;
+  const size_t nb = (size_t)b * (P.L + 1) * sl;
+  dens_copy(sl, P.init + (size_t)b * sl, D.S);
+  if (which == 0) dens_copy(sl, D.S, R.psi_nodes + nb);
+  int nxt = 1;
+  for (int j = 0; j < P.K; ++j) {
+    dens_inverse(P, b, u + (size_t)j * C, D);
+    dens_forward(dm, D, D.S);
+    if (which == 0 && nxt <= P.L && P.node[nxt] == j + 1) {
+      dens_copy(sl, D.S, R.psi_nodes + nb + (size_t)nxt * sl);
+      ++nxt;
+    }
+  }
+  if (which == 1) {
+    double t = 0.0;
+    for (int i = threadIdx.x; i < sl; i += BT) t += cconjmul(P.targ[(size_t)b * sl + i], D.S[i]).x;
+    t = block_sum(t, D.lin.red);
+    if (threadIdx.x == 0) {
+      double pen = 0.0;
+      for (int n = 0; n < P.L; ++n) pen += R.pen[(size_t)b * P.L + n];
+      R.rec_exact[(size_t)b * R.cap + k] = P.ip_w * t - 0.5 * P.dt * pen;
+    }
+    return;
+  }
+  dens_copy(sl, P.targ + (size_t)b * sl, D.X);
+  dens_copy(sl, D.X, R.chi_nodes + nb + (size_t)P.L * sl);
+  int prev = P.L - 1;
+  for (int j = P.K - 1; j >= 0; --j) {
+    dens_inverse(P, b, u + (size_t)j * C, D);
+    dens_adjoint(dm, D, D.X);
+    if (prev >= 0 && P.node[prev] == j) {
+      dens_copy(sl, D.X, R.chi_nodes + nb + (size_t)prev * sl);
+      --prev;
+    }
+  }
+}
+
 }  // namespace
 
 bool dense_big_supported(int d) { return d > 32 && d <= BIG_MAX; }
@@ -437,6 +721,29 @@ cudaError_t dense_big_horizon(const DevProblem& P, const DevRun& R, int which, i
       cudaFuncSetAttribute(dense_big_horizon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dense_big_horizon_kernel<<<P.B, BT, smem, st>>>(P, R, which, k);
+  return cudaGetLastError();
+}
+
+}  // namespace qoc
+
+namespace qoc {
+
+bool density_supported(int dm) { return dm >= 1 && dm <= DENS_MAX; }
+
+cudaError_t density_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
+  const size_t smem = dens_smem(P.dm);
+  cudaError_t e = cudaFuncSetAttribute(density_task_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  density_task_kernel<<<dim3(P.L, P.B), BT, smem, st>>>(P, R, A, ignore_done);
+  return cudaGetLastError();
+}
+
+cudaError_t density_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
+  const size_t smem = dens_smem(P.dm);
+  cudaError_t e =
+      cudaFuncSetAttribute(density_horizon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  density_horizon_kernel<<<P.B, BT, smem, st>>>(P, R, which, k);
   return cudaGetLastError();
 }
 

@@ -170,9 +170,11 @@ void validate_problem(const qoc_problem_v1* p) {
   if (p->dim < 1 || p->channels < 1 || p->steps < 1 || p->batch < 1)
     fail(QOC_EINVAL, "dim, channels, steps and batch must be positive");
   if (!(p->dt > 0.0)) fail(QOC_EINVAL, "TimeGrid: dt must be positive");
-  if (p->channels > QOC_MAX_CHANNELS || (p->kind == QOC_KIND_BITFLIP && p->channels > 4))
+  const int cmax = p->kind == QOC_KIND_DENSITY ? QOC_MAX_DENSITY_CHANNELS
+                                                 : (p->kind == QOC_KIND_BITFLIP ? 4 : QOC_MAX_CHANNELS);
+  if (p->channels > cmax)
     fail(QOC_ELOGIC, "control channel count above what the device kernels carry (QOC_MAX_CHANNELS; 4 for the "
-                     "bit-flip kind)");
+                     "bit-flip kind, QOC_MAX_DENSITY_CHANNELS for the density kind)");
   if (!p->initial || !p->target) fail(QOC_EINVAL, "initial and target states are required");
 }
 
@@ -227,13 +229,21 @@ void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaS
   P.L = static_cast<int>(node.size()) - 1;
   P.dt = p->dt;
   P.ip_w = p->ip_weight;
+  P.dm = d;
   out.stride = d;
   switch (p->kind) {
+    case QOC_KIND_DENSITY:
     case QOC_KIND_DENSE: {
       if (!p->h0 || !p->linear) fail(QOC_EINVAL, "dense model needs h0 and linear operators");
-      if (dense_pad(d) < 0 && !dense_big_supported(d))
-        fail(QOC_ELOGIC, "dense device kernels support d <= 64; use a structured kind");
-      out.stride = dense_pad(d) > 0 ? dense_pad(d) : d;
+      if (p->kind == QOC_KIND_DENSITY) {
+        if (!density_supported(d)) fail(QOC_ELOGIC, "density-matrix device kernels support d <= 32");
+        P.d = d * d;  // the state is the d x d matrix (column-major)
+        out.stride = d * d;
+      } else {
+        if (dense_pad(d) < 0 && !dense_big_supported(d))
+          fail(QOC_ELOGIC, "dense device kernels support d <= 64; use a structured kind");
+        out.stride = dense_pad(d) > 0 ? dense_pad(d) : d;
+      }
       const size_t dd = (size_t)d * d;
       P.has_quad = p->quadratic != nullptr;
       const int nq = P.has_quad ? C : 0;
@@ -337,8 +347,8 @@ void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaS
     default:
       fail(QOC_EINVAL, "unknown model kind");
   }
-  P.init = out.put<double2>(reinterpret_cast<const double2*>(p->initial), (size_t)B * d);
-  P.targ = out.put<double2>(reinterpret_cast<const double2*>(p->target), (size_t)B * d);
+  P.init = out.put<double2>(reinterpret_cast<const double2*>(p->initial), (size_t)B * P.d);  // state length
+  P.targ = out.put<double2>(reinterpret_cast<const double2*>(p->target), (size_t)B * P.d);
   std::vector<double> alpha(K, 0.0);
   if (p->penalty) alpha.assign(p->penalty, p->penalty + K);
   P.alpha = out.put<double>(alpha.data(), alpha.size());
@@ -465,6 +475,7 @@ cudaError_t task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ig
     case QOC_KIND_TRIDIAG: return tridiag_task(P, R, A, ignore_done, st);
     case QOC_KIND_BITFLIP: return bitflip_task(P, R, A, ignore_done, st);
     case QOC_KIND_STRANG: return strang_task(P, R, A, ignore_done, st);
+    case QOC_KIND_DENSITY: return density_task(P, R, A, ignore_done, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -475,6 +486,7 @@ cudaError_t horizon(const DevProblem& P, const DevRun& R, int which, int k, cuda
     case QOC_KIND_TRIDIAG: return tridiag_horizon(P, R, which, k, st);
     case QOC_KIND_BITFLIP: return bitflip_horizon(P, R, which, k, st);
     case QOC_KIND_STRANG: return strang_horizon(P, R, which, k, st);
+    case QOC_KIND_DENSITY: return density_horizon(P, R, which, k, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -685,7 +697,7 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
     // The bit-flip kind never forms its d x d one-step matrices (16 MB each at d = 1024): its
     // boundary refresh always runs as direct node sweeps, which agree with the assembled
     // chain to rounding (ism_test.cpp:248-265).
-    const bool direct = cfg->plan == QOC_PLAN_DIRECT || p->kind == QOC_KIND_BITFLIP;
+    const bool direct = cfg->plan == QOC_PLAN_DIRECT || p->kind == QOC_KIND_BITFLIP || p->kind == QOC_KIND_DENSITY;
     const bool assembled_interp = L > 1 && !split && !direct;
     cudaStream_t st = ctx->stream;
     Launcher launch{ctx};
@@ -1023,7 +1035,7 @@ int32_t qoc_propagate_final(qoc_ctx* ctx, const qoc_problem_v1* p, const double*
     DeviceRun dr;
     dr.slots = fresh_slots(ctx->run_slots);
     single_run(ctx, p, u, M_FINAL, QOC_FORM_OVERLAP, false, false, dp, dr);
-    ck(cudaMemcpy(states_out, dr.R.psi_end, sizeof(double2) * p->batch * p->dim, cudaMemcpyDeviceToHost), "out");
+    ck(cudaMemcpy(states_out, dr.R.psi_end, sizeof(double2) * p->batch * dp.P.d, cudaMemcpyDeviceToHost), "out");
   });
 }
 

@@ -15,6 +15,11 @@ bool dense_big_supported(int d);
 cudaError_t dense_big_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
 cudaError_t dense_big_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st);
 
+// density-matrix conjugation kind, dm <= 32 (CTA per task, dense_big.cu)
+bool density_supported(int dm);
+cudaError_t density_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
+cudaError_t density_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st);
+
 // tridiagonal (d <= 32)
 cudaError_t tridiag_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
 cudaError_t tridiag_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st);

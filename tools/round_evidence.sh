@@ -10,6 +10,7 @@ set -u
 out=gpurun_out/${1:-evidence}
 shift || true
 sections=${*:-"bench ncu sanitize"}
+# (gpurun copies back at most 64 MiB of gpurun_out/: run the ncu section in its own call)
 mkdir -p "$out"
 nproc > "$out/nproc.txt"; lscpu > "$out/lscpu.txt" 2>&1
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > "$out/gpu.txt" 2>&1
@@ -24,16 +25,16 @@ fi
 if [[ " $sections " == *" ncu "* ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file "$out/launches_default.csv" \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-ttf > "$out/ncu_launch.log" 2>&1; echo "launches rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:dense_nm_assemble|dense_pc_eval16" -c 3 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:dense_nm_assemble|dense_pc_eval16" -c 2 \
     -o "$out/full_batch4096" python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-ttf > "$out/ncu_full_batch.log" 2>&1
   echo "full batch rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:bitflip_horizon_cluster|bitflip_task" -c 2 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:bitflip_horizon_cluster" -c 1 \
     -o "$out/full_ising10" python bench.py --workload ising10 --steps 1 --warmup 3 --no-cpu-baseline --no-ttf \
     > "$out/ncu_full_ising.log" 2>&1; echo "full ising rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:strang_task" -c 2 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:strang_task" -c 1 \
     -o "$out/full_gpe1024" python bench.py --workload gpe1024 --steps 1 --warmup 3 --no-cpu-baseline --no-ttf \
     > "$out/ncu_full_gpe.log" 2>&1; echo "full gpe rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:tri_pc_assemble|pc_eval|chain_small" -c 3 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:tri_pc_assemble" -c 1 \
     -o "$out/full_rotor21" python bench.py --workload rotor21 --steps 1 --warmup 3 --no-cpu-baseline --no-ttf \
     > "$out/ncu_full_rotor.log" 2>&1; echo "full rotor rc=$?"
 fi
