@@ -145,17 +145,34 @@ class IterationStat:
         return self.device_seconds
 
 
-@dataclass
 class RunRecord:
-    """runtime.hpp:65-75."""
-    subintervals: int = 1
-    workers: int = 1
-    solver: str = "gradient"
-    variant: str = "interpolated"
-    plan: str = "assembled"
-    iterations: list = field(default_factory=list)
-    aborted: bool = False
-    abort_reason: str = ""
+    """runtime.hpp:65-75.  Records returned by a device run keep their per-iteration arrays and
+    build the IterationStat list on first access of `iterations` (a 4096-problem batch returns
+    ~10^5 of them; the e2e path should not pay for objects nobody reads)."""
+
+    def __init__(self, subintervals: int = 1, workers: int = 1, solver: str = "gradient",
+                 variant: str = "interpolated", plan: str = "assembled", iterations=None,
+                 aborted: bool = False, abort_reason: str = ""):
+        self.subintervals, self.workers, self.solver = subintervals, workers, solver
+        self.variant, self.plan = variant, plan
+        self.aborted, self.abort_reason = aborted, abort_reason
+        self._iterations = list(iterations) if iterations is not None else []
+        self._build = None
+
+    @property
+    def iterations(self) -> list:
+        if self._build is not None:
+            self._iterations, self._build = self._build(), None
+        return self._iterations
+
+    @iterations.setter
+    def iterations(self, value) -> None:
+        self._iterations, self._build = list(value), None
+
+    def __repr__(self) -> str:
+        return (f"RunRecord(subintervals={self.subintervals}, workers={self.workers}, solver={self.solver!r}, "
+                f"variant={self.variant!r}, plan={self.plan!r}, iterations=<{len(self.iterations)}>, "
+                f"aborted={self.aborted}, abort_reason={self.abort_reason!r})")
 
     def objectives(self) -> np.ndarray:
         return np.array([it.objective for it in self.iterations])
@@ -284,31 +301,32 @@ def unpack_records(recs: np.ndarray, tvals: np.ndarray, status, cfg: IsmConfig,
 
 def unpack_all(recs: np.ndarray, tvals: np.ndarray, status, cfg: IsmConfig, solver: SolverSpec,
                task_value_lists: bool = True) -> list:
-    """RunRecords of every batch member (fields converted once for the whole batch).  With
-    task_value_lists=False each IterationStat.task_values is a read-only row view of `tvals`
-    (no per-value Python objects: the batched device path returns 4096 x iterations x L of them)."""
-    cols = {f: recs[f].tolist() for f in ("iteration", "objective", "exact_objective", "error",
-                                           "device_seconds", "has_exact_objective", "has_error")}
-    if task_value_lists:
-        tv = tvals.tolist()
-    else:
+    """RunRecords of every batch member.  With task_value_lists=False each IterationStat.task_values
+    is a read-only row view of `tvals`; the IterationStat objects are built lazily per record."""
+    if not task_value_lists:
         tvals.setflags(write=False)
-        tv = tvals
+
+    def builder(b: int, n: int, aborted: bool, reason: str):
+        def build():
+            rb = recs[b, :n]
+            it_, obj, ex = rb["iteration"].tolist(), rb["objective"].tolist(), rb["exact_objective"].tolist()
+            er, sec = rb["error"].tolist(), rb["device_seconds"].tolist()
+            hx, he = rb["has_exact_objective"].tolist(), rb["has_error"].tolist()
+            tv = tvals[b, :n].tolist() if task_value_lists else tvals[b]
+            its = [IterationStat(iteration=it_[k], objective=obj[k], exact_objective=ex[k] if hx[k] else None,
+                                 error=er[k] if he[k] else None, task_values=tv[k], device_seconds=sec[k])
+                   for k in range(n)]
+            if aborted and its:  # the stopping iteration carries the reason
+                its[-1].events.append(reason)
+            return its
+        return build
+
     out = []
     for b, st in enumerate(status):
-        n = st.iterations_recorded
         rec = RunRecord(subintervals=cfg.subintervals, workers=cfg.workers, solver=solver.kind,
                         variant=cfg.variant, plan=cfg.plan, aborted=bool(st.aborted),
                         abort_reason=st.abort_reason.decode())
-        it_, obj, ex, er, sec = (cols["iteration"][b], cols["objective"][b], cols["exact_objective"][b],
-                                 cols["error"][b], cols["device_seconds"][b])
-        hx, he, tvb = cols["has_exact_objective"][b], cols["has_error"][b], tv[b]
-        rec.iterations = [IterationStat(iteration=it_[k], objective=obj[k],
-                                        exact_objective=ex[k] if hx[k] else None,
-                                        error=er[k] if he[k] else None, task_values=tvb[k],
-                                        device_seconds=sec[k]) for k in range(n)]
-        if rec.aborted and rec.iterations:  # the stopping iteration carries the reason
-            rec.iterations[-1].events.append(rec.abort_reason)
+        rec._build = builder(b, st.iterations_recorded, rec.aborted, rec.abort_reason)
         out.append(rec)
     return out
 
