@@ -26,8 +26,9 @@ namespace {
 
 __device__ __forceinline__ double2 flip_coef(double2 ab, int one) { return cx(ab.x, one ? ab.y : -ab.y); }
 
-template <int LOG2E, int LOG2T, int LOG2CL, bool PUSH>
+template <int LOG2E, int LOG2T, int LOG2CL, int MODE>
 __global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_cluster_kernel(DevProblem P, DevRun R, int which, int k) {
+  constexpr bool PUSH = MODE >= 1, ASYNC = MODE == 2;
   constexpr int E = 1 << LOG2E, T = 1 << LOG2T, CL = 1 << LOG2CL, Dl = E * T, N = LOG2E + LOG2T + LOG2CL;
   if (R.kdev) k = *R.kdev;
   cg::cluster_group cluster = cg::this_cluster();
@@ -39,6 +40,7 @@ __global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_cluster_kernel(Dev
   // PUSH: partner rb's amplitudes of the current sweep, written by the partner (remote stores
   // before the barrier, local loads after it) instead of loaded remotely after the barrier
   __shared__ __align__(16) double2 inbox[PUSH ? 2 : 1][PUSH ? (LOG2CL > 0 ? LOG2CL : 1) : 1][PUSH ? Dl : 1];
+  __shared__ __align__(8) unsigned long long mbar[2];  // ASYNC: inbox arrival per buffer parity
   __shared__ double2 sa[2][N];
   __shared__ int ssw[2];
   __shared__ double red[T / 32 + 1];
@@ -59,6 +61,24 @@ __global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_cluster_kernel(Dev
     rem[rb] = cluster.map_shared_rank(&buf[0][0], rank ^ (1 << rb));
     if constexpr (PUSH) outbox[rb] = cluster.map_shared_rank(&inbox[0][rb][0], rank ^ (1 << rb));
   }
+  // ASYNC: shared::cluster addresses of my slot in each partner's inbox and of its barriers
+  unsigned r_inbox[LOG2CL > 0 ? LOG2CL : 1], r_bar[LOG2CL > 0 ? LOG2CL : 1][2];
+  if constexpr (ASYNC) {
+    if (t == 0) {
+      mbar_init(&mbar[0], 1);
+      mbar_init(&mbar[1], 1);
+      mbar_init_fence();
+    }
+#pragma unroll
+    for (int rb = 0; rb < LOG2CL; ++rb) {
+      const unsigned peer = (unsigned)(rank ^ (1 << rb));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r_inbox[rb]) : "r"(smem_addr(&inbox[0][rb][0])), "r"(peer));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r_bar[rb][0]) : "r"(smem_addr(&mbar[0])), "r"(peer));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r_bar[rb][1]) : "r"(smem_addr(&mbar[1])), "r"(peer));
+    }
+    cluster.sync();  // every barrier is initialised before any peer signals it
+  }
+  unsigned phase[2] = {0u, 0u};
   double2 cl[LOG2T > 0 ? LOG2T : 1], ch[LOG2E > 0 ? LOG2E : 1], cr[LOG2CL > 0 ? LOG2CL : 1];
   int par = 0, spar = 0;
   bool ok = true;
@@ -108,20 +128,38 @@ __global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_cluster_kernel(Dev
       par ^= 1;
 #pragma unroll
       for (int e = 0; e < E; ++e) buf[par][t + e * T] = z[e];
-      if constexpr (PUSH) {
+      if constexpr (ASYNC) {
+        // asynchronous remote stores that complete on the partner's barrier: no cluster-wide
+        // release fence (a GPU-scope MEMBAR per sweep with the cluster barrier)
+#pragma unroll
+        for (int rb = 0; rb < LOG2CL; ++rb)
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const unsigned dst = r_inbox[rb] + (unsigned)sizeof(double2) * (unsigned)(par * LOG2CL * Dl + t + e * T);
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(dst),
+                         "d"(z[e].x), "d"(z[e].y), "r"(r_bar[rb][par])
+                         : "memory");
+          }
+        if (t == 0) mbar_expect_tx(&mbar[par], (unsigned)(LOG2CL * Dl * sizeof(double2)));
+        __syncthreads();  // the CTA-local publish
+      } else if constexpr (PUSH) {
 #pragma unroll
         for (int rb = 0; rb < LOG2CL; ++rb)
 #pragma unroll
           for (int e = 0; e < E; ++e) outbox[rb][par * LOG2CL * Dl + t + e * T] = z[e];
+        cluster.sync();  // every CTA's publish of this sweep is visible cluster-wide
+      } else {
+        cluster.sync();
       }
-      cluster.sync();  // every CTA's publish of this sweep is visible cluster-wide
 #pragma unroll
       for (int e = 0; e < E; ++e) vv[e] = cx(0.0, 0.0);
+      if constexpr (!ASYNC) {
 #pragma unroll
-      for (int rb = 0; rb < LOG2CL; ++rb) {
-        const double2* rbuf = PUSH ? &inbox[par][rb][0] : rem[rb] + par * Dl;
+        for (int rb = 0; rb < LOG2CL; ++rb) {
+          const double2* rbuf = PUSH ? &inbox[par][rb][0] : rem[rb] + par * Dl;
 #pragma unroll
-        for (int e = 0; e < E; ++e) vv[e] = cfma(cr[rb], rbuf[t + e * T], vv[e]);
+          for (int e = 0; e < E; ++e) vv[e] = cfma(cr[rb], rbuf[t + e * T], vv[e]);
+        }
       }
 #pragma unroll
       for (int hb = 0; hb < LOG2E; ++hb)
@@ -131,6 +169,14 @@ __global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_cluster_kernel(Dev
       for (int bb = 0; bb < LOG2T; ++bb)
 #pragma unroll
         for (int e = 0; e < E; ++e) vv[e] = cfma(cl[bb], buf[par][(t ^ (1 << bb)) + e * T], vv[e]);
+      if constexpr (ASYNC) {  // the partners' amplitudes of this sweep have landed
+        mbar_wait(&mbar[par], phase[par]);
+        phase[par] ^= 1u;
+#pragma unroll
+        for (int rb = 0; rb < LOG2CL; ++rb)
+#pragma unroll
+          for (int e = 0; e < E; ++e) vv[e] = cfma(cr[rb], inbox[par][rb][t + e * T], vv[e]);
+      }
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const double2 tt = cx(x[e].x + sh * vv[e].y, x[e].y - sh * vv[e].x);  // x - s V z
@@ -203,9 +249,9 @@ __global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_cluster_kernel(Dev
   cluster.sync();  // no CTA leaves while a peer may still read its shared memory
 }
 
-template <int LOG2E, int LOG2T, int LOG2CL, bool PUSH = false>
+template <int LOG2E, int LOG2T, int LOG2CL, int MODE = 0>
 cudaError_t launch_cluster(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
-  auto kern = bitflip_horizon_cluster_kernel<LOG2E, LOG2T, LOG2CL, PUSH>;
+  auto kern = bitflip_horizon_cluster_kernel<LOG2E, LOG2T, LOG2CL, MODE>;
   constexpr int CL = 1 << LOG2CL;
   if (CL > 8) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -229,26 +275,32 @@ cudaError_t launch_cluster(const DevProblem& P, const DevRun& R, int which, int 
 }  // namespace
 
 // QOC_BF_CLUSTER selects the cluster shape for d = 1024 node sweeps ("0" keeps the single-CTA
-// kernel): "8x1" = 8 CTAs x 128 threads x 1 amplitude, "8x2" = 8 x 64 x 2,
-// "16x1" = 16 x 64 x 1 (non-portable cluster size); "8p" / "8q" = 8x1 / 8x2 with the partner
-// amplitudes pushed (remote stores) instead of pulled, "4p" = 4 x 128 x 2 (default), "2p" = 2 x 128 x 4.
-// Measured per config-3 outer iteration (node sweeps): single CTA 22.8 ms, 8x1 21.2, 8p 20.1,
-// 4p 20.0, 2p 20.1, 8x2 34.8, 16x1 29.8 -- the per-sweep floor is the exchange + barrier
-// latency of a dependent chain (~1,200 cycles), not the arithmetic.
+// kernel).  "8a" (default): 8 CTAs x 128 threads x 1 amplitude, partner amplitudes pushed with
+// st.async onto the partner's mbarrier (no cluster barrier, so no GPU-scope MEMBAR per sweep);
+// "4a" / "2a" / "8b" / "16a": 4 x 128 x 2, 2 x 128 x 4, 8 x 64 x 2, 16 x 64 x 1 of the same.
+// Barrier-synchronised variants: "8x1" pull, "8p" push (8 x 128 x 1), "8q" / "4p" / "2p" push
+// with 2 / 2 / 4 amplitudes, "8x2", "16x1".  Measured per config-3 outer iteration (node
+// sweeps): single CTA 22.8 ms; barrier variants 20.0-21.2 ms (MEMBAR.ALL.GPU per cluster
+// barrier); 8a 13.8 ms, 2a 16.4, 8b 19.4, 4a 19.7.
 cudaError_t bitflip_horizon_cluster(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st,
                                     bool* used) {
   *used = false;
   if (P.nspins != 10 || P.C > 4) return cudaSuccess;
   const char* e = std::getenv("QOC_BF_CLUSTER");
-  const char* shape = e ? e : "4p";
+  const char* shape = e ? e : "8a";
   if (shape[0] == '0') return cudaSuccess;
   cudaError_t r;
-  if (shape[0] == '1' && shape[1] == '6') r = launch_cluster<0, 6, 4>(P, R, which, k, st);
+  if (shape[0] == '1' && shape[1] == '6' && shape[2] != 'a') r = launch_cluster<0, 6, 4>(P, R, which, k, st);
   else if (shape[2] == '2') r = launch_cluster<1, 6, 3>(P, R, which, k, st);
-  else if (shape[1] == 'p') r = launch_cluster<0, 7, 3, true>(P, R, which, k, st);
-  else if (shape[1] == 'q') r = launch_cluster<1, 6, 3, true>(P, R, which, k, st);
-  else if (shape[0] == '4') r = launch_cluster<1, 7, 2, true>(P, R, which, k, st);
-  else if (shape[0] == '2') r = launch_cluster<2, 7, 1, true>(P, R, which, k, st);
+  else if (shape[0] == '8' && shape[1] == 'a') r = launch_cluster<0, 7, 3, 2>(P, R, which, k, st);
+  else if (shape[0] == '1' && shape[1] == '6' && shape[2] == 'a') r = launch_cluster<0, 6, 4, 2>(P, R, which, k, st);
+  else if (shape[0] == '4' && shape[1] == 'a') r = launch_cluster<1, 7, 2, 2>(P, R, which, k, st);
+  else if (shape[0] == '2' && shape[1] == 'a') r = launch_cluster<2, 7, 1, 2>(P, R, which, k, st);
+  else if (shape[0] == '8' && shape[1] == 'b') r = launch_cluster<1, 6, 3, 2>(P, R, which, k, st);
+  else if (shape[1] == 'p') r = launch_cluster<0, 7, 3, 1>(P, R, which, k, st);
+  else if (shape[1] == 'q') r = launch_cluster<1, 6, 3, 1>(P, R, which, k, st);
+  else if (shape[0] == '4') r = launch_cluster<1, 7, 2, 1>(P, R, which, k, st);
+  else if (shape[0] == '2') r = launch_cluster<2, 7, 1, 1>(P, R, which, k, st);
   else r = launch_cluster<0, 7, 3>(P, R, which, k, st);
   *used = r == cudaSuccess;
   if (r != cudaSuccess) cudaGetLastError();  // e.g. no cluster support: fall back
