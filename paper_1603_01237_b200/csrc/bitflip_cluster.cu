@@ -275,19 +275,20 @@ cudaError_t launch_cluster(const DevProblem& P, const DevRun& R, int which, int 
 }  // namespace
 
 // QOC_BF_CLUSTER selects the cluster shape for d = 1024 node sweeps ("0" keeps the single-CTA
-// kernel).  "8a" (default): 8 CTAs x 128 threads x 1 amplitude, partner amplitudes pushed with
+// kernel).  "16a" (default; 8a where 16-CTA clusters cannot launch): 16 CTAs x 64 threads x 1
+// amplitude; "8a": 8 CTAs x 128 threads x 1 amplitude, partner amplitudes pushed with
 // st.async onto the partner's mbarrier (no cluster barrier, so no GPU-scope MEMBAR per sweep);
 // "4a" / "2a" / "8b" / "16a": 4 x 128 x 2, 2 x 128 x 4, 8 x 64 x 2, 16 x 64 x 1 of the same.
 // Barrier-synchronised variants: "8x1" pull, "8p" push (8 x 128 x 1), "8q" / "4p" / "2p" push
 // with 2 / 2 / 4 amplitudes, "8x2", "16x1".  Measured per config-3 outer iteration (node
 // sweeps): single CTA 22.8 ms; barrier variants 20.0-21.2 ms (MEMBAR.ALL.GPU per cluster
-// barrier); 8a 13.8 ms, 2a 16.4, 8b 19.4, 4a 19.7.
+// barrier); 16a 13.1 ms, 8a 13.8, 2a 16.4, 8b 19.4, 4a 19.7.
 cudaError_t bitflip_horizon_cluster(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st,
                                     bool* used) {
   *used = false;
   if (P.nspins != 10 || P.C > 4) return cudaSuccess;
   const char* e = std::getenv("QOC_BF_CLUSTER");
-  const char* shape = e ? e : "8a";
+  const char* shape = e ? e : "16a";
   if (shape[0] == '0') return cudaSuccess;
   cudaError_t r;
   if (shape[0] == '1' && shape[1] == '6' && shape[2] != 'a') r = launch_cluster<0, 6, 4>(P, R, which, k, st);
@@ -302,8 +303,12 @@ cudaError_t bitflip_horizon_cluster(const DevProblem& P, const DevRun& R, int wh
   else if (shape[0] == '4') r = launch_cluster<1, 7, 2, 1>(P, R, which, k, st);
   else if (shape[0] == '2') r = launch_cluster<2, 7, 1, 1>(P, R, which, k, st);
   else r = launch_cluster<0, 7, 3>(P, R, which, k, st);
+  if (r != cudaSuccess && !e) {  // 16-CTA clusters are non-portable: fall back to 8
+    cudaGetLastError();
+    r = launch_cluster<0, 7, 3, 2>(P, R, which, k, st);
+  }
   *used = r == cudaSuccess;
-  if (r != cudaSuccess) cudaGetLastError();  // e.g. no cluster support: fall back
+  if (r != cudaSuccess) cudaGetLastError();  // e.g. no cluster support: the single-CTA kernel
   return cudaSuccess;
 }
 
