@@ -42,9 +42,13 @@ def _stale_obj(src: Path, hdr_mtime: float) -> bool:
 def stale() -> bool:
     if not OUT.exists():
         return True
+    # per object (a source edited while an earlier build was compiling it leaves an object
+    # older than its source but a library newer than both)
+    hdr = max(p.stat().st_mtime for p in _headers())
+    if any(_stale_obj(s, hdr) for s in sources()):
+        return True
     t = OUT.stat().st_mtime
-    deps = sources() + _headers()
-    return any(p.stat().st_mtime > t for p in deps)
+    return any(_obj(s).stat().st_mtime > t for s in sources())
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:

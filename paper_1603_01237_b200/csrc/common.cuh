@@ -177,6 +177,11 @@ struct DevRun {
   int* nm_fallback;     // [B][L]
   double2* nm_v;        // [B][L][traj_len - 1][d] fused-residual vectors v_j
   int* nm_count;        // [1] tasks handed to Gauss-Jordan by the last Neumann sweep
+  // one-pass iteration (dense_nm.cu dual evaluation): the update computed at the end of an
+  // iteration and applied at the start of the next, and the previous iteration's tasks
+  double* gpend;        // [B][K] weight * g_j
+  double2* old_init;    // [B][L][d]
+  double2* old_targ;    // [B][L][d]
   int cap;
 };
 

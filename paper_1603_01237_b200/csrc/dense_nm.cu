@@ -393,23 +393,63 @@ __global__ void __launch_bounds__(NM_WARPS * 32, 2) dense_nm_assemble_kernel(Dev
 //   psi_j = P_j phi,  chi_j = P_j chi_0,  chi_0 = P_len^dag seed       (objective.cpp:31-34)
 //   g_j = -alpha_j dt u_j + dt/4 w Im<chi_j + chi_{j+1}, Hc (psi_j + psi_{j+1})>  (objective.cpp:55-57)
 // Lane (row = l & 15, g = l >> 4) holds columns 2t + g of its row of every matrix.
+//
+// dual = 1 is the one-pass iteration: the two warps of a pair read the same P_j (the second
+// read hits L1/L2, so the 36 GB cache leaves HBM once) and evaluate
+//   warp 0: the residual of iteration k with its tasks S_k (R.old_*) at the updated control;
+//   warp 1: the entry value and gradient of iteration k + 1 with the refreshed tasks S_{k+1},
+//           whose weighted gradient w g_j goes to R.gpend (applied by the next iteration's first kernel).
+// dual = 2 is warp-1 work only (bootstrap).
+//
+// RING (dual = 1 only): a pair shares one stream, which halves the loads a warp keeps in flight;
+// the pair's matrices instead arrive by TMA bulk copies (4 KB each) into a DS-stage shared
+// ring per task, issued by lane 0 of the pair's second warp, so DS matrices per task are in
+// flight regardless of registers.  Consumption order c = 0..len reads P_len, P_1, ..., P_len.
+constexpr int DT = 4, DS = 4;  // tasks per CTA, ring stages per task
+template <bool RING>
 __global__ void __launch_bounds__(256, 2) dense_pc_eval16_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done,
-                                                                  int handed_off_only) {
+                                                                  int handed_off_only, int dual) {
   constexpr int PE_ENTRY = 1, PE_GRAD = 2, PE_ERR = 4;
   __shared__ double2 hcs[ND * ND];  // Hc column-major: lane (row, g) reads 512-byte runs
   __shared__ double2 xs[8][ND];
+  extern __shared__ __align__(128) unsigned char ring_raw[];  // RING: [DT][DS][256] double2 + barriers
+  double2* ring = reinterpret_cast<double2*>(ring_raw);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + DT * DS * ND * ND);
   const int b = blockIdx.y;
   if (handed_off_only && *R.nm_count == 0) return;  // nothing was handed off (the common case)
   if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
   const size_t dd = (size_t)ND * ND;
   for (int e = threadIdx.x; e < ND * ND; e += blockDim.x) hcs[(e & 15) * ND + (e >> 4)] = P.lin[(size_t)b * dd + e];
-  __syncthreads();
   const int warp = threadIdx.x >> 5, l = threadIdx.x & 31, row = l & 15, g = l >> 4;
-  const int n = blockIdx.x * 8 + warp;
+  const int n = dual == 1 ? blockIdx.x * 4 + (warp >> 1) : blockIdx.x * 8 + warp;
+  const int role = dual == 1 ? (warp & 1) : 1;  // 0: residual of S_k, 1: entry + gradient
+  const int tl = warp >> 1;                     // RING: task slot of the pair
+  const bool producer = RING && role == 1 && l == 0 && n < P.L;
+  const int plen = n < P.L ? P.node[n + 1] - P.node[n] : 0;
+  const double2* Pg = R.pc + ((size_t)b * P.L + n) * (size_t)R.traj_len * dd;
+  auto issue = [&](int c) {  // producer: matrix of consumption step c into its stage
+    const int st = c % DS;
+    mbar_expect_tx(&full[tl * DS + st], (unsigned)(dd * sizeof(double2)));
+    bulk_g2s(ring + (size_t)(tl * DS + st) * dd, Pg + (size_t)(c ? c : plen) * dd, (unsigned)(dd * sizeof(double2)),
+             &full[tl * DS + st]);
+  };
+  if (RING) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < DT * DS; ++i) mbar_init(&full[i], 1);
+      mbar_init_fence();
+    }
+    __syncthreads();
+    if (producer)
+      for (int c = 0; c < DS && c <= plen; ++c) issue(c);
+  } else {
+    __syncthreads();
+  }
   if (n >= P.L) return;
   // residual of the tasks the Neumann sweep handed to Gauss-Jordan (its fused residual covers the rest)
   if (handed_off_only && R.nm_fallback[(size_t)b * P.L + n] == 0) return;
-  const int mode = A.mode;
+  const int mode = dual ? (role ? (PE_ENTRY | PE_GRAD) : PE_ERR) : A.mode;
+  const double2* t_init = (dual && !role) ? R.old_init : R.task_init;
+  const double2* t_targ = (dual && !role) ? R.old_targ : R.task_targ;
   const int node0 = P.node[n], len = P.node[n + 1] - node0;
   const double Kd = (double)P.K, weight = A.weighted ? Kd / (double)len : 1.0, scale = (double)len / Kd;
   const double dt = P.dt, w = P.ip_w;
@@ -419,21 +459,41 @@ __global__ void __launch_bounds__(256, 2) dense_pc_eval16_kernel(DevProblem P, D
   double* u = R.u + (size_t)b * P.K + node0;
   double2 phi[8];
 #pragma unroll
-  for (int t = 0; t < 8; ++t) phi[t] = R.task_init[tix + 2 * t + g];
+  for (int t = 0; t < 8; ++t) phi[t] = t_init[tix + 2 * t + g];
   auto half_sum = [&](double2 v) { return cadd(v, shfl_xor(v, 16)); };
   auto row_sum = [&](double v) {
 #pragma unroll
     for (int off = 1; off < 16; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
     return v;
   };
-  double2 m[8];
+  // matrix of consumption step c (P_len for c = 0, else P_c) into m
+  auto fetch = [&](int c, double2* m) {
+    if (RING) {
+      const int st = c % DS;
+      mbar_wait(&full[tl * DS + st], (unsigned)((c / DS) & 1));
+      const double2* src = ring + (size_t)(tl * DS + st) * dd + l;
 #pragma unroll
-  for (int t = 0; t < 8; ++t) m[t] = __ldcs(Pc + (size_t)len * dd + 32 * t);  // P_len
+      for (int t = 0; t < 8; ++t) m[t] = src[32 * t];
+    } else {
+      const double2* src = Pc + (size_t)(c ? c : len) * dd;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) m[t] = __ldcs(src + 32 * t);
+    }
+  };
+  // both warps of the pair are done with step c's stage: refill it with step c + DS
+  auto release = [&](int c) {
+    if (RING) {
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + tl) : "memory");
+      if (producer && c + DS <= len) issue(c + DS);
+    }
+  };
+  double2 m[8];
+  fetch(0, m);  // P_len
   double2 acc = cx(0.0, 0.0);
 #pragma unroll
   for (int t = 0; t < 8; ++t) acc = cfma(m[t], phi[t], acc);
   const double2 psiL = half_sum(acc);  // row `row` of P_len phi
-  const double2 targ = R.task_targ[tix + row];
+  const double2 targ = t_targ[tix + row];
   if (mode & PE_ENTRY) {
     const double tv = A.form == 0 ? cconjmul(targ, psiL).x : cabs2(csub(psiL, targ));
     const double s = row_sum(g == 0 ? tv : 0.0);
@@ -455,15 +515,15 @@ __global__ void __launch_bounds__(256, 2) dense_pc_eval16_kernel(DevProblem P, D
       for (int off = 1; off < 16; off <<= 1) v = cadd(v, shfl_xor(v, off));
       chi0[t] = v;
     }
+    release(0);
     // row-distributed psi_0 = phi and chi_0 (column slots -> rows through shared memory)
     if (row == 0)
 #pragma unroll
       for (int t = 0; t < 8; ++t) xs[warp][2 * t + g] = chi0[t];
     __syncwarp();
-    double2 psi_prev = R.task_init[tix + row], chi_prev = xs[warp][row];
+    double2 psi_prev = t_init[tix + row], chi_prev = xs[warp][row];
     for (int j = 0; j < len; ++j) {
-#pragma unroll
-      for (int t = 0; t < 8; ++t) m[t] = __ldcs(Pc + (size_t)(j + 1) * dd + 32 * t);
+      fetch(j + 1, m);
       double2 a = cx(0.0, 0.0), c = cx(0.0, 0.0);
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
@@ -471,6 +531,7 @@ __global__ void __launch_bounds__(256, 2) dense_pc_eval16_kernel(DevProblem P, D
         c = cfma(m[t], chi0[t], c);
       }
       const double2 psi_n = half_sum(a), chi_n = half_sum(c);
+      release(j + 1);
       const double2 ps = cadd(psi_prev, psi_n), cs = cadd(chi_prev, chi_n);
       // (Hc ps)[row]: ps of column 2t + g comes from lane 2t + g (its own row)
       double2 h = cx(0.0, 0.0);
@@ -480,7 +541,11 @@ __global__ void __launch_bounds__(256, 2) dense_pc_eval16_kernel(DevProblem P, D
       const double im = row_sum(g == 0 ? cconjmul(cs, h).y : 0.0);
       const double uj = u[j];
       const double gj = -(P.alpha[node0 + j] * scale) * dt * uj + 0.25 * dt * (w * im);
-      if (l == 0 && (mode & PE_GRAD)) u[j] = uj + A.rho * (weight * gj);
+      if (l == 0 && (mode & PE_GRAD)) {
+        // u + rho (w g) as one explicit fma in both orders (apply_pending_kernel repeats it)
+        if (dual) R.gpend[(size_t)b * P.K + node0 + j] = weight * gj;
+        else u[j] = __fma_rn(A.rho, weight * gj, uj);
+      }
       err += fabs(gj);  // C = 1: ||g_j||_2 = |g_j| (error_norm, objective.cpp:152-160)
       psi_prev = psi_n;
       chi_prev = chi_n;
@@ -489,6 +554,9 @@ __global__ void __launch_bounds__(256, 2) dense_pc_eval16_kernel(DevProblem P, D
   if (l == 0) {
     if (handed_off_only) {
       R.err[(size_t)b * P.L + n] = err;
+    } else if (dual) {
+      if (role) R.chunk_pen[(size_t)b * P.L + n] = pen;
+      else R.chunk_err[(size_t)b * P.L + n] = err;
     } else {
       R.chunk_pen[(size_t)b * P.L + n] = pen;
       R.chunk_err[(size_t)b * P.L + n] = err;
@@ -528,8 +596,17 @@ bool dense_pc_eval16_applicable(const DevProblem& P, const DevRun& R, int mode, 
 }
 
 cudaError_t dense_pc_eval16(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st,
-                            int handed_off_only) {
-  dense_pc_eval16_kernel<<<dim3((P.L + 7) / 8, P.B), 256, 0, st>>>(P, R, A, ignore_done, handed_off_only);
+                            int handed_off_only, int dual) {
+  if (dual == 1 && !disabled("ring")) {
+    const size_t smem = sizeof(double2) * DT * DS * ND * ND + sizeof(unsigned long long) * DT * DS;
+    cudaError_t e = cudaFuncSetAttribute(dense_pc_eval16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    dense_pc_eval16_kernel<true><<<dim3((P.L + DT - 1) / DT, P.B), 256, smem, st>>>(P, R, A, ignore_done, 0, 1);
+    return cudaGetLastError();
+  }
+  const int per = dual == 1 ? 4 : 8;
+  dense_pc_eval16_kernel<false><<<dim3((P.L + per - 1) / per, P.B), 256, 0, st>>>(P, R, A, ignore_done, handed_off_only, dual);
   return cudaGetLastError();
 }
 

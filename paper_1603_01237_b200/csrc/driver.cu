@@ -443,6 +443,9 @@ void alloc_run(const DeviceProblem& dp, int cap, const std::vector<int>& node, b
       R.nm_fallback = out.alloc<int>(B * L);
       R.nm_v = out.alloc<double2>(B * L * (R.traj_len - 1) * d);
       R.nm_count = out.alloc<int>(1);
+      R.gpend = out.alloc<double>(B * K);
+      R.old_init = out.alloc<double2>(B * L * d);
+      R.old_targ = out.alloc<double2>(B * L * d);
       ck(cudaMemsetAsync(R.nm_fallback, 0, sizeof(int) * B * L, st), "memset");
     }
     const int nchunk = pc_nchunk(P, R);
@@ -587,6 +590,12 @@ int32_t guarded(qoc_ctx* ctx, F&& f) {
   }
 }
 
+// QOC_DISABLE="onepass" restores the two-pass iteration order (A/B on the GPU box)
+bool disabled_path(const char* what) {
+  const char* e = std::getenv("QOC_DISABLE");
+  return e && std::strstr(e, what) != nullptr;
+}
+
 }  // namespace
 
 extern "C" {
@@ -723,6 +732,17 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
     auto destroy_events = [&] {
       for (auto& e : ev) cudaEventDestroy(e);
     };
+    const int form = split ? QOC_FORM_OVERLAP : QOC_FORM_TRACKING;
+    // run_inner (optimizers.cpp:261-285): inner_iterations <= 0 makes no update but the entry
+    // value is still evaluated (ism.cpp:407)
+    const int inner = std::max(0, solver->inner_iterations);
+    // One cache pass per iteration instead of two (Neumann path, one inner update, residual
+    // logged): the pass after the boundary refresh evaluates the residual of iteration k with
+    // the saved tasks S_k and the entry value + update of iteration k + 1 with S_{k+1}, both at
+    // the control u_{k+1} the cache was assembled for; the update lands at the start of k + 1.
+    // Same arithmetic as the gradient -> assembly -> residual order, reordered.
+    const bool onepass = pcache && R.nm && !split && inner == 1 && cfg->compute_error &&
+                         dense_pc_eval16_applicable(P, R, PCM_ENTRY | PCM_GRAD | PCM_ERR, 1) && !disabled_path("onepass");
     try {
       ck(cudaEventRecord(ev[0], st), "event");
       // ---- bootstrap (ism.cpp:344-393)
@@ -743,13 +763,11 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
       } else {
         launch(set_single_tasks(P, R, st), "tasks");
       }
+      // one-pass iteration: the first entry value and update come from the bootstrap cache
+      if (onepass) launch(pc_eval_dual(P, R, form, split ? 0 : 1, solver->step_size, 2, st), "gradient");
       ck(cudaEventRecord(ev[1], st), "event");
       trace.mark("bootstrap", st);
 
-      const int form = split ? QOC_FORM_OVERLAP : QOC_FORM_TRACKING;
-      // run_inner (optimizers.cpp:261-285): inner_iterations <= 0 makes no update but the entry
-      // value is still evaluated (ism.cpp:407)
-      const int inner = std::max(0, solver->inner_iterations);
       int mode = M_ENTRY | (inner > 0 ? M_UPDATE : 0);
       if (cfg->compute_error) mode |= M_ERROR;
       if (assembled_interp) mode |= M_ASSEMBLE;
@@ -762,6 +780,24 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
       launch.in_iteration = true;
       // One outer iteration (ism.cpp:396-592) as a launch sequence on `st` (+ the side stream).
       auto body = [&](const DevRun& RR, int k) {
+        if (onepass) {
+          launch.run([&] { return apply_pending(P, RR, solver->step_size, st); }, "update");
+          launch.run([&] { return penalty_partials(P, RR, 0, st); }, "penalty");
+          launch.run([&] { return merge_iteration(P, RR, k, nullptr, st); }, "merge");
+          launch.run([&] { return pc_assemble(P, RR, 0, st); }, "assembly", true);
+          launch.run([&] { return save_tasks(P, RR, st); }, "save tasks");
+          if (L > 1) {
+            if (direct) launch.run([&] { return horizon(P, RR, 0, k, st); }, "node sweeps", true);
+            else launch.run([&] { return chain_propagators(P, RR, st); }, "chain");
+            launch.run([&] { return boundary_update(P, RR, k, split, 0, st); }, "boundary");
+          }
+          if (cfg->log_exact_objective) launch.run([&] { return horizon(P, RR, 1, k, st); }, "exact objective", true);
+          launch.run([&] { return pc_eval_dual(P, RR, form, 1, solver->step_size, 1, st); }, "evaluation", true);
+          launch.run([&] { return total_error(P, RR, st); }, "error total");
+          launch.run([&] { return finish_iteration_ex(P, RR, k, cfg->compute_error, cfg->eta,
+                                                      cfg->log_exact_objective, st); }, "finish");
+          return;
+        }
         if (pcache) {
           // gradient + update through the cache, then the assembly sweep at the new control,
           // then residual / lagged endpoints through the new cache
@@ -840,7 +876,7 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
         put(&P, sizeof(P));
         put(&RG, sizeof(RG));
         const int cfgv[] = {form, (int)split, (int)direct, (int)pcache, (int)assembled_interp, L,
-                            cfg->compute_error, cfg->log_exact_objective, solver->inner_iterations};
+                            cfg->compute_error, cfg->log_exact_objective, solver->inner_iterations, (int)onepass};
         put(cfgv, sizeof(cfgv));
         const double cfgd[] = {solver->step_size, cfg->eta};
         put(cfgd, sizeof(cfgd));
@@ -933,7 +969,9 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
       trace.mark("outer iterations", st);
       // ---- trailing evaluation (ism.cpp:594-609)
       {
-        if (pcache) {
+        if (onepass) {
+          // the last evaluation pass already left every problem's final entry values
+        } else if (pcache) {
           const TaskArgs T{PCM_ENTRY, form, split ? 0 : 1, 1, 0.0};
           launch(pc_eval(P, R, T, 1, st), "trailing task");
         } else {

@@ -93,6 +93,37 @@ __global__ void __launch_bounds__(128) merge_kernel(DevProblem P, DevRun R, int 
   }
 }
 
+// one-pass iteration: the update of the previous evaluation pass (R.gpend) lands first
+__global__ void apply_pending_kernel(DevProblem P, DevRun R, double rho) {
+  const int b = blockIdx.y;
+  if (R.done[b] || R.status[b]) return;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < P.K; j += gridDim.x * blockDim.x) {
+    const size_t i = (size_t)b * P.K + j;
+    R.u[i] = __fma_rn(rho, R.gpend[i], R.u[i]);
+  }
+}
+
+__global__ void save_tasks_kernel(DevProblem P, DevRun R) {
+  const int b = blockIdx.y;
+  if (R.done[b] || R.status[b]) return;
+  const size_t n = (size_t)P.L * P.d;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    R.old_init[(size_t)b * n + i] = R.task_init[(size_t)b * n + i];
+    R.old_targ[(size_t)b * n + i] = R.task_targ[(size_t)b * n + i];
+  }
+}
+
+// the residual total the merge would have formed (same index-order block reduction)
+__global__ void __launch_bounds__(128) total_error_kernel(DevProblem P, DevRun R) {
+  __shared__ double sh[128];
+  const int b = blockIdx.x;
+  if (R.done[b] || R.status[b]) return;
+  double tot = 0.0;
+  for (int n = threadIdx.x; n < P.L; n += 128) tot += R.err[(size_t)b * P.L + n];
+  tot = block_sum<128>(tot, sh);
+  if (threadIdx.x == 0) R.tot_err[b] = tot;
+}
+
 // compose_from_propagators for d <= 1024 held row-major: psi_{n+1} = M_n psi_n,
 // chi_n = M_n^dagger chi_{n+1}.  One CTA per problem, rows over threads.
 __global__ void chain_kernel(DevProblem P, DevRun R) {
@@ -381,6 +412,18 @@ cudaError_t finish_iteration(const DevProblem& P, const DevRun& R, int k, const 
 cudaError_t finish_iteration_ex(const DevProblem& P, const DevRun& R, int k, int compute_error, double eta,
                                 int log_exact, cudaStream_t st) {
   finish_kernel<<<(P.B + 127) / 128, 128, 0, st>>>(P, R, k, compute_error, eta, log_exact);
+  return cudaGetLastError();
+}
+cudaError_t apply_pending(const DevProblem& P, const DevRun& R, double rho, cudaStream_t st) {
+  apply_pending_kernel<<<dim3((P.K + 255) / 256, P.B), 256, 0, st>>>(P, R, rho);
+  return cudaGetLastError();
+}
+cudaError_t save_tasks(const DevProblem& P, const DevRun& R, cudaStream_t st) {
+  save_tasks_kernel<<<dim3((P.L * P.d + 255) / 256, P.B), 256, 0, st>>>(P, R);
+  return cudaGetLastError();
+}
+cudaError_t total_error(const DevProblem& P, const DevRun& R, cudaStream_t st) {
+  total_error_kernel<<<P.B, 128, 0, st>>>(P, R);
   return cudaGetLastError();
 }
 cudaError_t trailing_values(const DevProblem& P, const DevRun& R, cudaStream_t st) {

@@ -50,7 +50,11 @@ cudaError_t dense_nm_setup(const DevProblem& P, const DevRun& R, cudaStream_t st
 cudaError_t dense_nm_assemble(const DevProblem& P, const DevRun& R, int ignore_done, int residual, cudaStream_t st);
 bool dense_pc_eval16_applicable(const DevProblem& P, const DevRun& R, int mode, int nchunk);
 cudaError_t dense_pc_eval16(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st,
-                            int handed_off_only = 0);
+                            int handed_off_only = 0, int dual = 0);
+// One-pass iteration (dense_nm.cu): dual = 1 evaluates the residual of the saved tasks and the
+// entry value + pending update of the current tasks in one cache pass; dual = 2 only the latter.
+cudaError_t pc_eval_dual(const DevProblem& P, const DevRun& R, int form, int weighted, double rho, int dual,
+                         cudaStream_t st);
 
 // glue (kind independent)
 cudaError_t penalty_partials(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st);
@@ -63,6 +67,10 @@ cudaError_t finish_iteration(const DevProblem& P, const DevRun& R, int k, const 
                              double eta, cudaStream_t st);
 cudaError_t finish_iteration_ex(const DevProblem& P, const DevRun& R, int k, int compute_error, double eta,
                                 int log_exact, cudaStream_t st);
+// one-pass iteration glue: u += rho R.gpend, the task backup S_k -> R.old_*, and R.tot_err
+cudaError_t apply_pending(const DevProblem& P, const DevRun& R, double rho, cudaStream_t st);
+cudaError_t save_tasks(const DevProblem& P, const DevRun& R, cudaStream_t st);
+cudaError_t total_error(const DevProblem& P, const DevRun& R, cudaStream_t st);
 cudaError_t trailing_values(const DevProblem& P, const DevRun& R, cudaStream_t st);
 
 }  // namespace qoc

@@ -646,6 +646,16 @@ cudaError_t pc_eval(const DevProblem& P, const DevRun& R, const TaskArgs& A, int
   return cudaGetLastError();
 }
 
+cudaError_t pc_eval_dual(const DevProblem& P, const DevRun& R, int form, int weighted, double rho, int dual,
+                         cudaStream_t st) {
+  if (!dense_pc_eval16_applicable(P, R, PCM_ENTRY | PCM_GRAD | PCM_ERR, 1)) return cudaErrorNotSupported;
+  const TaskArgs A{dual == 1 ? (PCM_ENTRY | PCM_ERR) : PCM_ENTRY, form, weighted, 1, rho};
+  cudaError_t e = dense_pc_eval16(P, R, A, 0, st, 0, dual);
+  if (e != cudaSuccess) return e;
+  pc_finalize_kernel<<<(P.B * P.L + 127) / 128, 128, 0, st>>>(P, R, A, 1, 0);
+  return cudaGetLastError();
+}
+
 template <int D>
 static cudaError_t launch_dense_pc(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st) {
   using Cfg = DenseCfg<D, 1>;

@@ -54,6 +54,8 @@ def run(name: str):
         out[f"{tag}_exact"] = np.array([np.nan if it.exact_objective is None else it.exact_objective for it in its])
         out[f"{tag}_task_values"] = np.array([it.task_values for it in its])
         out[f"{tag}_rho"] = np.array(w.solver.step_size)
+        if name == "config4":  # host-dependent iterative eigen-solve: freeze the states used
+            out["initial"], out["target"] = np.asarray(w.problem.initial), np.asarray(w.problem.target)
         print(name, tag, f"{time.time() - t0:.1f}s", "final objective", out[f"{tag}_objective"][-1], flush=True)
     np.savez_compressed(OUT / f"{name}_full.npz", **out)
 

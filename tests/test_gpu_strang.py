@@ -84,6 +84,9 @@ def test_gpe1024_config4(ctx, tag):
     from tests.test_gpu_bitflip import FIXTURES, compare_run
     fx = np.load(FIXTURES / "config4_full.npz")
     w = problems.gpe1024(iterations=100)
+    # the stationary states are an iterative eigen-solve whose last digits depend on the host's
+    # BLAS: the fixture carries the exact states the oracle ran from
+    w.problem.initial, w.problem.target = fx["initial"], fx["target"]
     w.config.log_exact_objective = True
     w.solver.step_size = float(fx[f"{tag}_rho"])
     g = I.run_ism(w.problem, w.u0, w.config, w.solver, ctx)
