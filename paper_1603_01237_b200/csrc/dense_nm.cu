@@ -28,6 +28,7 @@
 //                             which keeps the partial-pivoting path.
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "dense.cuh"
 #include "kernels.h"
@@ -144,7 +145,7 @@ __device__ __forceinline__ int neumann_terms(double x) {
 //     v_j = (P_j + P_{j+1})^dag Hc (psi_j + psi_{j+1}),   y = P_len^dag seed,
 // (chi_j = P_j y by unitarity, as in pcache.cu): v_j is formed on the way (psi_{j+1} = C_j psi_j
 // from the Horner output), parked in `R.nm_v`, and contracted with y once P_len exists.
-template <bool GAUSS3, bool RESIDUAL>
+template <bool GAUSS3, bool RESIDUAL, int HB>
 __global__ void __launch_bounds__(NM_WARPS * 32, 2) dense_nm_assemble_kernel(DevProblem P, DevRun R, int ignore_done) {
   constexpr bool residual = RESIDUAL;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -185,12 +186,12 @@ __global__ void __launch_bounds__(NM_WARPS * 32, 2) dense_nm_assemble_kernel(Dev
   const double* u = R.u + (size_t)b * P.K + node0;
   // certified range check over the task's steps (warp-uniform); out-of-range tasks are handed
   // to the Gauss-Jordan kernel
+  // (len <= 32: lane j holds step j's control and certified term count, computed once here
+  // instead of as a dependent multiply chain in front of every step's Horner evaluation)
+  const double u_l = l < len ? u[l] : 0.0;
+  const int M_l = neumann_terms(fabs(u_l) * gam);  // NaN controls give -1
   {
-    double um = 0.0;
-    for (int j = l; j < len; j += 32) um = fmax(um, fabs(u[j]));
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) um = fmax(um, __shfl_xor_sync(0xffffffffu, um, off));
-    const bool ok = neumann_terms(um * gam) >= 0;  // NaN controls also fail here
+    const bool ok = __all_sync(0xffffffffu, M_l >= 0);
     if (l == 0 && live) {
       R.nm_fallback[(size_t)b * P.L + n] = ok ? 0 : 1;
       if (!ok) atomicAdd(R.nm_count, 1);
@@ -223,20 +224,39 @@ __global__ void __launch_bounds__(NM_WARPS * 32, 2) dense_nm_assemble_kernel(Dev
   mbar_wait(&bar, 0);
   if (residual) __syncthreads();  // hc_s visible
 
-  for (int j = 0; j < len; ++j) {
-    const double uj = u[j];
-    const int M = live ? neumann_terms(fabs(uj) * gam) : 0;
-    // Horner: Y = N_M; Y = N_m + u Y (m = M-1 .. 0); Y[s] = C(u)[8 jn + q][4 kk + r]
-    double2 Y[SLOTS];
+  // Horner for HB consecutive steps at once: every coefficient fragment read from shared memory
+  // (the kernel's bound: (M + 1) x 4 KB per step) serves HB controls.  The batch uses the largest
+  // certified term count of its steps (extra terms only shrink the truncation error).
+  for (int j0 = 0; j0 < len; j0 += HB) {
+    double uh[HB];
+    int M = 0;
 #pragma unroll
-    for (int s = 0; s < SLOTS; ++s) Y[s] = nm_s[(M * SLOTS + s) * 32 + l];
+    for (int h = 0; h < HB; ++h) {
+      uh[h] = __shfl_sync(0xffffffffu, u_l, (j0 + h) & 31);  // 0 past len
+      M = max(M, __shfl_sync(0xffffffffu, M_l, (j0 + h) & 31));
+    }
+    if (!live) M = 0;
+    // Horner: Y = N_M; Y = N_m + u Y (m = M-1 .. 0); Y[s] = C(u)[8 jn + q][4 kk + r]
+    double2 YH[HB][SLOTS];
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      const double2 nv = nm_s[(M * SLOTS + s) * 32 + l];
+#pragma unroll
+      for (int h = 0; h < HB; ++h) YH[h][s] = nv;
+    }
     for (int m = M - 1; m >= 0; --m) {
 #pragma unroll
       for (int s = 0; s < SLOTS; ++s) {
         const double2 nv = nm_s[(m * SLOTS + s) * 32 + l];
-        Y[s] = cx(fma(uj, Y[s].x, nv.x), fma(uj, Y[s].y, nv.y));
+#pragma unroll
+        for (int h = 0; h < HB; ++h) YH[h][s] = cx(fma(uh[h], YH[h][s].x, nv.x), fma(uh[h], YH[h][s].y, nv.y));
       }
     }
+#pragma unroll
+    for (int h = 0; h < HB; ++h) {
+    const int j = j0 + h;
+    if (j < len) {
+    const double2* Y = YH[h];
     double2 bc[4], vp[2];
     if (residual) {
       // psi_{j+1} = C_j psi_j: rows 8 jn + q, reduced over the quad's columns
@@ -336,6 +356,8 @@ __global__ void __launch_bounds__(NM_WARPS * 32, 2) dense_nm_assemble_kernel(Dev
         if (r == 0 && live) vj[(size_t)j * ND + 8 * i + q] = acc;
       }
     }
+    }
+    }
   }
   // M_n = P_len for the boundary chain (row-major)
   if (R.prop && live) {
@@ -405,16 +427,21 @@ __global__ void __launch_bounds__(NM_WARPS * 32, 2) dense_nm_assemble_kernel(Dev
 // the pair's matrices instead arrive by TMA bulk copies (4 KB each) into a DS-stage shared
 // ring per task, issued by lane 0 of the pair's second warp, so DS matrices per task are in
 // flight regardless of registers.  Consumption order c = 0..len reads P_len, P_1, ..., P_len.
-constexpr int DT = 4, DS = 4;  // tasks per CTA, ring stages per task
+// Each warp marks a stage consumed on its `empty` barrier without waiting; the producer refills
+// the stage one step late (so it rarely waits for the slower warp of the pair).
+constexpr int DT = 4, DS = 5;  // tasks per CTA, ring stages per task
 template <bool RING>
 __global__ void __launch_bounds__(256, 2) dense_pc_eval16_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done,
                                                                   int handed_off_only, int dual) {
   constexpr int PE_ENTRY = 1, PE_GRAD = 2, PE_ERR = 4;
   __shared__ double2 hcs[ND * ND];  // Hc column-major: lane (row, g) reads 512-byte runs
   __shared__ double2 xs[8][ND];
+  __shared__ double2 pss[8][ND];       // psi_j + psi_{j+1} by row, read back as broadcasts
+  __shared__ double ush[8][32], ash[8][32];  // the task's controls and penalty weights (len <= 32)
   extern __shared__ __align__(128) unsigned char ring_raw[];  // RING: [DT][DS][256] double2 + barriers
   double2* ring = reinterpret_cast<double2*>(ring_raw);
   unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + DT * DS * ND * ND);
+  unsigned long long* empty = full + DT * DS;
   const int b = blockIdx.y;
   if (handed_off_only && *R.nm_count == 0) return;  // nothing was handed off (the common case)
   if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
@@ -435,7 +462,10 @@ __global__ void __launch_bounds__(256, 2) dense_pc_eval16_kernel(DevProblem P, D
   };
   if (RING) {
     if (threadIdx.x == 0) {
-      for (int i = 0; i < DT * DS; ++i) mbar_init(&full[i], 1);
+      for (int i = 0; i < DT * DS; ++i) {
+        mbar_init(&full[i], 1);
+        mbar_init(&empty[i], 2);
+      }
       mbar_init_fence();
     }
     __syncthreads();
@@ -480,11 +510,16 @@ __global__ void __launch_bounds__(256, 2) dense_pc_eval16_kernel(DevProblem P, D
       for (int t = 0; t < 8; ++t) m[t] = __ldcs(src + 32 * t);
     }
   };
-  // both warps of the pair are done with step c's stage: refill it with step c + DS
+  // this warp is done with step c's stage; the producer refills step c - 1's stage (both
+  // warps done with it) with step c - 1 + DS
   auto release = [&](int c) {
     if (RING) {
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + tl) : "memory");
-      if (producer && c + DS <= len) issue(c + DS);
+      __syncwarp();
+      if (l == 0) mbar_arrive(&empty[tl * DS + c % DS]);
+      if (producer && c >= 1 && c - 1 + DS <= len) {
+        mbar_wait(&empty[tl * DS + (c - 1) % DS], (unsigned)(((c - 1) / DS) & 1));
+        issue(c - 1 + DS);
+      }
     }
   };
   double2 m[8];
@@ -522,25 +557,41 @@ __global__ void __launch_bounds__(256, 2) dense_pc_eval16_kernel(DevProblem P, D
       for (int t = 0; t < 8; ++t) xs[warp][2 * t + g] = chi0[t];
     __syncwarp();
     double2 psi_prev = t_init[tix + row], chi_prev = xs[warp][row];
+    if (l < len) {
+      ush[warp][l] = u[l];
+      ash[warp][l] = P.alpha[node0 + l];
+    }
+    __syncwarp();
     for (int j = 0; j < len; ++j) {
       fetch(j + 1, m);
-      double2 a = cx(0.0, 0.0), c = cx(0.0, 0.0);
+      // two accumulators per product (even / odd column slots) halve the dependent fma chains
+      double2 a0 = cx(0.0, 0.0), a1 = cx(0.0, 0.0), c0 = cx(0.0, 0.0), c1 = cx(0.0, 0.0);
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        a = cfma(m[t], phi[t], a);
-        c = cfma(m[t], chi0[t], c);
+      for (int t = 0; t < 8; t += 2) {
+        a0 = cfma(m[t], phi[t], a0);
+        c0 = cfma(m[t], chi0[t], c0);
+        a1 = cfma(m[t + 1], phi[t + 1], a1);
+        c1 = cfma(m[t + 1], chi0[t + 1], c1);
       }
-      const double2 psi_n = half_sum(a), chi_n = half_sum(c);
+      const double2 psi_n = half_sum(cadd(a0, a1)), chi_n = half_sum(cadd(c0, c1));
       release(j + 1);
       const double2 ps = cadd(psi_prev, psi_n), cs = cadd(chi_prev, chi_n);
-      // (Hc ps)[row]: ps of column 2t + g comes from lane 2t + g (its own row)
-      double2 h = cx(0.0, 0.0);
+      // (Hc ps)[row]: ps of column 2t + g read back from shared memory (broadcast)
+      __syncwarp();
+      if (g == 0) pss[warp][row] = ps;
+      __syncwarp();
+      double2 h0 = cx(0.0, 0.0), h1 = cx(0.0, 0.0);
 #pragma unroll
-      for (int t = 0; t < 8; ++t) h = cfma(hcs[(2 * t + g) * ND + row], shfl(ps, 2 * t + g), h);
-      h = half_sum(h);
-      const double im = row_sum(g == 0 ? cconjmul(cs, h).y : 0.0);
-      const double uj = u[j];
-      const double gj = -(P.alpha[node0 + j] * scale) * dt * uj + 0.25 * dt * (w * im);
+      for (int t = 0; t < 8; t += 2) {
+        h0 = cfma(hcs[(2 * t + g) * ND + row], pss[warp][2 * t + g], h0);
+        h1 = cfma(hcs[(2 * t + 2 + g) * ND + row], pss[warp][2 * t + 2 + g], h1);
+      }
+      // Im <cs, Hc ps> = sum over all 32 lanes of Im(conj(cs_row) (this half's part of (Hc ps)_row))
+      double im = cconjmul(cs, cadd(h0, h1)).y;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) im += __shfl_xor_sync(0xffffffffu, im, off);
+      const double uj = ush[warp][j];
+      const double gj = -(ash[warp][j] * scale) * dt * uj + 0.25 * dt * (w * im);
       if (l == 0 && (mode & PE_GRAD)) {
         // u + rho (w g) as one explicit fma in both orders (apply_pending_kernel repeats it)
         if (dual) R.gpend[(size_t)b * P.K + node0 + j] = weight * gj;
@@ -598,7 +649,7 @@ bool dense_pc_eval16_applicable(const DevProblem& P, const DevRun& R, int mode, 
 cudaError_t dense_pc_eval16(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st,
                             int handed_off_only, int dual) {
   if (dual == 1 && !disabled("ring")) {
-    const size_t smem = sizeof(double2) * DT * DS * ND * ND + sizeof(unsigned long long) * DT * DS;
+    const size_t smem = sizeof(double2) * DT * DS * ND * ND + 2 * sizeof(unsigned long long) * DT * DS;
     cudaError_t e = cudaFuncSetAttribute(dense_pc_eval16_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
@@ -622,8 +673,16 @@ static bool nm_gauss3() {
 }
 
 cudaError_t dense_nm_assemble(const DevProblem& P, const DevRun& R, int ignore_done, int residual, cudaStream_t st) {
-  auto kern = nm_gauss3() ? (residual ? dense_nm_assemble_kernel<true, true> : dense_nm_assemble_kernel<true, false>)
-                          : (residual ? dense_nm_assemble_kernel<false, true> : dense_nm_assemble_kernel<false, false>);
+  // QOC_NM_HB: steps per Horner batch (1, 2 or 4; default 2)
+  const char* hbe = std::getenv("QOC_NM_HB");
+  const int hb = hbe ? std::atoi(hbe) : 2;
+  auto pick = [&](auto g3) {
+    constexpr bool G = decltype(g3)::value;
+    if (residual) return dense_nm_assemble_kernel<G, true, 1>;
+    return hb == 4 ? dense_nm_assemble_kernel<G, false, 4>
+                   : hb == 1 ? dense_nm_assemble_kernel<G, false, 1> : dense_nm_assemble_kernel<G, false, 2>;
+  };
+  auto kern = nm_gauss3() ? pick(std::true_type{}) : pick(std::false_type{});
   const size_t smem = dense_nm_smem();
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
