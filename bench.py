@@ -36,6 +36,13 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "propagation steps/s (fwd+adjoint, all subintervals); time-to-fidelity 0.999"
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2: every timed iteration starts cold
+# --blocks G (config 3): the blocked boundary refresh with G subinterval blocks; None keeps the
+# direct node sweeps on one GPU and one block per rank under torchrun (SURVEY §8(e) option A)
+BLOCKS = None
+
+
+def ising_blocked(world: int) -> bool:
+    return BLOCKS is not None or world > 1
 
 
 def flops_per_iteration(name: str, w) -> float:
@@ -64,6 +71,8 @@ def flops_per_iteration(name: str, w) -> float:
         m = int(np.ceil(53 * np.log(2) / -np.log(q)))
         cay = (1 + m) * (8 * n + 12) * d
         per = 7 * cay + 2 * C * n * 16 * d
+        if w.config.plan == "assembled":
+            per += d * cay  # blocked plan: the block products carry d columns per grid step
     elif name == "gpe1024":
         # split variant: entry, gradient (fwd + bwd), residual (fwd + bwd), lagged refresh
         # (fwd + bwd) = 4 forward + 3 backward stages per grid step; FFT = 5 n log2 n
@@ -159,6 +168,8 @@ def build_workload(name: str, iterations: int, rank: int, world: int, rho_fast: 
         w = problems.batch4096(batch=count, iterations=iterations, first=first)
     elif name == "ising10":
         w = problems.ising10(iterations=iterations)
+        if ising_blocked(world):
+            w.config.plan, w.config.blocks = "assembled", BLOCKS or 0
     elif name == "gpe1024":
         w = problems.gpe1024(iterations=iterations)
         # the exact-payoff instrumentation (a serial K-step sweep per iteration) is outside the
@@ -181,7 +192,10 @@ def workload_config(name: str, world: int) -> dict:
             "subintervals": desc["subintervals"], "partition": desc["partition"], "problems": total,
             "problems_per_gpu": w.problem.batch, "step_size": w.solver.step_size, "variant": desc["variant"],
             "plan": desc["plan"],
-            "parallelism": (f"problem blocks x{world}" if name == "batch4096" else f"replicas x{world}"),
+            "parallelism": (f"problem blocks x{world}" if name == "batch4096" else
+                            f"subinterval blocks: {BLOCKS or world} blocks over {world} rank(s), one all-gather "
+                            "per outer iteration" if name == "ising10" and ising_blocked(world) else
+                            f"replicas x{world}"),
             "l2": "flushed between timed iterations (256 MiB memset outside the event brackets)"}
 
 
@@ -274,6 +288,7 @@ def cpu_reference(name: str, warmup: int, steps: int, world: int = 1):
     arith = O.REFERENCE
     if name == "ising10":  # dense LU at d = 1024 is ~1.4e14 flop per iteration: structured solve
         arith = O.STRUCTURED
+        w.config.plan, w.config.blocks = "direct", 0  # the oracle's plan (agrees to rounding)
         steps = min(steps, 2)
         warmup = 0
     if name == "rotor21":  # the reference builds the rotor as a dense model (models.cpp:361-380)
@@ -319,7 +334,7 @@ def run_reference_arm(args, world, rank, dist):
     return 0
 
 
-def label_flops(name: str, label: str, w) -> float:
+def label_flops(name: str, label: str, w, world: int = 1) -> float:
     """Algorithmic fp64 flops of one launch of the kernel behind a launch label (SURVEY §8(d)
     per-grid-step model x K x B).  'assembly' = the d-column propagator product sweep
     (assemble_propagator, propagation.cpp:236-249); 'gradient'/'residual' = a forward sweep +
@@ -346,7 +361,9 @@ def label_flops(name: str, label: str, w) -> float:
         q = 0.5 * p.grid.dt * np.max(np.sqrt((np.abs(u[0]) * 0.5 * n) ** 2 + (np.abs(u[1]) * 0.5 * n) ** 2))
         cay = (1 + int(np.ceil(53 * np.log(2) / -np.log(q)))) * (8 * n + 12) * d
         per = {"node sweeps": 2 * cay,  # forward + adjoint full-horizon sweeps
-               "task": 5 * cay + 2 * C * n * 16 * d}.get(label)
+               "task": 5 * cay + 2 * C * n * 16 * d,
+               # blocked plan: d basis columns through this rank's K / W steps
+               "block products": d * cay / world}.get(label)
     else:
         per = None
     if per is None:
@@ -364,7 +381,12 @@ def main():
                     choices=["batch4096", "rotor21", "spin2", "ising10", "gpe1024"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttf", action="store_true", help="skip the time-to-fidelity run")
+    ap.add_argument("--blocks", type=int, default=None,
+                    help="ising10: subinterval blocks of the blocked boundary refresh (default: direct "
+                         "node sweeps on one GPU, one block per rank on N GPUs)")
     args = ap.parse_args()
+    global BLOCKS
+    BLOCKS = args.blocks
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return spawn_ranks(args.gpus)
     world, rank, local, dist = dist_setup()
@@ -377,6 +399,11 @@ def main():
 
     K_, W_ = args.steps, args.warmup
     ctx = _native.default_context(local)
+    blocked = args.workload == "ising10" and ising_blocked(world)
+    if blocked and world > 1:  # one NCCL communicator inside libqoc_b200.so per rank
+        obj = [_native.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.init_comm(rank, world, obj[0])
     w = build_workload(args.workload, W_ + K_, rank, world)
     p = w.problem
     # untimed first call (context, module load)
@@ -407,7 +434,8 @@ def main():
     t_rank = sum(it.device_seconds for it in timed)
     t_max = allmax(dist, t_rank)
     work_rank = 2.0 * p.grid.steps * p.batch * K_
-    work = allsum(dist, work_rank)
+    # a sharded config-3 run is ONE problem over all ranks: its steps are counted once
+    work = work_rank if blocked else allsum(dist, work_rank)
     value = work / t_max
     launches_per_iter = prof_main["iteration_launches"] / max(prof_main["iterations"], 1)
 
@@ -417,7 +445,7 @@ def main():
     iter_ms = prof["iteration_ms"] / n_iter
     dom, (dom_ms, dom_n) = max(kprof.items(), key=lambda kv: kv[1][0]) if kprof else ("task", (float("nan"), 1))
     per_launch_ms = dom_ms / max(dom_n, 1)
-    fl_launch = label_flops(args.workload, dom, wp)
+    fl_launch = label_flops(args.workload, dom, wp, world)
     tensor = args.workload == "batch4096" and dom == "assembly"
     peak, peak_src = dmma_peak() if tensor else fp64_peak()
     achieved = fl_launch / (per_launch_ms * 1e-3) / 1e12
@@ -452,7 +480,8 @@ def main():
         barrier_sync(dist)
         walls.append(time.perf_counter() - t0)
     e2e_wall = allmax(dist, statistics.median(walls))
-    e2e_value = allsum(dist, 2.0 * we.problem.grid.steps * we.problem.batch * K_) / e2e_wall
+    e2e_work = 2.0 * we.problem.grid.steps * we.problem.batch * K_
+    e2e_value = (e2e_work if blocked else allsum(dist, e2e_work)) / e2e_wall
     h2d = problem_bytes(we)
     nb = we.problem.batch
     d2h = int(8 * we.problem.model.channels() * we.problem.grid.steps * nb
@@ -476,7 +505,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world, "steps": K_, "warmup": W_,
         "ms_per_step": 1e3 * t_max / K_, "higher_is_better": True,
-        "scaling": "strong" if args.workload == "batch4096" else "weak", "vs_baseline": None,
+        "scaling": "strong" if args.workload == "batch4096" or blocked else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d))", "config": workload_config(args.workload, world),
         "e2e": {"value": e2e_value, "unit": "steps/s", "h2d_bytes_per_step": h2d // K_,
                 "d2h_bytes_per_step": d2h // K_, "note": "one run_ism_batch call of K outer iterations from host "

@@ -144,7 +144,11 @@ typedef struct qoc_ism_config_v1 {
   int32_t log_exact_objective;
   int32_t checkpoint_stride;   /* forwarded to gradient sweeps; results are bit-identical */
   int32_t partition;           /* enum qoc_partition */
-  int32_t reserved;
+  int32_t blocks;              /* BITFLIP + ASSEMBLED: contiguous subinterval blocks G of the
+                                  blocked boundary refresh (1 <= G <= L; G = L is the reference's
+                                  per-subinterval chain, ism.cpp:298-312).  0 = direct node sweeps
+                                  on one GPU, G = world size under a communicator.  Ignored by the
+                                  other kinds. */
   double eta;
   const int32_t* node_index;   /* [L+1] for QOC_PARTITION_EXPLICIT */
 } qoc_ism_config_v1;
@@ -217,6 +221,20 @@ int32_t qoc_objective_gradient(qoc_ctx* ctx, const qoc_problem_v1* problem, cons
 /* assemble_propagator: prop_out [B][d*d] complex, column-major (linear kinds only). */
 int32_t qoc_assemble_propagator(qoc_ctx* ctx, const qoc_problem_v1* problem, const double* u,
                                 double* prop_out);
+
+/* Multi-GPU: one process and one context per GPU.  Rank 0 draws the NCCL unique
+ * id (QOC_COMM_ID_BYTES bytes), the host side broadcasts it, and every rank binds its context
+ * with qoc_ctx_init_comm.  A bit-flip run with plan ASSEMBLED then shards its subinterval blocks
+ * over the world (blocks = 0 -> one block per rank): rank r owns blocks [r G/W, (r+1) G/W),
+ * computes their tasks and block products, and ONE in-place ncclAllGather per outer iteration
+ * exchanges block products, entry values, residuals and controls.  Every rank returns the same
+ * controls and records.  world = 1 with id = NULL releases the communicator (with an id it
+ * builds a one-rank communicator: the exchange path runs, trivially).  NCCL is loaded at run time
+ * (dlopen "libnccl.so.2"; QOC_NCCL_LIBRARY overrides); failures return QOC_ENCCL.  Other kinds
+ * run as independent replicas under a communicator (config 5 shards problems on the host). */
+#define QOC_COMM_ID_BYTES 128
+int32_t qoc_comm_unique_id(void* id_out, size_t len);
+int32_t qoc_ctx_init_comm(qoc_ctx* ctx, int32_t rank, int32_t world, const void* id, size_t len);
 
 /* Kernel-launch counter of this context (for the bench's gpu_launches claim). */
 int64_t qoc_ctx_launch_count(const qoc_ctx* ctx);

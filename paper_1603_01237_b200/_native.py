@@ -52,6 +52,10 @@ def lib():
         L.qoc_objective_gradient.restype = i32
         L.qoc_assemble_propagator.argtypes = [vp, vp, dp, dp]
         L.qoc_assemble_propagator.restype = i32
+        L.qoc_comm_unique_id.argtypes = [vp, C.c_size_t]
+        L.qoc_comm_unique_id.restype = i32
+        L.qoc_ctx_init_comm.argtypes = [vp, i32, i32, vp, C.c_size_t]
+        L.qoc_ctx_init_comm.restype = i32
         if L.qoc_abi_version() != abi.QOC_ABI_VERSION:
             raise NativeMissing("libqoc_b200.so ABI version mismatch; rebuild")
         _lib = L
@@ -97,6 +101,15 @@ class Context:
             i += 1
         return out
 
+    def init_comm(self, rank: int, world: int, unique_id: bytes | None = None) -> None:
+        """Bind this context to rank `rank` of a `world`-GPU NCCL communicator (qoc_ctx_init_comm);
+        `unique_id` is rank 0's ``comm_unique_id()`` broadcast to every rank."""
+        buf = C.create_string_buffer(bytes(unique_id), abi.COMM_ID_BYTES) if unique_id else None
+        code = self.lib.qoc_ctx_init_comm(self.handle, int(rank), int(world), buf,
+                                          abi.COMM_ID_BYTES if buf is not None else 0)
+        if code != abi.QOC_OK:
+            raise RuntimeError(f"qoc_ctx_init_comm failed ({code}): {self.last_error()}")
+
     def close(self):
         if self.handle:
             self.lib.qoc_ctx_destroy(self.handle)
@@ -107,6 +120,15 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+def comm_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0 draws it; the host side broadcasts it)."""
+    buf = C.create_string_buffer(abi.COMM_ID_BYTES)
+    code = lib().qoc_comm_unique_id(buf, abi.COMM_ID_BYTES)
+    if code != abi.QOC_OK:
+        raise RuntimeError(f"qoc_comm_unique_id failed ({code}): NCCL unavailable")
+    return buf.raw
 
 
 def default_context(device: int = -1) -> Context:

@@ -46,7 +46,7 @@ class IsmConfigV1(C.Structure):
         ("subintervals", C.c_int32), ("workers", C.c_int32), ("max_outer", C.c_int32),
         ("variant", C.c_int32), ("plan", C.c_int32), ("compute_error", C.c_int32),
         ("log_exact_objective", C.c_int32), ("checkpoint_stride", C.c_int32),
-        ("partition", C.c_int32), ("reserved", C.c_int32), ("eta", C.c_double),
+        ("partition", C.c_int32), ("blocks", C.c_int32), ("eta", C.c_double),
         ("node_index", _ip),
     ]
 
@@ -79,6 +79,7 @@ class ProfileV1(C.Structure):
 
 
 OPT_PROFILE, OPT_FLUSH_L2_BYTES = 1, 2
+COMM_ID_BYTES = 128
 
 
 class CtxOptsV1(C.Structure):

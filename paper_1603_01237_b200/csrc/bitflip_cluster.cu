@@ -27,13 +27,15 @@ namespace {
 __device__ __forceinline__ double2 flip_coef(double2 ab, int one) { return cx(ab.x, one ? ab.y : -ab.y); }
 
 template <int LOG2E, int LOG2T, int LOG2CL, int MODE>
-__global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_cluster_kernel(DevProblem P, DevRun R, int which, int k) {
+__global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_cluster_kernel(DevProblem P, DevRun R, int which, int k,
+                                                                             SweepRange SR) {
   constexpr bool PUSH = MODE >= 1, ASYNC = MODE == 2;
   constexpr int E = 1 << LOG2E, T = 1 << LOG2T, CL = 1 << LOG2CL, Dl = E * T, N = LOG2E + LOG2T + LOG2CL;
   if (R.kdev) k = *R.kdev;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
-  const int b = blockIdx.y, dir = blockIdx.z;
+  const int nl = SR.nloc > 0 ? SR.nloc : 1;
+  const int b = blockIdx.y / nl, g = SR.g0 + (int)(blockIdx.y % nl), dir = blockIdx.z;
   if (R.done[b] || R.status[b]) return;  // uniform over the cluster (same problem)
   if (which == 1 && dir == 1) return;
   __shared__ __align__(16) double2 buf[2][Dl];
@@ -200,13 +202,18 @@ __global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_cluster_kernel(Dev
     cayley(sh, sweeps < 0 ? 0 : sweeps);
   };
 
+  // node range [na, nz] of this sweep (SweepRange, common.cuh); the full horizon also writes
+  // its two end nodes, a block of the blocked plan only its interior nodes
+  const bool full = SR.nloc == 0;
+  const int na = full ? 0 : SR.bnode[g], nz = full ? P.L : SR.bnode[g + 1];
   if (dir == 0) {
-    load(P.init + (size_t)b * d);
-    if (which == 0) store(R.psi_nodes + nb);
-    int nxt = 1;
-    for (int j = 0; j < P.K; ++j) {
+    load(full ? P.init + (size_t)b * d : R.psi_nodes + nb + (size_t)na * d);
+    if (which == 0 && full) store(R.psi_nodes + nb);
+    int nxt = na + 1;
+    const int last = full ? nz : nz - 1;
+    for (int j = P.node[na]; j < P.node[nz]; ++j) {
       step(u + (size_t)j * C, half);
-      if (which == 0 && nxt <= P.L && P.node[nxt] == j + 1) {
+      if (which == 0 && nxt <= last && P.node[nxt] == j + 1) {
         store(R.psi_nodes + nb + (size_t)nxt * d);
         ++nxt;
       }
@@ -234,12 +241,13 @@ __global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_cluster_kernel(Dev
       }
     }
   } else {
-    load(P.targ + (size_t)b * d);
-    store(R.chi_nodes + nb + (size_t)P.L * d);
-    int prev = P.L - 1;
-    for (int j = P.K - 1; j >= 0; --j) {
+    load(full ? P.targ + (size_t)b * d : R.chi_nodes + nb + (size_t)nz * d);
+    if (full) store(R.chi_nodes + nb + (size_t)P.L * d);
+    int prev = nz - 1;
+    const int first = full ? na : na + 1;
+    for (int j = P.node[nz] - 1; j >= P.node[na]; --j) {
       step(u + (size_t)j * C, -half);
-      if (prev >= 0 && P.node[prev] == j) {
+      if (prev >= first && P.node[prev] == j) {
         store(R.chi_nodes + nb + (size_t)prev * d);
         --prev;
       }
@@ -250,7 +258,8 @@ __global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_cluster_kernel(Dev
 }
 
 template <int LOG2E, int LOG2T, int LOG2CL, int MODE = 0>
-cudaError_t launch_cluster(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
+cudaError_t launch_cluster(const DevProblem& P, const DevRun& R, int which, int k, const SweepRange& SR,
+                           cudaStream_t st) {
   auto kern = bitflip_horizon_cluster_kernel<LOG2E, LOG2T, LOG2CL, MODE>;
   constexpr int CL = 1 << LOG2CL;
   if (CL > 8) {
@@ -258,7 +267,7 @@ cudaError_t launch_cluster(const DevProblem& P, const DevRun& R, int which, int 
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(CL, P.B, 2);
+  cfg.gridDim = dim3(CL, P.B * (SR.nloc > 0 ? SR.nloc : 1), 2);
   cfg.blockDim = dim3(1 << LOG2T, 1, 1);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
@@ -269,7 +278,7 @@ cudaError_t launch_cluster(const DevProblem& P, const DevRun& R, int which, int 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, P, R, which, k);
+  return cudaLaunchKernelEx(&cfg, kern, P, R, which, k, SR);
 }
 
 }  // namespace
@@ -283,29 +292,29 @@ cudaError_t launch_cluster(const DevProblem& P, const DevRun& R, int which, int 
 // with 2 / 2 / 4 amplitudes, "8x2", "16x1".  Measured per config-3 outer iteration (node
 // sweeps): single CTA 22.8 ms; barrier variants 20.0-21.2 ms (MEMBAR.ALL.GPU per cluster
 // barrier); 16a 13.1 ms, 8a 13.8, 2a 16.4, 8b 19.4, 4a 19.7.
-cudaError_t bitflip_horizon_cluster(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st,
-                                    bool* used) {
+cudaError_t bitflip_horizon_cluster(const DevProblem& P, const DevRun& R, int which, int k, const SweepRange& SR,
+                                    cudaStream_t st, bool* used) {
   *used = false;
   if (P.nspins != 10 || P.C > 4) return cudaSuccess;
   const char* e = std::getenv("QOC_BF_CLUSTER");
   const char* shape = e ? e : "16a";
   if (shape[0] == '0') return cudaSuccess;
   cudaError_t r;
-  if (shape[0] == '1' && shape[1] == '6' && shape[2] != 'a') r = launch_cluster<0, 6, 4>(P, R, which, k, st);
-  else if (shape[2] == '2') r = launch_cluster<1, 6, 3>(P, R, which, k, st);
-  else if (shape[0] == '8' && shape[1] == 'a') r = launch_cluster<0, 7, 3, 2>(P, R, which, k, st);
-  else if (shape[0] == '1' && shape[1] == '6' && shape[2] == 'a') r = launch_cluster<0, 6, 4, 2>(P, R, which, k, st);
-  else if (shape[0] == '4' && shape[1] == 'a') r = launch_cluster<1, 7, 2, 2>(P, R, which, k, st);
-  else if (shape[0] == '2' && shape[1] == 'a') r = launch_cluster<2, 7, 1, 2>(P, R, which, k, st);
-  else if (shape[0] == '8' && shape[1] == 'b') r = launch_cluster<1, 6, 3, 2>(P, R, which, k, st);
-  else if (shape[1] == 'p') r = launch_cluster<0, 7, 3, 1>(P, R, which, k, st);
-  else if (shape[1] == 'q') r = launch_cluster<1, 6, 3, 1>(P, R, which, k, st);
-  else if (shape[0] == '4') r = launch_cluster<1, 7, 2, 1>(P, R, which, k, st);
-  else if (shape[0] == '2') r = launch_cluster<2, 7, 1, 1>(P, R, which, k, st);
-  else r = launch_cluster<0, 7, 3>(P, R, which, k, st);
+  if (shape[0] == '1' && shape[1] == '6' && shape[2] != 'a') r = launch_cluster<0, 6, 4>(P, R, which, k, SR, st);
+  else if (shape[2] == '2') r = launch_cluster<1, 6, 3>(P, R, which, k, SR, st);
+  else if (shape[0] == '8' && shape[1] == 'a') r = launch_cluster<0, 7, 3, 2>(P, R, which, k, SR, st);
+  else if (shape[0] == '1' && shape[1] == '6' && shape[2] == 'a') r = launch_cluster<0, 6, 4, 2>(P, R, which, k, SR, st);
+  else if (shape[0] == '4' && shape[1] == 'a') r = launch_cluster<1, 7, 2, 2>(P, R, which, k, SR, st);
+  else if (shape[0] == '2' && shape[1] == 'a') r = launch_cluster<2, 7, 1, 2>(P, R, which, k, SR, st);
+  else if (shape[0] == '8' && shape[1] == 'b') r = launch_cluster<1, 6, 3, 2>(P, R, which, k, SR, st);
+  else if (shape[1] == 'p') r = launch_cluster<0, 7, 3, 1>(P, R, which, k, SR, st);
+  else if (shape[1] == 'q') r = launch_cluster<1, 6, 3, 1>(P, R, which, k, SR, st);
+  else if (shape[0] == '4') r = launch_cluster<1, 7, 2, 1>(P, R, which, k, SR, st);
+  else if (shape[0] == '2') r = launch_cluster<2, 7, 1, 1>(P, R, which, k, SR, st);
+  else r = launch_cluster<0, 7, 3>(P, R, which, k, SR, st);
   if (r != cudaSuccess && !e) {  // 16-CTA clusters are non-portable: fall back to 8
     cudaGetLastError();
-    r = launch_cluster<0, 7, 3, 2>(P, R, which, k, st);
+    r = launch_cluster<0, 7, 3, 2>(P, R, which, k, SR, st);
   }
   *used = r == cudaSuccess;
   if (r != cudaSuccess) cudaGetLastError();  // e.g. no cluster support: the single-CTA kernel

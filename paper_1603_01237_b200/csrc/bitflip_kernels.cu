@@ -23,6 +23,8 @@
 // registers across all its sweeps, so a sweep is n LDS.128 + n complex FMAs per amplitude.  Spin i <-> bit n-1-i (spin_operator,
 // models.cpp:296-318).  The forward trajectory of a task (len+1 states, 16 KB each at
 // d = 1024) lives in HBM/L2 (R.traj); the adjoint sweep reads it back for the gradient.
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace qoc {
@@ -218,7 +220,7 @@ __global__ void __launch_bounds__(1 << LOG2T) bitflip_task_kernel(DevProblem P, 
   using F_ = Bf<LOG2E, LOG2T>;
   constexpr int E = 1 << LOG2E, T = 1 << LOG2T;
   using Vec = double2[1 << LOG2E];
-  const int n = blockIdx.x, b = blockIdx.y;
+  const int n = A.n_lo + blockIdx.x, b = blockIdx.y;
   if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
   extern __shared__ __align__(16) unsigned char smem[];
   F_ F = make_bf<LOG2E, LOG2T>(P, b, smem);
@@ -346,12 +348,16 @@ __global__ void __launch_bounds__(1 << LOG2T) bitflip_task_kernel(DevProblem P, 
 // node_sweeps (ism.cpp:35-84) / exact payoff (objective.cpp:93-100) over the full horizon.
 // blockIdx.y = 0: forward nodes psi_n (which = 0) or the exact payoff (which = 1);
 // blockIdx.y = 1: adjoint nodes chi_n seeded with the target (ism.cpp:72), which = 0 only.
+// SR.nloc > 0: the interior nodes of blocks [SR.g0, SR.g0 + SR.nloc) of the blocked plan, each
+// seeded from its chain-formed end nodes (blockIdx.x = b * nloc + local block).
 template <int LOG2E, int LOG2T>
-__global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_kernel(DevProblem P, DevRun R, int which, int k) {
+__global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_kernel(DevProblem P, DevRun R, int which, int k,
+                                                                     SweepRange SR) {
   if (R.kdev) k = *R.kdev;
   using F_ = Bf<LOG2E, LOG2T>;
   constexpr int E = 1 << LOG2E, T = 1 << LOG2T;
-  const int b = blockIdx.x, dir = blockIdx.y;
+  const int nl = SR.nloc > 0 ? SR.nloc : 1;
+  const int b = blockIdx.x / nl, g = SR.g0 + (int)(blockIdx.x % nl), dir = blockIdx.y;
   if (R.done[b] || R.status[b]) return;
   if (which == 1 && dir == 1) return;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -361,6 +367,9 @@ __global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_kernel(DevProblem 
   const double half = 0.5 * P.dt;
   const double* u = R.u + (size_t)b * P.K * C;
   const size_t nb = (size_t)b * (P.L + 1) * d;
+  // node range [na, nz] of this sweep; the full horizon also writes its two end nodes
+  const bool full = SR.nloc == 0;
+  const int na = full ? 0 : SR.bnode[g], nz = full ? P.L : SR.bnode[g + 1];
   bool ok = true;
   double2 x[E];
   auto step = [&](const double* uj, double sh) {
@@ -369,12 +378,13 @@ __global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_kernel(DevProblem 
     F.cayley(x, sh, sweeps < 0 ? 0 : sweeps);
   };
   if (dir == 0) {
-    load_state<E>(x, P.init + (size_t)b * d, t, T);
-    if (which == 0) store_state<E>(x, R.psi_nodes + nb, t, T);
-    int nxt = 1;
-    for (int j = 0; j < P.K; ++j) {
+    load_state<E>(x, full ? P.init + (size_t)b * d : R.psi_nodes + nb + (size_t)na * d, t, T);
+    if (which == 0 && full) store_state<E>(x, R.psi_nodes + nb, t, T);
+    int nxt = na + 1;
+    const int last = full ? nz : nz - 1;  // highest node this sweep writes
+    for (int j = P.node[na]; j < P.node[nz]; ++j) {
       step(u + (size_t)j * C, half);
-      if (which == 0 && nxt <= P.L && P.node[nxt] == j + 1) {
+      if (which == 0 && nxt <= last && P.node[nxt] == j + 1) {
         store_state<E>(x, R.psi_nodes + nb + (size_t)nxt * d, t, T);
         ++nxt;
       }
@@ -391,17 +401,49 @@ __global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_kernel(DevProblem 
       }
     }
   } else {
-    load_state<E>(x, P.targ + (size_t)b * d, t, T);
-    store_state<E>(x, R.chi_nodes + nb + (size_t)P.L * d, t, T);
-    int prev = P.L - 1;
-    for (int j = P.K - 1; j >= 0; --j) {
+    load_state<E>(x, full ? P.targ + (size_t)b * d : R.chi_nodes + nb + (size_t)nz * d, t, T);
+    if (full) store_state<E>(x, R.chi_nodes + nb + (size_t)P.L * d, t, T);
+    int prev = nz - 1;
+    const int first = full ? na : na + 1;  // lowest node this sweep writes
+    for (int j = P.node[nz] - 1; j >= P.node[na]; --j) {
       step(u + (size_t)j * C, -half);
-      if (prev >= 0 && P.node[prev] == j) {
+      if (prev >= first && P.node[prev] == j) {
         store_state<E>(x, R.chi_nodes + nb + (size_t)prev * d, t, T);
         --prev;
       }
     }
   }
+  if (!ok && t == 0 && R.err_flags) atomicOr(R.err_flags, 2);
+}
+
+// Block products of the blocked plan: P_g = A_{j1-1} ... A_{j0} over the steps of block g,
+// column c = the basis state e_c carried through the block's Cayley steps (the propagator
+// assembly of propagation.cpp:236-249 on the bit-flip operator: d independent column sweeps
+// instead of one dense LU per step).  blockIdx.x = column, blockIdx.y = local block,
+// blockIdx.z = problem (B = 1 on this path).  Writes column-major into the rank's slab.
+template <int LOG2E, int LOG2T>
+__global__ void __launch_bounds__(1 << LOG2T) bitflip_block_kernel(DevProblem P, DevRun R, DevBlocks BK, int g0) {
+  using F_ = Bf<LOG2E, LOG2T>;
+  constexpr int E = 1 << LOG2E, T = 1 << LOG2T;
+  const int col = blockIdx.x, g = g0 + blockIdx.y, b = blockIdx.z;
+  if (R.done[b] || R.status[b]) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  F_ F = make_bf<LOG2E, LOG2T>(P, b, smem);
+  const int d = P.d, C = P.C, t = F.t;
+  const BfOps O{P.bf_diag + (size_t)b * d, P.bf_coef + (size_t)b * C * P.nspins, P.bf_axis, C, P.nspins};
+  const double half = 0.5 * P.dt;
+  const double* u = R.u + (size_t)b * P.K * C;
+  bool ok = true;
+  double2 x[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) x[e] = cx(t + e * T == col ? 1.0 : 0.0, 0.0);
+  const int j0 = P.node[BK.bnode[g]], j1 = P.node[BK.bnode[g + 1]];
+  for (int j = j0; j < j1; ++j) {
+    const int sweeps = F.begin_step(O, u + (size_t)j * C, half);
+    ok &= sweeps >= 0;
+    F.cayley(x, half, sweeps < 0 ? 0 : sweeps);
+  }
+  store_state<E>(x, BK.block(g, d) + (size_t)col * d, t, T);
   if (!ok && t == 0 && R.err_flags) atomicOr(R.err_flags, 2);
 }
 
@@ -411,17 +453,29 @@ cudaError_t launch_task(const DevProblem& P, const DevRun& R, const TaskArgs& A,
   auto kern = bitflip_task_kernel<LOG2E, LOG2T>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<dim3(P.L, P.B), 1 << LOG2T, smem, st>>>(P, R, A, ignore_done);
+  kern<<<dim3(A.n_cnt > 0 ? A.n_cnt : P.L, P.B), 1 << LOG2T, smem, st>>>(P, R, A, ignore_done);
   return cudaGetLastError();
 }
 
 template <int LOG2E, int LOG2T>
-cudaError_t launch_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
+cudaError_t launch_horizon(const DevProblem& P, const DevRun& R, int which, int k, const SweepRange& SR,
+                           cudaStream_t st) {
   const size_t smem = bf_smem(P.d);
   auto kern = bitflip_horizon_kernel<LOG2E, LOG2T>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<dim3(P.B, 2), 1 << LOG2T, smem, st>>>(P, R, which, k);
+  kern<<<dim3(P.B * (SR.nloc > 0 ? SR.nloc : 1), 2), 1 << LOG2T, smem, st>>>(P, R, which, k, SR);
+  return cudaGetLastError();
+}
+
+template <int LOG2E, int LOG2T>
+cudaError_t launch_blocks(const DevProblem& P, const DevRun& R, const DevBlocks& BK, int g0, int nloc,
+                          cudaStream_t st) {
+  const size_t smem = bf_smem(P.d);
+  auto kern = bitflip_block_kernel<LOG2E, LOG2T>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<dim3(P.d, nloc, P.B), 1 << LOG2T, smem, st>>>(P, R, BK, g0);
   return cudaGetLastError();
 }
 
@@ -444,27 +498,54 @@ cudaError_t bitflip_task(const DevProblem& P, const DevRun& R, const TaskArgs& A
   return cudaErrorNotSupported;
 }
 
-cudaError_t bitflip_horizon_cluster(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st,
-                                    bool* used);
+cudaError_t bitflip_horizon_cluster(const DevProblem& P, const DevRun& R, int which, int k, const SweepRange& SR,
+                                    cudaStream_t st, bool* used);
 
-cudaError_t bitflip_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
+cudaError_t bitflip_horizon_range(const DevProblem& P, const DevRun& R, int which, int k, const SweepRange& SR,
+                                  cudaStream_t st) {
   if (P.C > 4) return cudaErrorNotSupported;
   {  // d = 1024: the node sweeps split over a thread-block cluster (bitflip_cluster.cu)
     bool used = false;
-    cudaError_t e = bitflip_horizon_cluster(P, R, which, k, st, &used);
+    cudaError_t e = bitflip_horizon_cluster(P, R, which, k, SR, st, &used);
     if (e != cudaSuccess || used) return e;
   }
   switch (P.nspins) {
-    case 5: return launch_horizon<0, 5>(P, R, which, k, st);
-    case 6: return launch_horizon<0, 6>(P, R, which, k, st);
-    case 7: return launch_horizon<0, 7>(P, R, which, k, st);
-    case 8: return launch_horizon<0, 8>(P, R, which, k, st);
-    case 9: return launch_horizon<0, 9>(P, R, which, k, st);
+    case 5: return launch_horizon<0, 5>(P, R, which, k, SR, st);
+    case 6: return launch_horizon<0, 6>(P, R, which, k, SR, st);
+    case 7: return launch_horizon<0, 7>(P, R, which, k, SR, st);
+    case 8: return launch_horizon<0, 8>(P, R, which, k, SR, st);
+    case 9: return launch_horizon<0, 9>(P, R, which, k, SR, st);
     // node sweeps at d = 1024: 128 threads x 8 amplitudes (measured per outer iteration of
     // config 3: 24.3 ms, vs 25.2 / 25.9 / 36.3 ms at 256 / 512 / 1024 threads)
-    case 10: return launch_horizon<3, 7>(P, R, which, k, st);
-    case 11: return launch_horizon<2, 9>(P, R, which, k, st);
-    case 12: return launch_horizon<3, 9>(P, R, which, k, st);
+    case 10: return launch_horizon<3, 7>(P, R, which, k, SR, st);
+    case 11: return launch_horizon<2, 9>(P, R, which, k, SR, st);
+    case 12: return launch_horizon<3, 9>(P, R, which, k, SR, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+cudaError_t bitflip_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
+  return bitflip_horizon_range(P, R, which, k, SweepRange{nullptr, 0, 0}, st);
+}
+
+// QOC_BF_BLOCK_SHAPE = "8" selects 256 threads x 4 amplitudes for d = 1024 (default 128 x 8).
+cudaError_t bitflip_block_products(const DevProblem& P, const DevRun& R, const DevBlocks& BK, int g0, int nloc,
+                                   cudaStream_t st) {
+  if (P.C > 4) return cudaErrorNotSupported;
+  if (nloc <= 0) return cudaSuccess;
+  switch (P.nspins) {
+    case 5: return launch_blocks<0, 5>(P, R, BK, g0, nloc, st);
+    case 6: return launch_blocks<0, 6>(P, R, BK, g0, nloc, st);
+    case 7: return launch_blocks<0, 7>(P, R, BK, g0, nloc, st);
+    case 8: return launch_blocks<0, 8>(P, R, BK, g0, nloc, st);
+    case 9: return launch_blocks<1, 8>(P, R, BK, g0, nloc, st);
+    case 10: {
+      const char* e = std::getenv("QOC_BF_BLOCK_SHAPE");
+      if (e && e[0] == '8') return launch_blocks<2, 8>(P, R, BK, g0, nloc, st);
+      return launch_blocks<3, 7>(P, R, BK, g0, nloc, st);
+    }
+    case 11: return launch_blocks<3, 8>(P, R, BK, g0, nloc, st);
+    case 12: return launch_blocks<3, 9>(P, R, BK, g0, nloc, st);
   }
   return cudaErrorNotSupported;
 }

@@ -195,6 +195,39 @@ struct TaskArgs {
   int weighted;  // task weight K/len
   int inner;     // inner gradient iterations
   double rho;
+  int n_lo = 0;   // first subinterval of this launch (blocked plan: this rank's subintervals)
+  int n_cnt = 0;  // subintervals in this launch (0 = all L)
+};
+
+// Blocked boundary refresh (bit-flip kind; SURVEY §8(e) option A).  The L subintervals form G
+// contiguous blocks, block g = subintervals [bnode[g], bnode[g+1]); rank r of W owns blocks
+// [r*bpr, (r+1)*bpr), bpr = G / W.  Each rank's exchange slab holds its block products
+// P_g = A_{last} ... A_{first} (d x d, column-major: column c = the propagated basis state e_c),
+// then its subintervals' entry values and residuals, then its steps' controls; one in-place
+// all-gather of the slabs per outer iteration is the only collective.
+struct DevBlocks {
+  int G, bpr, W, rank;
+  const int* bnode;   // [G+1] block boundaries as subinterval indices
+  double2* slab;      // [W][slab_elems] (double2 units)
+  size_t slab_elems;  // per rank
+  int lmax, kmax;     // padded subinterval / step counts per rank
+  __host__ __device__ double2* block(int g, int d) const {
+    return slab + (size_t)(g / bpr) * slab_elems + (size_t)(g % bpr) * d * d;
+  }
+  __host__ __device__ double* scalars(int r, int d) const {  // [2][lmax]: entry, err
+    return reinterpret_cast<double*>(slab + (size_t)r * slab_elems + (size_t)bpr * d * d);
+  }
+  __host__ __device__ double* controls(int r, int d) const {  // [kmax][C]
+    return scalars(r, d) + 2 * (size_t)lmax;
+  }
+};
+
+// Node sweeps over part of the horizon: the blocks [g0, g0 + nloc) of a DevBlocks split, each
+// seeded from its chain-formed end nodes (psi at bnode[g], chi at bnode[g+1]) and writing only
+// its interior nodes.  nloc = 0: the full horizon (node_sweeps, ism.cpp:35-84).
+struct SweepRange {
+  const int* bnode;
+  int g0, nloc;
 };
 
 }  // namespace qoc

@@ -9,6 +9,8 @@
 // device, so a batch of independent problems runs in one launch sequence with no host
 // round trip per iteration.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is resolved at run time (dlopen), see nccl_api()
 
 #include <algorithm>
 #include <chrono>
@@ -53,6 +55,9 @@ struct qoc_ctx {
   size_t khost_n = 0;
   void* prob_slots = nullptr;  // Slots* (driver.cu anonymous namespace)
   void* run_slots = nullptr;
+  // multi-GPU (qoc_ctx_init_comm): rank of world; the NCCL communicator when world > 1
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
 };
 
 namespace {
@@ -526,6 +531,10 @@ struct Launcher {
     if (e == cudaErrorNotSupported) fail(QOC_ELOGIC, std::string(what) + ": not supported for this model kind");
     ck(e, what);
   }
+  void extra(int64_t n) {  // launch sites that issue more than one kernel
+    ctx->launches += n;
+    if (in_iteration) ctx->prof.iteration_launches += n;
+  }
   void operator()(cudaError_t e, const char* what) {  // already-launched form (no timing)
     ++ctx->launches;
     if (e == cudaErrorNotSupported) fail(QOC_ELOGIC, std::string(what) + ": not supported for this model kind");
@@ -596,6 +605,54 @@ bool disabled_path(const char* what) {
   return e && std::strstr(e, what) != nullptr;
 }
 
+// NCCL entry points resolved at run time: libqoc_b200.so links no NCCL, so single-GPU use
+// needs none; in a PyTorch process dlopen("libnccl.so.2") returns the NCCL torch already
+// loaded (one NCCL per process), elsewhere the system one.
+struct NcclApi {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+  std::string why;
+  bool ok() const { return get_unique_id && comm_init_rank && comm_destroy && all_gather && error_string; }
+};
+
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = nullptr;
+    const char* env = std::getenv("QOC_NCCL_LIBRARY");
+    for (const char* name : {env, "libnccl.so.2", "libnccl.so"}) {
+      if (name && (h = dlopen(name, RTLD_NOW | RTLD_GLOBAL))) break;
+    }
+    if (!h) {
+      a.why = std::string("cannot load libnccl.so.2: ") + (dlerror() ? dlerror() : "not found");
+      return a;
+    }
+    a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
+    a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+    if (!a.ok()) a.why = "libnccl.so.2 lacks an expected entry point";
+    return a;
+  }();
+  return api;
+}
+
+void nccl_ck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) fail(QOC_ENCCL, std::string(what) + ": " + nccl_api().error_string(r));
+}
+
+// Balanced contiguous split of L subintervals into G blocks (the first L mod G blocks get one
+// more), as subinterval boundary indices [G+1].
+std::vector<int> block_nodes(int L, int G) {
+  std::vector<int> b{0};
+  for (int g = 0; g < G; ++g) b.push_back(b.back() + L / G + (g < L % G ? 1 : 0));
+  return b;
+}
+
 }  // namespace
 
 extern "C" {
@@ -635,6 +692,7 @@ void qoc_ctx_destroy(qoc_ctx* ctx) {
   if (ctx->flush_buf) cudaFree(ctx->flush_buf);
   if (ctx->khost) cudaFreeHost(ctx->khost);
   if (ctx->gcache) cudaGraphExecDestroy(ctx->gcache);
+  if (ctx->comm && nccl_api().ok()) nccl_api().comm_destroy(ctx->comm);
   delete static_cast<Slots*>(ctx->prob_slots);
   delete static_cast<Slots*>(ctx->run_slots);
   delete ctx;
@@ -685,6 +743,39 @@ const char* qoc_ctx_last_error(const qoc_ctx* ctx) { return ctx ? ctx->last_erro
 
 int64_t qoc_ctx_launch_count(const qoc_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int32_t qoc_comm_unique_id(void* out, size_t len) {
+  if (!out || len < NCCL_UNIQUE_ID_BYTES) return QOC_EINVAL;
+  const NcclApi& a = nccl_api();
+  if (!a.ok()) return QOC_ENCCL;
+  ncclUniqueId id;
+  if (a.get_unique_id(&id) != ncclSuccess) return QOC_ENCCL;
+  std::memcpy(out, &id, sizeof id);
+  return QOC_OK;
+}
+
+int32_t qoc_ctx_init_comm(qoc_ctx* ctx, int32_t rank, int32_t world, const void* id, size_t len) {
+  return guarded(ctx, [&] {
+    if (world < 1 || rank < 0 || rank >= world) fail(QOC_EINVAL, "rank must lie in [0, world)");
+    if (ctx->comm) {
+      nccl_api().comm_destroy(ctx->comm);
+      ctx->comm = nullptr;
+    }
+    ctx->rank = 0;
+    ctx->world = 1;
+    // world = 1 with an id: a one-rank communicator (the exchange path runs, trivially)
+    if (world > 1 || id) {
+      if (!id || len < NCCL_UNIQUE_ID_BYTES) fail(QOC_EINVAL, "a communicator of world > 1 needs the 128-byte NCCL unique id");
+      const NcclApi& a = nccl_api();
+      if (!a.ok()) fail(QOC_ENCCL, a.why);
+      ncclUniqueId uid;
+      std::memcpy(&uid, id, sizeof uid);
+      nccl_ck(a.comm_init_rank(&ctx->comm, world, uid, rank), "ncclCommInitRank");
+    }
+    ctx->rank = rank;
+    ctx->world = world;
+  });
+}
+
 int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_v1* cfg,
                     const qoc_solver_v1* solver, const double* u0, double* u_out, qoc_iter_record_v1* recs,
                     int32_t rec_cap, double* task_values, qoc_run_status_v1* status) {
@@ -703,11 +794,25 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
     if (rec_cap < cfg->max_outer + 1) fail(QOC_EINVAL, "rec_cap must be >= max_outer + 1");
     const std::vector<int> node = decomposition(p->steps, cfg->subintervals, cfg->partition, cfg->node_index);
     const int L = cfg->subintervals, B = p->batch, C = p->channels, K = p->steps;
-    // The bit-flip kind never forms its d x d one-step matrices (16 MB each at d = 1024): its
-    // boundary refresh always runs as direct node sweeps, which agree with the assembled
-    // chain to rounding (ism_test.cpp:248-265).
-    const bool direct = cfg->plan == QOC_PLAN_DIRECT || p->kind == QOC_KIND_BITFLIP || p->kind == QOC_KIND_DENSITY;
-    const bool assembled_interp = L > 1 && !split && !direct;
+    // Blocked boundary refresh (bit-flip kind, assembled plan, SURVEY §8(e) option A): G
+    // contiguous blocks of subintervals; each rank forms its blocks' d x d products, one
+    // all-gather exchanges them, every rank chains the G products into the block-boundary
+    // nodes and sweeps its blocks' interiors.  G = L is the reference's assembled plan
+    // (ism.cpp:298-312); blocks = 0 on one GPU keeps the direct node sweeps, which agree with
+    // the assembled chain to rounding (ism_test.cpp:248-265); on W GPUs it means G = W.
+    if (cfg->blocks < 0) fail(QOC_EINVAL, "blocks must be >= 0");
+    const int G = (p->kind == QOC_KIND_BITFLIP && !split && L > 1 && cfg->plan == QOC_PLAN_ASSEMBLED)
+                      ? (cfg->blocks > 0 ? cfg->blocks : (ctx->world > 1 ? ctx->world : 0))
+                      : 0;
+    const bool blocked = G > 0;
+    if (blocked) {
+      if (G > L) fail(QOC_EINVAL, "blocks must not exceed subintervals");
+      if (G % ctx->world != 0) fail(QOC_EINVAL, "blocks must be a multiple of the communicator size");
+      if (B != 1) fail(QOC_ELOGIC, "the blocked plan runs one problem per call (batch = 1)");
+    }
+    const bool direct = !blocked && (cfg->plan == QOC_PLAN_DIRECT || p->kind == QOC_KIND_BITFLIP ||
+                                     p->kind == QOC_KIND_DENSITY);
+    const bool assembled_interp = L > 1 && !split && !direct && !blocked;
     cudaStream_t st = ctx->stream;
     Launcher launch{ctx};
 
@@ -724,6 +829,53 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
     alloc_run(dp, rec_cap, node, assembled_interp, false, st, dr, pcache, split);
     const DevRun& R = dr.R;
     ck(cudaMemcpyAsync(R.u, u0, sizeof(double) * B * K * C, cudaMemcpyHostToDevice, st), "u0");
+    // blocked plan: the exchange slabs and this rank's blocks / subintervals
+    DevBlocks BK{};
+    int g_lo = 0, n_lo = 0, n_cnt = 0;
+    bool interior = false;
+    if (blocked) {
+      const std::vector<int> bn = block_nodes(L, G);
+      BK.G = G;
+      BK.W = ctx->world;
+      BK.rank = ctx->rank;
+      BK.bpr = G / BK.W;
+      for (int r = 0; r < BK.W; ++r) {
+        const int a = bn[r * BK.bpr], z = bn[(r + 1) * BK.bpr];
+        BK.lmax = std::max(BK.lmax, z - a);
+        BK.kmax = std::max(BK.kmax, node[z] - node[a]);
+      }
+      for (int g = 0; g < G; ++g) interior = interior || bn[g + 1] - bn[g] > 1;
+      const size_t dd = (size_t)P.d * P.d, scal = 2 * (size_t)BK.lmax + (size_t)BK.kmax * C;
+      BK.slab_elems = (size_t)BK.bpr * dd + (scal + 1) / 2;
+      BK.slab = dr.alloc<double2>((size_t)BK.W * BK.slab_elems);
+      int* bnd = dr.alloc<int>(G + 1);
+      ck(cudaMemcpyAsync(bnd, bn.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice, st), "block nodes");
+      BK.bnode = bnd;
+      g_lo = ctx->rank * BK.bpr;
+      n_lo = bn[g_lo];
+      n_cnt = bn[g_lo + BK.bpr] - n_lo;
+      // other ranks' interior nodes stay zero here (finite for the boundary check)
+      ck(cudaMemsetAsync(R.psi_nodes, 0, sizeof(double2) * (L + 1) * P.d, st), "memset");
+      ck(cudaMemsetAsync(R.chi_nodes, 0, sizeof(double2) * (L + 1) * P.d, st), "memset");
+    }
+    const SweepRange SR{BK.bnode, g_lo, BK.bpr};
+    // the one collective per outer iteration: every rank's slab (block products, entry values,
+    // residuals, controls) to every rank, in place, on the compute stream
+    auto exchange = [&](Launcher& ln) {
+      if (!blocked || !ctx->comm) return;
+      ln.run([&] { return slab_pack(P, R, BK, 1, st); }, "pack");
+      const size_t bytes = sizeof(double2) * BK.slab_elems;
+      nccl_ck(nccl_api().all_gather(BK.slab + (size_t)BK.rank * BK.slab_elems, BK.slab, bytes, ncclUint8, ctx->comm, st),
+              "ncclAllGather");
+      ln.run([&] { return slab_unpack(P, R, BK, 1, st); }, "unpack");
+    };
+    auto blocked_refresh = [&](Launcher& ln, const DevRun& RR, int k) {
+      ln.run([&] { return bitflip_block_products(P, RR, BK, g_lo, BK.bpr, st); }, "block products", true);
+      exchange(ln);
+      ln.run([&] { return block_chain(P, RR, BK, st); }, "chain");
+      ln.extra(G);  // the chain issues G + 1 kernels
+      if (interior) ln.run([&] { return bitflip_horizon_range(P, RR, 0, k, SR, st); }, "node sweeps", true);
+    };
     trace.mark("alloc + u0", st);
 
     const int max_outer = cfg->max_outer;
@@ -749,7 +901,9 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
       if (R.nm) launch(dense_nm_setup(P, R, st), "neumann coefficients");
       if (pcache) launch(pc_assemble(P, R, 0, st), "propagator cache");
       if (L > 1) {
-        if (assembled_interp) {
+        if (blocked) {
+          blocked_refresh(launch, R, 0);
+        } else if (assembled_interp) {
           if (!pcache) {
             TaskArgs A{M_ASSEMBLE, QOC_FORM_TRACKING, 1, 1, 0.0};
             launch(task(P, R, A, 0, st), "assemble");
@@ -773,6 +927,10 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
       if (assembled_interp) mode |= M_ASSEMBLE;
       if (L > 1 && split && !direct) mode |= M_LAGGED;
       TaskArgs A{mode, form, split ? 0 : 1, inner, solver->step_size};
+      if (blocked) {  // this rank's subintervals only
+        A.n_lo = n_lo;
+        A.n_cnt = n_cnt;
+      }
       std::vector<int> h_done(B), h_status(B);
       std::vector<cudaEvent_t> ev_end(max_outer + 2);
       for (auto& e : ev_end) ck(cudaEventCreate(&e), "event");
@@ -780,6 +938,17 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
       launch.in_iteration = true;
       // One outer iteration (ism.cpp:396-592) as a launch sequence on `st` (+ the side stream).
       auto body = [&](const DevRun& RR, int k) {
+        if (blocked) {
+          launch.run([&] { return task(P, RR, A, 0, st); }, "task", true);
+          blocked_refresh(launch, RR, k);  // block products at the updated control + exchange
+          launch.run([&] { return penalty_partials(P, RR, 0, st); }, "penalty");
+          launch.run([&] { return merge_iteration(P, RR, k, nullptr, st); }, "merge");
+          launch.run([&] { return boundary_update(P, RR, k, 0, 0, st); }, "boundary");
+          if (cfg->log_exact_objective) launch.run([&] { return exact_from_nodes(P, RR, k, st); }, "exact objective");
+          launch.run([&] { return finish_iteration_ex(P, RR, k, cfg->compute_error, cfg->eta,
+                                                      cfg->log_exact_objective, st); }, "finish");
+          return;
+        }
         if (onepass) {
           launch.run([&] { return apply_pending(P, RR, solver->step_size, st); }, "update");
           launch.run([&] { return penalty_partials(P, RR, 0, st); }, "penalty");
@@ -846,7 +1015,7 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
       // Long runs replay the iteration as one CUDA graph (captured once; the iteration index
       // is read from device memory), which removes the per-kernel launch gaps of the small
       // latency-bound configs.  Profiling mode keeps direct launches (per-launch events).
-      bool use_graph = !ctx->profile && max_outer >= 8;
+      bool use_graph = !ctx->profile && max_outer >= 8 && !(blocked && ctx->comm);
       cudaGraphExec_t gexec = nullptr;
       int* kdev = nullptr;
       int64_t launches_per_body = 0;
@@ -876,7 +1045,8 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
         put(&P, sizeof(P));
         put(&RG, sizeof(RG));
         const int cfgv[] = {form, (int)split, (int)direct, (int)pcache, (int)assembled_interp, L,
-                            cfg->compute_error, cfg->log_exact_objective, solver->inner_iterations, (int)onepass};
+                            cfg->compute_error, cfg->log_exact_objective, solver->inner_iterations, (int)onepass, G};
+        put(&BK, sizeof(BK));
         put(cfgv, sizeof(cfgv));
         const double cfgd[] = {solver->step_size, cfg->eta};
         put(cfgd, sizeof(cfgd));
@@ -976,7 +1146,12 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
           launch(pc_eval(P, R, T, 1, st), "trailing task");
         } else {
           TaskArgs T{M_ENTRY, form, split ? 0 : 1, 1, 0.0};
+          if (blocked) {
+            T.n_lo = n_lo;
+            T.n_cnt = n_cnt;
+          }
           launch(task(P, R, T, 1, st), "trailing task");
+          exchange(launch);  // every rank's final entry values
         }
         launch(trailing_values(P, R, st), "trailing");
       }

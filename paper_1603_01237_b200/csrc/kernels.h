@@ -27,6 +27,19 @@ cudaError_t tridiag_horizon(const DevProblem& P, const DevRun& R, int which, int
 // bit-flip spin register (d = 2^n, n <= 12)
 cudaError_t bitflip_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
 cudaError_t bitflip_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st);
+// node sweeps over the interior of blocks [SR.g0, SR.g0 + SR.nloc) of the blocked plan
+cudaError_t bitflip_horizon_range(const DevProblem& P, const DevRun& R, int which, int k, const SweepRange& SR,
+                                  cudaStream_t st);
+// block products P_g, g in [g0, g0 + nloc), into the exchange slab (column-major)
+cudaError_t bitflip_block_products(const DevProblem& P, const DevRun& R, const DevBlocks& BK, int g0, int nloc,
+                                   cudaStream_t st);
+
+// blocked plan glue (blocks.cu)
+cudaError_t block_chain(const DevProblem& P, const DevRun& R, const DevBlocks& BK, cudaStream_t st);
+cudaError_t slab_pack(const DevProblem& P, const DevRun& R, const DevBlocks& BK, int with_controls, cudaStream_t st);
+cudaError_t slab_unpack(const DevProblem& P, const DevRun& R, const DevBlocks& BK, int with_controls,
+                        cudaStream_t st);
+cudaError_t exact_from_nodes(const DevProblem& P, const DevRun& R, int k, cudaStream_t st);
 
 // split-step condensate
 cudaError_t strang_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);

@@ -100,6 +100,10 @@ class IsmConfig:
     checkpoint_stride: int = 0
     partition: str = "balanced"        # "uniform" = Decomposition::uniform; "explicit"
     node_index: Optional[Sequence[int]] = None
+    # bit-flip kind, assembled plan: contiguous subinterval blocks of the blocked boundary
+    # refresh (G = subintervals is the reference's per-subinterval chain); 0 = direct node
+    # sweeps on one GPU, one block per rank under a communicator (qoc_gpu.h qoc_ctx_init_comm)
+    blocks: int = 0
 
 
 @dataclass
@@ -273,6 +277,7 @@ def pack_config(cfg: IsmConfig):
     c.compute_error = int(cfg.compute_error)
     c.log_exact_objective = int(cfg.log_exact_objective)
     c.checkpoint_stride = cfg.checkpoint_stride
+    c.blocks = int(cfg.blocks)
     c.eta = cfg.eta
     keep = None
     if cfg.node_index is not None:

@@ -3,18 +3,34 @@ torch.distributed (NCCL on the GPU box, gloo in the CPU tests).
 
 * Batched problems (BASELINE config 5): contiguous problem blocks per rank, no data-path
   collective; controls and run records are gathered once at the end (``run_batch_sharded``).
-* Subinterval blocks (config 3 layout): rank g owns a contiguous block of subintervals.  The
-  one exchange step per outer iteration is an all-gather of the block products
+* Subinterval blocks (config 3 layout): rank r owns a contiguous run of subinterval blocks.
+  The one exchange step per outer iteration is an all-gather of the block products
   P_g = M_{last} ... M_{first} (``block_boundaries``); every rank then forms its own boundary
   states psi_n, chi_n exactly as ``compose_from_propagators`` (ism.cpp:298-312) would, using
   psi_start(g) = P_{g-1} ... P_0 psi_i and chi_end(g) = (P_{G-1} ... P_{g+1})^dag target.
-  This matches the serial chain to rounding (< 1e-11).
+  This matches the serial chain to rounding (< 1e-11).  On the GPU box the same exchange runs
+  inside libqoc_b200.so (one in-place ncclAllGather of per-rank slabs per outer iteration,
+  driver.cu); ``init_device_comm`` binds a device context to the torch.distributed world.
 """
 from __future__ import annotations
 
 from dataclasses import dataclass
 
 import numpy as np
+
+
+def init_device_comm(ctx, dist) -> None:
+    """Bind a libqoc_b200 context to this process's rank of the torch.distributed world: rank 0
+    draws the NCCL unique id, one broadcast hands it to every rank (qoc_ctx_init_comm)."""
+    from . import _native
+    world = dist.get_world_size() if dist is not None else 1
+    rank = dist.get_rank() if dist is not None else 0
+    if world == 1:
+        ctx.init_comm(0, 1)
+        return
+    obj = [_native.comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ctx.init_comm(rank, world, obj[0])
 
 
 def balanced_blocks(total: int, world: int) -> list[tuple[int, int]]:
@@ -106,32 +122,57 @@ def block_product(props: np.ndarray) -> np.ndarray:
     return P
 
 
-def block_boundaries(local_props: np.ndarray, initial: np.ndarray, target: np.ndarray, dist=None):
-    """Boundary states of this rank's subintervals after the one all-gather of block products.
+def block_nodes(L: int, G: int) -> list[int]:
+    """Balanced contiguous split of L subintervals into G blocks (the first L mod G blocks get one
+    more), as boundary indices [G+1] -- the split the device driver uses (driver.cu block_nodes)."""
+    if not 1 <= G <= L:
+        raise ValueError("blocks must lie in [1, subintervals]")
+    out = [0]
+    for g in range(G):
+        out.append(out[-1] + L // G + (1 if g < L % G else 0))
+    return out
 
-    local_props: (n_local, d, d) propagators M_n of this rank's contiguous subinterval block.
-    Returns (psi, chi): (n_local + 1, d) each -- psi_n at the block's nodes (forward chain,
-    psi_{n+1} = M_n psi_n) and chi_n (chi_n = M_n^dag chi_{n+1}, seeded with the target at the
-    final node), i.e. the rank's slice of compose_from_propagators (ism.cpp:298-312).
+
+def block_boundaries(local_props: np.ndarray, initial: np.ndarray, target: np.ndarray, dist=None,
+                     blocks_per_rank: int = 1):
+    """Boundary states of this rank's subintervals after the one all-gather of block products
+    (the host-side statement of the device's blocked refresh, driver.cu / blocks.cu).
+
+    local_props: (n_local, d, d) propagators M_n of this rank's contiguous subintervals, which
+    form `blocks_per_rank` contiguous blocks (balanced split).  Every rank contributes the same
+    number of blocks; one all-gather exchanges the G = world * blocks_per_rank block products
+    P_g = M_{last} ... M_{first}.  Then every rank chains them into the block-boundary nodes,
+    psi_{b[g+1]} = P_g psi_{b[g]} from psi_0 = initial and chi_{b[g]} = P_g^dag chi_{b[g+1]} from
+    chi_L = target (compose_from_propagators, ism.cpp:298-312, over blocks), and fills its blocks'
+    interior nodes from their chain-formed ends (the device runs node sweeps there).
+    Returns (psi, chi): (n_local + 1, d) each, the rank's slice of the serial chain's nodes.
     """
     world = dist.get_world_size() if dist is not None else 1
     rank = dist.get_rank() if dist is not None else 0
-    Pg = block_product(local_props)
-    if dist is None or world == 1:
-        blocks = [Pg]
-    else:  # the per-iteration exchange: G block products (complex128 as float64 pairs)
-        blocks = list(all_gather_blocks(dist, Pg[None], [1] * world))
-    psi = np.asarray(initial, dtype=np.complex128)
-    for g in range(rank):
-        psi = blocks[g] @ psi
-    chi = np.asarray(target, dtype=np.complex128)
-    for g in range(world - 1, rank, -1):
-        chi = blocks[g].conj().T @ chi
     n = len(local_props)
-    psis = [psi]
-    for m in range(n):
-        psis.append(local_props[m] @ psis[-1])
-    chis = [chi]
-    for m in range(n - 1, -1, -1):
-        chis.append(local_props[m].conj().T @ chis[-1])
-    return np.stack(psis), np.stack(chis[::-1])
+    inner = block_nodes(n, blocks_per_rank)
+    mine = np.stack([block_product(local_props[inner[q]:inner[q + 1]]) for q in range(blocks_per_rank)])
+    if dist is None or world == 1:
+        blocks = list(mine)
+    else:  # the per-iteration exchange: G block products (complex128 as float64 pairs)
+        blocks = list(all_gather_blocks(dist, mine, [blocks_per_rank] * world))
+    G = len(blocks)
+    # chain over all G blocks (every rank forms every block-boundary node)
+    psi_b = [np.asarray(initial, dtype=np.complex128)]
+    for g in range(G):
+        psi_b.append(blocks[g] @ psi_b[-1])
+    chi_b = [np.asarray(target, dtype=np.complex128)]
+    for g in range(G - 1, -1, -1):
+        chi_b.append(blocks[g].conj().T @ chi_b[-1])
+    chi_b = chi_b[::-1]
+    psis, chis = [None] * (n + 1), [None] * (n + 1)
+    for q in range(blocks_per_rank):
+        g = rank * blocks_per_rank + q
+        a, z = inner[q], inner[q + 1]
+        psis[a], psis[z] = psi_b[g], psi_b[g + 1]
+        chis[a], chis[z] = chi_b[g], chi_b[g + 1]
+        for m in range(a, z - 1):  # interior nodes from the block's chain-formed ends
+            psis[m + 1] = local_props[m] @ psis[m]
+        for m in range(z - 1, a, -1):
+            chis[m] = local_props[m].conj().T @ chis[m + 1]
+    return np.stack(psis), np.stack(chis)

@@ -90,6 +90,12 @@ def test_gpe1024_config4(ctx, tag):
     w.config.log_exact_objective = True
     w.solver.step_size = float(fx[f"{tag}_rho"])
     g = I.run_ism(w.problem, w.u0, w.config, w.solver, ctx)
-    compare_run(g, fx, tag)
+    # Controls: 1e-9 relative at rho = 0.1.  At rho = 0.1/dt = 200 the 100-iteration split run
+    # amplifies last-bit differences ~4.5e4-fold (tools/config4_drift.py on the B200: a 1e-15 shift
+    # of u0 alone moves the final controls by 4.5e-11; profiles/r02/config4_drift.json): the
+    # device's FFT / phase rounding order (radix-4 Stockham, fused multiply-adds) against the
+    # oracle's radix-2 order leaves 3.0e-9 there while the objective and exact-payoff histories
+    # still agree to 2.5e-11, so the control bound of that one case is 5e-9.
+    compare_run(g, fx, tag, ctl_tol=1e-9 if tag == "literal" else 5e-9)
     ex = np.array([it.exact_objective for it in g.record.iterations[1:]])
     assert np.max(np.abs(ex - fx[f"{tag}_exact"][1:])) < 1e-10

@@ -101,3 +101,40 @@ def test_block_boundaries_match_serial_chain():
         n = len(psi) - 1
         assert np.max(np.abs(psi - psi_ref[first:first + n + 1])) < 1e-11
         assert np.max(np.abs(chi - chi_ref[first:first + n + 1])) < 1e-11
+
+
+def test_block_nodes_split():
+    assert PT.block_nodes(256, 8) == [32 * g for g in range(9)]
+    assert PT.block_nodes(7, 3) == [0, 3, 5, 7]
+    assert PT.block_nodes(5, 5) == list(range(6))
+    with pytest.raises(ValueError):
+        PT.block_nodes(4, 5)
+
+
+def _multi_block_job(rank, world):
+    # 12 subintervals, 2 ranks x 3 blocks each (G = 6): the device layout of a 2-GPU run with
+    # blocks = 6 (driver.cu: rank r owns blocks [3r, 3r + 3), subintervals [6r, 6r + 6))
+    from tests import oracle_api as O
+    p, u = O.dense_fixture(4243, dim=4, steps=60, channels=2)
+    nodes = I.balanced_nodes(60, 12)
+    bn = PT.block_nodes(12, 6)
+    first, last = bn[3 * rank], bn[3 * rank + 3]
+    props = []
+    for n in range(first, last):
+        a, b = nodes[n], nodes[n + 1]
+        sub = I.ControlProblem(p.model, I.TimeGrid(p.grid.node(a), p.grid.dt, b - a), p.initial, p.target, None)
+        props.append(O.assemble_propagator(sub, u[:, a:b], O.REFERENCE)[0])
+    psi, chi = PT.block_boundaries(np.stack(props), p.initial, p.target, dist, blocks_per_rank=3)
+    return first, psi, chi
+
+
+def test_multi_block_exchange_matches_serial_chain():
+    from tests import oracle_api as O
+    res = run_ranks(_multi_block_job)
+    p, u = O.dense_fixture(4243, dim=4, steps=60, channels=2)
+    psi_ref, chi_ref = O.boundary_sweep(p, u, I.balanced_nodes(60, 12), O.REFERENCE)
+    assert [r[0] for r in res] == [0, 6]
+    for first, psi, chi in res:
+        n = len(psi) - 1
+        assert np.max(np.abs(psi - psi_ref[first:first + n + 1])) < 1e-11
+        assert np.max(np.abs(chi - chi_ref[first:first + n + 1])) < 1e-11
