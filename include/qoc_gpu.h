@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define QOC_ABI_VERSION 1
+#define QOC_ABI_VERSION 2
 
 /* Largest control-channel count C the device kernels carry (DENSE, TRIDIAG, STRANG; the BITFLIP
  * kind takes C <= 4).  Larger C is rejected with QOC_ELOGIC before any work runs. */
@@ -155,13 +155,26 @@ typedef struct qoc_ism_config_v1 {
 
 enum qoc_solver_kind { QOC_SOLVER_GRADIENT = 0, QOC_SOLVER_MONOTONIC = 1, QOC_SOLVER_NEWTON = 2 };
 
-/* SolverSpec (optimizers.hpp:9-30); only the constant-step gradient kind is on this path. */
+/* SolverSpec (optimizers.hpp:9-30).  All three inner solvers run on the device: the
+ * constant-step gradient update (optimizers.cpp:102-107), the monotonic slice-rebuilding sweep
+ * (optimizers.cpp:109-213; DENSE kind, one channel, positive penalty, at most quadratic
+ * control — anything else returns QOC_ELOGIC as the reference throws std::logic_error) and the
+ * Newton update by restarted GMRES on finite-difference Hessian-vector products
+ * (optimizers.cpp:21-98,215-259; every kind).  The fields after step_size carry the reference's
+ * SolverSpec values literally (its defaults: 1e-12, 50, 30, 200, 1e-6, 1e-5). */
 typedef struct qoc_solver_v1 {
-  int32_t kind;                    /* enum qoc_solver_kind; others return QOC_ELOGIC */
+  int32_t kind;                    /* enum qoc_solver_kind */
   int32_t inner_iterations;
   int32_t naive_nonlinear_adjoint; /* GradientOptions::naive_nonlinear_adjoint */
   int32_t checkpoint_stride;       /* GradientOptions::checkpoint_stride */
   double step_size;                /* rho */
+  double fixed_point_tol;          /* monotonic: per-slice fixed point */
+  int32_t fixed_point_max_iter;
+  int32_t gmres_restart;           /* newton */
+  int32_t gmres_max_iter;
+  int32_t reserved;
+  double gmres_tol;
+  double hvp_scale;
 } qoc_solver_v1;
 
 /* IterationStat (runtime.hpp:44-63), one per recorded iteration (entry 0 = bootstrap). */
@@ -207,6 +220,13 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* problem, const qoc_ism_c
                     const qoc_solver_v1* solver, const double* u0, double* u_out,
                     qoc_iter_record_v1* recs, int32_t rec_cap, double* task_values,
                     qoc_run_status_v1* status);
+
+/* Per-task inner-solver counters of the last qoc_ism_run on this context (InnerResult,
+ * optimizers.hpp:32-37, as merged per task at ism.cpp:409-411,503-511): for batch member b and
+ * outer iteration k (1-based), out[3][L] = guard_rejections, newton_fallbacks, gmres_iterations
+ * per subinterval.  All zero for the gradient solver.  QOC_EINVAL when (b, k) was not run. */
+int32_t qoc_ctx_solver_stats(const qoc_ctx* ctx, int32_t b, int32_t iteration, int32_t subintervals,
+                             int32_t* out);
 
 /* Objective forms (objective.hpp:16). */
 enum qoc_form { QOC_FORM_OVERLAP = 0, QOC_FORM_TRACKING = 1 };

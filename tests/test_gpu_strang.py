@@ -95,7 +95,9 @@ def test_gpe1024_config4(ctx, tag):
     # of u0 alone moves the final controls by 4.5e-11; profiles/r02/config4_drift.json): the
     # device's FFT / phase rounding order (radix-4 Stockham, fused multiply-adds) against the
     # oracle's radix-2 order leaves 3.0e-9 there while the objective and exact-payoff histories
-    # still agree to 2.5e-11, so the control bound of that one case is 5e-9.
-    compare_run(g, fx, tag, ctl_tol=1e-9 if tag == "literal" else 5e-9)
+    # still agree to 2.5e-11, so the control bound of that one case is 5e-9.  The per-task payoffs
+    # of that case (lagged boundary states of single subintervals, values up to 1.2) follow the
+    # controls: 5.5e-10 measured, bound 2e-9; the summed objective stays inside 1e-10.
+    compare_run(g, fx, tag, ctl_tol=1e-9 if tag == "literal" else 5e-9, tv_tol=None if tag == "literal" else 2e-9)
     ex = np.array([it.exact_objective for it in g.record.iterations[1:]])
     assert np.max(np.abs(ex - fx[f"{tag}_exact"][1:])) < 1e-10
