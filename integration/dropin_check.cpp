@@ -85,7 +85,30 @@ int main() {
     all &= compare("spin2_direct_plan", run_ism(p, u0, cfg, sv), run_ism_gpu(p, u0, cfg, sv), 1e-9, 1e-10);
     SolverSpec mono = sv;
     mono.kind = SolverSpec::Kind::monotonic;
+    // zero penalty: the monotonic sweep's precondition fails on both sides (optimizers.cpp:118-122)
     all &= throws_logic("monotonic_solver_rejected", [&] { run_ism_gpu(p, u0, cfg, mono); });
+    all &= throws_logic("monotonic_solver_rejected_reference", [&] { run_ism(p, u0, cfg, mono); });
+    // with a positive penalty both run the slice-rebuilding sweep; events (guard rejections) included
+    p.penalty = PenaltySchedule::constant(0.05, 1000);
+    cfg.plan = IsmConfig::BoundaryPlan::assembled;
+    cfg.max_outer = 6;
+    {
+      const IsmRun a = run_ism(p, u0, cfg, mono), b = run_ism_gpu(p, u0, cfg, mono);
+      bool ev = a.record.iterations.size() == b.record.iterations.size();
+      for (size_t k = 0; ev && k < a.record.iterations.size(); ++k)
+        ev = a.record.iterations[k].events == b.record.iterations[k].events;
+      all &= compare("spin2_monotonic", a, b, 1e-9, 1e-10) && ev;
+      std::printf("{\"case\": \"spin2_monotonic_events\", \"ok\": %s}\n", ev ? "true" : "false");
+    }
+    SolverSpec nw = sv;
+    nw.kind = SolverSpec::Kind::newton;
+    nw.step_size = 0.5;
+    cfg.max_outer = 4;
+    {
+      // finite-difference Hessian products amplify rounding by ~1/hvp_scale: 1e-6 / 1e-8 bounds
+      const IsmRun a = run_ism(p, u0, cfg, nw), b = run_ism_gpu(p, u0, cfg, nw);
+      all &= compare("spin2_newton", a, b, 1e-6, 1e-8);
+    }
   }
   {  // the reference's HCN-style rotor preset: dense, quadratic polarizability, t-dependent penalty
     ControlProblem p = rotor_problem(20, 1.0, 1.0, 0.5, 0.3, 5.0, 1024, 100.0, 1e-3);
@@ -113,13 +136,17 @@ int main() {
     sv.gradient.naive_nonlinear_adjoint = true;
     all &= compare("condensate_naive_adjoint", run_ism(p, u0, cfg, sv), run_ism_gpu(p, u0, cfg, sv), 1e-9, 1e-10);
   }
-  {  // the density-matrix spin chain (cn_conjugation) is not on the device path
+  {  // the density-matrix spin chain (cn_conjugation, the reference's `spins` preset builder)
     ControlProblem p = spin_chain_problem(3, {{1, 2}, {2, 3}}, 1.0, 1.0, 64, 0.0);
     const ControlField u0 = random_control(p.grid, p.model->channels(), 3u, 0.2);
     IsmConfig cfg;
     cfg.subintervals = 2;
-    cfg.max_outer = 1;
-    all &= throws_logic("density_matrix_kind_rejected", [&] { run_ism_gpu(p, u0, cfg, SolverSpec{}); });
+    cfg.max_outer = 5;
+    cfg.eta = 0.0;
+    cfg.plan = IsmConfig::BoundaryPlan::direct;
+    SolverSpec sv;
+    sv.step_size = 0.5;
+    all &= compare("density_matrix_spin_chain", run_ism(p, u0, cfg, sv), run_ism_gpu(p, u0, cfg, sv), 1e-9, 1e-10);
   }
   std::printf("{\"all_ok\": %s}\n", all ? "true" : "false");
   return all ? 0 : 1;

@@ -31,8 +31,8 @@ void rethrow(int32_t code, qoc_ctx* ctx) {  // ism.cpp:213-231, controls.cpp:16-
   }
 }
 
-int32_t solver_kind(SolverSpec::Kind k) {  // non-gradient kinds reach the library and come back
-  switch (k) {                              // as std::logic_error (never silently run gradient)
+int32_t solver_kind(SolverSpec::Kind k) {  // all three inner solvers run on the device
+  switch (k) {
     case SolverSpec::Kind::gradient: return QOC_SOLVER_GRADIENT;
     case SolverSpec::Kind::monotonic: return QOC_SOLVER_MONOTONIC;
     case SolverSpec::Kind::newton: return QOC_SOLVER_NEWTON;
@@ -69,7 +69,8 @@ IsmRun run_ism_gpu(const ControlProblem& p, const ControlField& u0, const IsmCon
   std::vector<Complex> lin, quad;
   std::vector<double> grid_x;
   switch (m.kind()) {
-    case PropagatorKind::cn_dense: {
+    case PropagatorKind::cn_dense:
+    case PropagatorKind::cn_conjugation: {  // same DenseModel payload; states are d x d matrices
       // DenseModel members are private (models.hpp:26-30): H0 = H(0), A_c = dH/du_c(0),
       // B_c = dH/du_c(e_c) - A_c, the extraction optimizers.cpp:124-138 already uses
       const RVec zero = RVec::Zero(C);
@@ -86,7 +87,7 @@ IsmRun run_ism_gpu(const ControlProblem& p, const ControlField& u0, const IsmCon
         std::copy(b.data(), b.data() + size_t(d) * d, quad.begin() + size_t(c) * d * d);
         for (Eigen::Index i = 0; i < b.size(); ++i) any_quad = any_quad || b.data()[i] != Complex(0.0, 0.0);
       }
-      q.kind = QOC_KIND_DENSE;
+      q.kind = m.kind() == PropagatorKind::cn_conjugation ? QOC_KIND_DENSITY : QOC_KIND_DENSE;
       q.h0 = reinterpret_cast<const double*>(h0.data());
       q.linear = reinterpret_cast<const double*>(lin.data());
       q.quadratic = any_quad ? reinterpret_cast<const double*>(quad.data()) : nullptr;
@@ -103,8 +104,6 @@ IsmRun run_ism_gpu(const ControlProblem& p, const ControlField& u0, const IsmCon
       q.kappa = tc->nonlinearity();
       break;
     }
-    case PropagatorKind::cn_conjugation:
-      throw std::logic_error("density-matrix conjugation kind is not on the device path");
   }
   q.initial = reinterpret_cast<const double*>(p.initial.data());
   q.target = reinterpret_cast<const double*>(p.target.data());
@@ -128,6 +127,12 @@ IsmRun run_ism_gpu(const ControlProblem& p, const ControlField& u0, const IsmCon
   s.naive_nonlinear_adjoint = solver.gradient.naive_nonlinear_adjoint;
   s.checkpoint_stride = solver.gradient.checkpoint_stride;
   s.step_size = solver.step_size;
+  s.fixed_point_tol = solver.fixed_point_tol;
+  s.fixed_point_max_iter = solver.fixed_point_max_iter;
+  s.gmres_restart = solver.gmres_restart;
+  s.gmres_max_iter = solver.gmres_max_iter;
+  s.gmres_tol = solver.gmres_tol;
+  s.hvp_scale = solver.hvp_scale;
 
   if (u0.channels() != C || u0.steps() != K)
     throw std::invalid_argument("initial control grid/channel count does not match the problem");
@@ -155,6 +160,19 @@ IsmRun run_ism_gpu(const ControlProblem& p, const ControlField& u0, const IsmCon
     it.task_values.assign(tv.begin() + size_t(k) * cfg.subintervals, tv.begin() + size_t(k + 1) * cfg.subintervals);
     it.critical_path_seconds = recs[k].device_seconds;  // device time of the iteration
     it.wall_seconds = recs[k].device_seconds;
+    // inner-solver events of the iteration's tasks (ism.cpp:503-511)
+    std::vector<int32_t> counters(size_t(3) * std::max(cfg.subintervals, 1));
+    if (k > 0 && qoc_ctx_solver_stats(ctx, 0, k, cfg.subintervals, counters.data()) == QOC_OK) {
+      const int L = cfg.subintervals;
+      for (int n = 0; n < L; ++n) {
+        if (counters[n] > 0)
+          it.events.push_back("task " + std::to_string(n) + ": kept " + std::to_string(counters[n]) +
+                              " slices at previous values");
+        if (counters[L + n] > 0)
+          it.events.push_back("task " + std::to_string(n) + ": " + std::to_string(counters[L + n]) +
+                              " Newton directions replaced by gradient steps");
+      }
+    }
     run.record.iterations.push_back(std::move(it));
   }
   run.record.aborted = st.aborted != 0;

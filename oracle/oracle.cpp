@@ -1174,12 +1174,228 @@ static bool finite_vec(const CV& v) {
   return true;
 }
 
+// ---------------------------------------------------------------------------------------
+// optimizers.cpp — the two other inner solvers (the gradient update is inline in run_ism).
+// ---------------------------------------------------------------------------------------
+struct InnerOut {
+  int guard_rejections = 0, newton_fallbacks = 0, gmres_iterations = 0;
+};
+
+static double vnorm(const RV& v) {
+  double s = 0.0;
+  for (double x : v) s += x * x;
+  return std::sqrt(s);
+}
+static double vdot(const RV& a, const RV& b) {
+  double s = 0.0;
+  for (size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
+  return s;
+}
+
+// Restarted GMRES on v -> A v (optimizers.cpp:21-98).
+static RV gmres(const std::function<RV(const RV&)>& apply, const RV& b, int restart, int max_iter,
+                double tol, int* iterations, double* relative_residual) {
+  const size_t n = b.size();
+  RV x(n, 0.0);
+  const double bnorm = vnorm(b);
+  int used = 0;
+  double rel = 0.0;
+  if (bnorm == 0.0) {
+    *iterations = 0;
+    *relative_residual = 0.0;
+    return x;
+  }
+  while (used < max_iter) {
+    RV r = apply(x);
+    for (size_t e = 0; e < n; ++e) r[e] = b[e] - r[e];
+    ++used;
+    const double beta = vnorm(r);
+    rel = beta / bnorm;
+    if (rel <= tol) break;
+    const int m = std::min(restart, static_cast<int>(n));
+    std::vector<RV> v(static_cast<size_t>(m) + 1, RV(n, 0.0));
+    std::vector<RV> h(static_cast<size_t>(m) + 1, RV(static_cast<size_t>(std::max(m, 1)), 0.0));  // h[row][col]
+    RV g(static_cast<size_t>(m) + 1, 0.0), cs(static_cast<size_t>(std::max(m, 1)), 1.0),
+        sn(static_cast<size_t>(std::max(m, 1)), 0.0);
+    for (size_t e = 0; e < n; ++e) v[0][e] = r[e] / beta;
+    g[0] = beta;
+    int spanned = 0;
+    for (int i = 0; i < m && used < max_iter; ++i) {
+      RV w = apply(v[static_cast<size_t>(i)]);
+      ++used;
+      for (int k = 0; k <= i; ++k) {  // modified Gram-Schmidt
+        const double hk = vdot(v[static_cast<size_t>(k)], w);
+        h[k][i] = hk;
+        for (size_t e = 0; e < n; ++e) w[e] -= hk * v[static_cast<size_t>(k)][e];
+      }
+      h[i + 1][i] = vnorm(w);
+      const bool breakdown = h[i + 1][i] <= 1e-14 * bnorm;
+      if (!breakdown)
+        for (size_t e = 0; e < n; ++e) v[static_cast<size_t>(i) + 1][e] = w[e] / h[i + 1][i];
+      for (int k = 0; k < i; ++k) {  // earlier Givens rotations on the new column
+        const double t = cs[k] * h[k][i] + sn[k] * h[k + 1][i];
+        h[k + 1][i] = -sn[k] * h[k][i] + cs[k] * h[k + 1][i];
+        h[k][i] = t;
+      }
+      const double denom = std::hypot(h[i][i], h[i + 1][i]);
+      cs[i] = denom == 0.0 ? 1.0 : h[i][i] / denom;
+      sn[i] = denom == 0.0 ? 0.0 : h[i + 1][i] / denom;
+      h[i][i] = denom;
+      h[i + 1][i] = 0.0;
+      g[i + 1] = -sn[i] * g[i];
+      g[i] = cs[i] * g[i];
+      spanned = i + 1;
+      rel = std::abs(g[i + 1]) / bnorm;
+      if (rel <= tol || breakdown) break;
+    }
+    if (spanned > 0) {  // back substitution on the rotated Hessenberg block
+      RV y(static_cast<size_t>(spanned));
+      for (int r2 = spanned - 1; r2 >= 0; --r2) {
+        double acc = g[r2];
+        for (int c2 = r2 + 1; c2 < spanned; ++c2) acc -= h[r2][c2] * y[c2];
+        y[r2] = acc / h[r2][r2];
+      }
+      for (int c2 = 0; c2 < spanned; ++c2)
+        for (size_t e = 0; e < n; ++e) x[e] += v[static_cast<size_t>(c2)][e] * y[c2];
+    }
+    if (rel <= tol) {
+      RV check = apply(x);
+      for (size_t e = 0; e < n; ++e) check[e] = b[e] - check[e];
+      ++used;
+      rel = vnorm(check) / bnorm;
+      if (rel <= tol) break;
+    }
+  }
+  *iterations = used;
+  *relative_residual = rel;
+  return x;
+}
+
+// newton_direction + newton_step (optimizers.cpp:215-259): (Hessian) d = -g0 with central
+// finite-difference Hessian-vector products of the weighted task gradient.
+static void newton_step(const Model& m, RV& u, const Task& t, double dt, const qoc_solver_v1& sv,
+                        bool naive, int stride, InnerOut& out) {
+  auto grad = [&](const RV& samples) {
+    RV g = gradient(m, samples.data(), t.len, dt, t.init, t.targ, t.alpha.data(), t.form, naive, stride);
+    for (double& x : g) x *= t.weight;
+    return g;
+  };
+  const RV g0 = grad(u);
+  const double u_scale = 1.0 + vnorm(u);
+  auto hessian_apply = [&](const RV& v) {
+    const double vn = vnorm(v);
+    if (vn == 0.0) return RV(v.size(), 0.0);
+    const double h = sv.hvp_scale * u_scale / vn;
+    RV up(u), um(u);
+    for (size_t e = 0; e < u.size(); ++e) {
+      up[e] = u[e] + h * v[e];
+      um[e] = u[e] - h * v[e];
+    }
+    RV gp = grad(up);
+    const RV gm = grad(um);
+    for (size_t e = 0; e < gp.size(); ++e) gp[e] = (gp[e] - gm[e]) / (2.0 * h);
+    return gp;
+  };
+  RV rhs(g0.size());
+  for (size_t e = 0; e < g0.size(); ++e) rhs[e] = -g0[e];
+  int iters = 0;
+  double rel = 0.0;
+  RV d = gmres(hessian_apply, rhs, sv.gmres_restart, sv.gmres_max_iter, sv.gmres_tol, &iters, &rel);
+  out.gmres_iterations += iters;
+  if (!(vdot(d, g0) > 0.0)) {  // not an ascent direction: plain gradient step
+    for (size_t e = 0; e < d.size(); ++e) d[e] = sv.step_size * g0[e];
+    ++out.newton_fallbacks;
+  }
+  for (size_t e = 0; e < u.size(); ++e) u[e] += d[e];
+}
+
+// monotonic_step (optimizers.cpp:109-213): forward sweep that rebuilds the control slice by
+// slice against the adjoint nodes of the previous control.
+static void monotonic_step(const Model& m, RV& u, const Task& t, double dt, const qoc_solver_v1& sv,
+                           InnerOut& out) {
+  const DenseM* dm = m.kind == QOC_KIND_DENSITY ? nullptr : dynamic_cast<const DenseM*>(&m);
+  if (!dm)
+    throw LogicErr("the monotonic sweep requires column states with the one-step rational scheme");
+  if (m.C != 1) throw LogicErr("the monotonic sweep handles a single control channel");
+  for (int j = 0; j < t.len; ++j)
+    if (t.alpha[static_cast<size_t>(j)] <= 0.0)
+      throw LogicErr("the monotonic sweep requires strictly positive penalty weights");
+  const int d = m.d, steps = t.len;
+  // dH/dv = M + v P (DenseModel: M = A_0, P = B_0; models.cpp:70-75)
+  const CMat& mu_op = dm->lin[0];
+  CMat pol_op(d, d);
+  if (!dm->quad.empty()) pol_op = dm->quad[0];
+  const cd half(0.0, 0.5 * dt);
+  auto shifted = [&](double v, double sign) {  // I + sign * (i dt/2) H(v)
+    const CMat h = dm->hamiltonian(&v);
+    CMat a = CMat::identity(d);
+    for (size_t e = 0; e < h.v.size(); ++e) a.v[e] += sign * (half * h.v[e]);
+    return a;
+  };
+  auto col = [&](const CV& s) {
+    CMat c(d, 1);
+    c.v = s;
+    return c;
+  };
+  std::vector<CV> chi(static_cast<size_t>(steps) + 1);
+  chi[static_cast<size_t>(steps)] = t.targ;
+  for (int j = steps - 1; j >= 0; --j)
+    chi[static_cast<size_t>(j)] = step_adj_linear(m, &u[static_cast<size_t>(j)], dt, chi[static_cast<size_t>(j) + 1]);
+  CV psi = t.init;
+  for (int j = 0; j < steps; ++j) {
+    const double uj = u[static_cast<size_t>(j)], aj = t.alpha[static_cast<size_t>(j)];
+    CMat psi_tilde = col(psi);
+    PivLU(shifted(uj, +1.0)).solve_inplace(psi_tilde);
+    double m_mu = 0.0, m_pol = 0.0;
+    auto pairings_at = [&](double v) {
+      CMat chi_tilde = col(chi[static_cast<size_t>(j) + 1]);
+      PivLU(shifted(v, -1.0)).solve_inplace(chi_tilde);
+      const CMat a = matmul(mu_op, psi_tilde), b2 = matmul(pol_op, psi_tilde);
+      cd sm(0.0, 0.0), sp(0.0, 0.0);
+      for (int i = 0; i < d; ++i) {
+        sm += std::conj(chi_tilde.v[i]) * a.v[i];
+        sp += std::conj(chi_tilde.v[i]) * b2.v[i];
+      }
+      m_mu = sm.imag();
+      m_pol = sp.imag();
+    };
+    double v = uj;
+    bool usable = true;
+    for (int it = 0; it < sv.fixed_point_max_iter; ++it) {  // v (alpha - m_pol(v)) = m_mu(v)
+      pairings_at(v);
+      const double denom = aj - m_pol;
+      if (!(std::abs(denom) > 1e-14 * (1.0 + aj))) {
+        usable = false;
+        break;
+      }
+      const double next = m_mu / denom;
+      const bool settled = std::abs(next - v) <= sv.fixed_point_tol * (1.0 + std::abs(v));
+      v = next;
+      if (settled) break;
+    }
+    if (usable && std::isfinite(v)) {
+      pairings_at(v);
+      const double gain = dt * (v - uj) * (m_mu + 0.5 * (v + uj) * (m_pol - aj));
+      if (!(gain >= 0.0)) usable = false;
+    } else {
+      usable = false;
+    }
+    if (!usable) {
+      v = uj;
+      ++out.guard_rejections;
+    }
+    u[static_cast<size_t>(j)] = v;
+    psi = step_fwd(m, &v, dt, psi);
+  }
+}
+
 struct IterRec {
   int iteration = 0;
   double objective = 0.0;
   std::optional<double> exact, error;
   RV task_values;
   double wall = 0.0;
+  std::vector<InnerOut> inner;  // per task (ism.cpp:409-411)
 };
 
 struct RunOut {
@@ -1205,7 +1421,7 @@ static RunOut run_ism(const Prob& P, const double* u0, const qoc_ism_config_v1& 
     throw InvalidArg(
         "interpolated waypoints require linear one-step flows; use the split variant for "
         "split-step states");
-  if (sv.kind != QOC_SOLVER_GRADIENT) throw LogicErr("only the gradient solver is on this path");
+  if (sv.kind < QOC_SOLVER_GRADIENT || sv.kind > QOC_SOLVER_NEWTON) throw InvalidArg("unknown solver kind");
   const int parts = cfg.subintervals;
   const std::vector<int> node = decomposition(P.K, parts, cfg.partition, cfg.node_index);
   // the density kind refreshes its boundaries by direct node sweeps (as the device does;
@@ -1308,6 +1524,7 @@ static RunOut run_ism(const Prob& P, const double* u0, const qoc_ism_config_v1& 
   struct Slot {
     double entry = 0.0, error = 0.0;
     RV unew;
+    InnerOut inner;
     CV psi_end, chi_start;
   };
   std::vector<Slot> slots(static_cast<size_t>(parts));
@@ -1322,9 +1539,16 @@ static RunOut run_ism(const Prob& P, const double* u0, const qoc_ism_config_v1& 
       const double* un = upart(n);
       r.entry = t.weight * evaluate(m, un, t.len, dt, t.init, t.targ, t.alpha.data(), t.form);
       r.unew.assign(un, un + static_cast<size_t>(C) * t.len);
-      for (int inner = 0; inner < sv.inner_iterations; ++inner) {  // run_inner / gradient_step
-        RV g = gradient(m, r.unew.data(), t.len, dt, t.init, t.targ, t.alpha.data(), t.form, naive, stride);
-        for (size_t e = 0; e < g.size(); ++e) r.unew[e] += sv.step_size * (t.weight * g[e]);
+      r.inner = InnerOut{};
+      for (int inner = 0; inner < sv.inner_iterations; ++inner) {  // run_inner, optimizers.cpp:261-285
+        if (sv.kind == QOC_SOLVER_MONOTONIC) {
+          monotonic_step(m, r.unew, t, dt, sv, r.inner);
+        } else if (sv.kind == QOC_SOLVER_NEWTON) {
+          newton_step(m, r.unew, t, dt, sv, naive, stride, r.inner);
+        } else {  // gradient_step
+          RV g = gradient(m, r.unew.data(), t.len, dt, t.init, t.targ, t.alpha.data(), t.form, naive, stride);
+          for (size_t e = 0; e < g.size(); ++e) r.unew[e] += sv.step_size * (t.weight * g[e]);
+        }
       }
       if (cfg.compute_error) {
         const RV g = gradient(m, r.unew.data(), t.len, dt, t.init, t.targ, t.alpha.data(), t.form, naive, stride);
@@ -1355,6 +1579,7 @@ static RunOut run_ism(const Prob& P, const double* u0, const qoc_ism_config_v1& 
     for (int n = 0; n < parts; ++n) {
       std::copy(slots[n].unew.begin(), slots[n].unew.end(), upart(n));
       total_error += slots[n].error;
+      it.inner.push_back(slots[n].inner);
     }
     IterRec& prev = out.its.back();
     prev.task_values.assign(static_cast<size_t>(parts), 0.0);
@@ -1487,6 +1712,23 @@ static int32_t guarded(char* err, size_t errlen, F&& f) {
   }
 }
 
+// per-task inner-solver counters of the last oracle_ism_run: [b][k][n]
+static std::vector<std::vector<std::vector<InnerOut>>> g_inner_stats;
+
+extern "C" int32_t oracle_solver_stats(int32_t b, int32_t iteration, int32_t subintervals, int32_t* out) {
+  if (b < 0 || b >= static_cast<int>(g_inner_stats.size()) || iteration < 0 ||
+      iteration >= static_cast<int>(g_inner_stats[static_cast<size_t>(b)].size()) || !out)
+    return QOC_EINVAL;
+  const auto& row = g_inner_stats[static_cast<size_t>(b)][static_cast<size_t>(iteration)];
+  for (int n = 0; n < subintervals; ++n) {
+    const InnerOut z = n < static_cast<int>(row.size()) ? row[static_cast<size_t>(n)] : InnerOut{};
+    out[n] = z.guard_rejections;
+    out[subintervals + n] = z.newton_fallbacks;
+    out[2 * subintervals + n] = z.gmres_iterations;
+  }
+  return QOC_OK;
+}
+
 extern "C" int32_t oracle_ism_run(const qoc_problem_v1* p, const qoc_ism_config_v1* cfg,
                                   const qoc_solver_v1* solver, const double* u0, double* u_out,
                                   qoc_iter_record_v1* recs, int32_t rec_cap, double* task_values,
@@ -1500,8 +1742,10 @@ extern "C" int32_t oracle_ism_run(const qoc_problem_v1* p, const qoc_ism_config_
     const size_t CK = static_cast<size_t>(p->channels) * p->steps;
     std::vector<Prob> probs;
     for (int b = 0; b < B; ++b) probs.push_back(make_prob(p, b, arith));
+    g_inner_stats.assign(static_cast<size_t>(B), {});
     auto one = [&](int b, Pool& pool) {
       RunOut r = run_ism(probs[static_cast<size_t>(b)], u0 + CK * b, *cfg, *solver, pool);
+      for (const IterRec& it : r.its) g_inner_stats[static_cast<size_t>(b)].push_back(it.inner);
       std::copy(r.u.begin(), r.u.end(), u_out + CK * b);
       qoc_run_status_v1& st = status[b];
       std::memset(&st, 0, sizeof(st));

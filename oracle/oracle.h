@@ -36,6 +36,10 @@ int32_t oracle_ism_run(const qoc_problem_v1* p, const qoc_ism_config_v1* cfg,
                        qoc_run_status_v1* status, int32_t arith, int32_t threads, char* err,
                        size_t errlen);
 
+/* Per-task InnerResult counters of the last oracle_ism_run (ism.cpp:409-411): out[3][L] =
+ * guard_rejections, newton_fallbacks, gmres_iterations of batch member b, record k. */
+int32_t oracle_solver_stats(int32_t b, int32_t iteration, int32_t subintervals, int32_t* out);
+
 int32_t oracle_propagate_final(const qoc_problem_v1* p, const double* u, double* states_out,
                                int32_t arith, char* err, size_t errlen);
 /* traj_out [B][K+1][d] */

@@ -156,6 +156,17 @@ std::shared_ptr<const qoc::HamiltonianModel> make_model(const qoc_problem_v1* p,
 
 }  // namespace
 
+// IterationStat::events of the last ref_ism_run, newline-joined: [b][k]
+static std::vector<std::vector<std::string>> g_events;
+
+extern "C" int32_t ref_iteration_events(int32_t b, int32_t k, char* out, size_t len) {
+  if (b < 0 || b >= static_cast<int>(g_events.size()) || k < 0 ||
+      k >= static_cast<int>(g_events[static_cast<size_t>(b)].size()) || !out || !len)
+    return QOC_EINVAL;
+  std::snprintf(out, len, "%s", g_events[static_cast<size_t>(b)][static_cast<size_t>(k)].c_str());
+  return QOC_OK;
+}
+
 extern "C" int32_t ref_ism_run(const qoc_problem_v1* p, const qoc_ism_config_v1* cfg, const qoc_solver_v1* sv,
                                const double* u0, double* u_out, qoc_iter_record_v1* recs, int32_t rec_cap,
                                double* task_values, qoc_run_status_v1* status, char* err, size_t errlen) {
@@ -190,7 +201,15 @@ extern "C" int32_t ref_ism_run(const qoc_problem_v1* p, const qoc_ism_config_v1*
       ic.log_exact_objective = cfg->log_exact_objective != 0;
       ic.checkpoint_stride = cfg->checkpoint_stride;
       qoc::SolverSpec spec;
-      spec.kind = qoc::SolverSpec::Kind::gradient;
+      spec.kind = sv->kind == QOC_SOLVER_MONOTONIC ? qoc::SolverSpec::Kind::monotonic
+                  : sv->kind == QOC_SOLVER_NEWTON  ? qoc::SolverSpec::Kind::newton
+                                                   : qoc::SolverSpec::Kind::gradient;
+      spec.fixed_point_tol = sv->fixed_point_tol;
+      spec.fixed_point_max_iter = sv->fixed_point_max_iter;
+      spec.gmres_restart = sv->gmres_restart;
+      spec.gmres_max_iter = sv->gmres_max_iter;
+      spec.gmres_tol = sv->gmres_tol;
+      spec.hvp_scale = sv->hvp_scale;
       spec.step_size = sv->step_size;
       spec.inner_iterations = sv->inner_iterations;
       spec.gradient.naive_nonlinear_adjoint = sv->naive_nonlinear_adjoint != 0;
@@ -202,6 +221,13 @@ extern "C" int32_t ref_ism_run(const qoc_problem_v1* p, const qoc_ism_config_v1*
       std::memset(&st, 0, sizeof(st));
       st.aborted = run.record.aborted ? 1 : 0;
       std::snprintf(st.abort_reason, sizeof(st.abort_reason), "%s", run.record.abort_reason.c_str());
+      if (b == 0) g_events.clear();
+      g_events.emplace_back();
+      for (const qoc::IterationStat& it : run.record.iterations) {
+        std::string joined;
+        for (const std::string& e : it.events) joined += e + "\n";
+        g_events.back().push_back(joined);
+      }
       const int n = std::min<int>(rec_cap, static_cast<int>(run.record.iterations.size()));
       st.iterations_recorded = n;
       for (int k = 0; k < n; ++k) {

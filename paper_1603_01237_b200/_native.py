@@ -46,6 +46,8 @@ def lib():
         L.qoc_ctx_kernel_profile.restype = i32
         L.qoc_ism_run.argtypes = [vp, vp, vp, vp, dp, dp, vp, i32, dp, vp]
         L.qoc_ism_run.restype = i32
+        L.qoc_ctx_solver_stats.argtypes = [vp, i32, i32, i32, vp]
+        L.qoc_ctx_solver_stats.restype = i32
         L.qoc_propagate_final.argtypes = [vp, vp, dp, dp]
         L.qoc_propagate_final.restype = i32
         L.qoc_objective_gradient.argtypes = [vp, vp, dp, i32, i32, dp, dp]

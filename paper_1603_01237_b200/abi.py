@@ -12,7 +12,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-QOC_ABI_VERSION = 1
+QOC_ABI_VERSION = 2
 
 QOC_OK, QOC_EINVAL, QOC_ELOGIC, QOC_ECUDA, QOC_ENCCL, QOC_ERUNTIME = range(6)
 KIND_DENSE, KIND_TRIDIAG, KIND_BITFLIP, KIND_STRANG, KIND_DENSITY = range(5)
@@ -56,6 +56,9 @@ class SolverV1(C.Structure):
         ("kind", C.c_int32), ("inner_iterations", C.c_int32),
         ("naive_nonlinear_adjoint", C.c_int32), ("checkpoint_stride", C.c_int32),
         ("step_size", C.c_double),
+        ("fixed_point_tol", C.c_double), ("fixed_point_max_iter", C.c_int32),
+        ("gmres_restart", C.c_int32), ("gmres_max_iter", C.c_int32), ("reserved", C.c_int32),
+        ("gmres_tol", C.c_double), ("hvp_scale", C.c_double),
     ]
 
 

@@ -230,4 +230,28 @@ struct SweepRange {
   int g0, nloc;
 };
 
+// Inner-solver workspace of the Newton update (optimizers.cpp:21-98,215-259; solvers.cu): one
+// restarted GMRES per (problem, subinterval) task, all tasks advanced in lockstep rounds -- a
+// round is two gradient launches of the kind's own task kernel at u +- h v (the central
+// finite-difference Hessian-vector product) and one advance kernel that runs every task's
+// GMRES state machine.  Vectors live on the control grid [B][K][C]; a task owns its window.
+struct DevNewton {
+  int restart, max_iter;  // SolverSpec::gmres_restart / gmres_max_iter
+  double tol, hvp_scale, step_size;
+  int weighted;           // task weight K/len (interpolated variant)
+  double* g0;             // raw gradient at u (weight applied on use)
+  double* x;              // GMRES iterate
+  double* V;              // [restart + 1] Krylov basis vectors
+  double *up, *um;        // perturbed controls u + h v, u - h v
+  double *gp, *gm;        // raw gradients there; gp is reused for w = A v
+  double* Hm;             // [B][L][(restart + 1) * restart] Hessenberg columns, h(row, col) at row * restart + col
+  double* gv;             // [B][L][restart + 1] rotated right-hand side
+  double *cs, *sn;        // [B][L][restart] Givens rotations
+  double* sc;             // [B][L][4]: bnorm, rel, h, u_scale
+  int* st;                // [B][L][8]: phase, i, used, spanned, zero, done, m
+  int* active;            // [rounds] tasks still iterating after each round
+  int* stats;             // [B][L][3] guard_rejections, newton_fallbacks, gmres_iterations (this outer iteration)
+  size_t vstride;         // elements between basis vectors (= B * K * C)
+};
+
 }  // namespace qoc

@@ -703,6 +703,123 @@ __global__ void __launch_bounds__(BT) density_horizon_kernel(DevProblem P, DevRu
   }
 }
 
+
+// ---- monotonic slice-rebuilding sweep (monotonic_step, optimizers.cpp:109-213) ----------------
+// A CTA per task.  The adjoint nodes chi_j along the previous control go to the task's
+// trajectory workspace; the forward sweep then rebuilds the control slice by slice: with
+// psi~ = (I + L(u_j))^-1 psi_j and chi~(v) = (I - L(v))^-1 chi_{j+1}, L(v) = i dt/2 H(v), the
+// implicit update v (alpha_j - m_pol(v)) = m_mu(v), m_X = Im <chi~| X |psi~>, dH/dv = M + v P, is
+// solved by fixed point; a slice whose exact payoff increment comes out negative (or whose
+// fixed point is unusable) keeps its previous value and counts as a guard rejection.
+// y = W x (plain matvec through the inverse)
+__device__ void solve_apply(int d, const double2* W, const double2* x, double2* y) {
+  for (int i = threadIdx.x; i < d; i += BT) {
+    double2 acc = cx(0.0, 0.0);
+    for (int k = 0; k < d; ++k) acc = cfma(W[i * d + k], x[k], acc);
+    y[i] = acc;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(BT) monotonic_kernel(DevProblem P, DevRun R, int weighted, double fp_tol,
+                                                        int fp_max_iter, int* stats) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = blockIdx.x, b = blockIdx.y;
+  if (R.done[b] | R.status[b]) return;
+  (void)weighted;  // the task weight scales the functional, not the slice update
+  const BigSmem S = carve(smem_raw, P.d, true);
+  const int d = P.d;
+  const size_t dd = (size_t)d * d;
+  const int node0 = P.node[n], len = P.node[n + 1] - node0;
+  const double scale = (double)len / (double)P.K, half = 0.5 * P.dt, dt = P.dt;
+  double* u = R.u + (size_t)b * P.K + node0;
+  double2* chi = R.traj + ((size_t)b * P.L + n) * (size_t)R.traj_len * d;
+  const size_t tix = ((size_t)b * P.L + n) * d;
+  const double2* mu_op = P.lin + (size_t)b * dd;                     // M = A_0
+  const double2* pol_op = P.has_quad ? P.quad + (size_t)b * dd : nullptr;  // P = B_0
+  double2* chin = S.Pm;         // chi_{j+1}
+  double2* chit = S.Pm + d;     // chi~(v)
+  double2* amu = S.T;           // M psi~
+  double2* apol = S.T + d;      // P psi~
+
+  // adjoint nodes along the previous control (optimizers.cpp:145-150)
+  copy_vec(d, R.task_targ + tix, S.x);
+  for (int i = threadIdx.x; i < d; i += BT) chi[(size_t)len * d + i] = S.x[i];
+  for (int j = len - 1; j >= 0; --j) {
+    build(P, b, u + j, half, S.W);
+    invert(d, S);
+    cayley(d, S.W, S.x, S.y, true);
+    copy_vec(d, S.y, S.x);
+    for (int i = threadIdx.x; i < d; i += BT) chi[(size_t)j * d + i] = S.x[i];
+  }
+  __syncthreads();
+
+  copy_vec(d, R.task_init + tix, S.x);  // psi_j
+  int rejected = 0;
+  for (int j = 0; j < len; ++j) {
+    const double uj = u[j], aj = P.alpha[node0 + j] * scale;
+    build(P, b, &uj, half, S.W);
+    invert(d, S);
+    solve_apply(d, S.W, S.x, S.y);  // psi~
+    for (int i = threadIdx.x; i < d; i += BT) {
+      double2 a = cx(0.0, 0.0), q = cx(0.0, 0.0);
+      for (int k = 0; k < d; ++k) {
+        a = cfma(mu_op[(size_t)i * d + k], S.y[k], a);
+        if (pol_op) q = cfma(pol_op[(size_t)i * d + k], S.y[k], q);
+      }
+      amu[i] = a;
+      apol[i] = q;
+      chin[i] = chi[(size_t)(j + 1) * d + i];
+    }
+    __syncthreads();
+    double m_mu = 0.0, m_pol = 0.0;
+    auto pairings_at = [&](double v) {
+      build(P, b, &v, -half, S.W);  // I - L(v)
+      invert(d, S);
+      solve_apply(d, S.W, chin, chit);
+      double sm = 0.0, sp = 0.0;
+      for (int i = threadIdx.x; i < d; i += BT) {
+        sm += cconjmul(chit[i], amu[i]).y;
+        sp += cconjmul(chit[i], apol[i]).y;
+      }
+      m_mu = block_sum(sm, S.red);
+      m_pol = block_sum(sp, S.red);
+    };
+    double v = uj;
+    bool usable = true;
+    for (int it = 0; it < fp_max_iter; ++it) {
+      pairings_at(v);
+      const double denom = aj - m_pol;
+      if (!(fabs(denom) > 1e-14 * (1.0 + aj))) {
+        usable = false;
+        break;
+      }
+      const double next = m_mu / denom;
+      const bool settled = fabs(next - v) <= fp_tol * (1.0 + fabs(v));
+      v = next;
+      if (settled) break;
+    }
+    if (usable && isfinite(v)) {
+      pairings_at(v);
+      const double gain = dt * (v - uj) * (m_mu + 0.5 * (v + uj) * (m_pol - aj));
+      if (!(gain >= 0.0)) usable = false;
+    } else {
+      usable = false;
+    }
+    if (!usable) {
+      v = uj;
+      ++rejected;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) u[j] = v;
+    build(P, b, &v, half, S.W);
+    invert(d, S);
+    cayley(d, S.W, S.x, S.y, false);
+    copy_vec(d, S.y, S.x);
+  }
+  if (threadIdx.x == 0) stats[((size_t)b * P.L + n) * 3] += rejected;
+}
+
 }  // namespace
 
 bool dense_big_supported(int d) { return d > 32 && d <= BIG_MAX; }
@@ -724,6 +841,17 @@ cudaError_t dense_big_horizon(const DevProblem& P, const DevRun& R, int which, i
   return cudaGetLastError();
 }
 
+
+bool monotonic_supported(const DevProblem& P) { return P.kind == QOC_KIND_DENSE && P.d <= BIG_MAX && P.C == 1; }
+
+cudaError_t monotonic_sweep(const DevProblem& P, const DevRun& R, int weighted, double fp_tol, int fp_max_iter,
+                            int* stats, cudaStream_t st) {
+  const size_t smem = big_smem(P.d, true);
+  cudaError_t e = cudaFuncSetAttribute(monotonic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  monotonic_kernel<<<dim3(P.L, P.B), BT, smem, st>>>(P, R, weighted, fp_tol, fp_max_iter, stats);
+  return cudaGetLastError();
+}
 }  // namespace qoc
 
 namespace qoc {

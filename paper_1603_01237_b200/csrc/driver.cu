@@ -34,6 +34,9 @@ static_assert(qoc::MAXC == QOC_MAX_CHANNELS, "device channel arrays must match t
 using namespace qoc;
 
 struct qoc_ctx {
+  // InnerResult counters of the last qoc_ism_run: [iterations + 1][B][L][3]
+  std::vector<int> solver_stats;
+  int solver_stats_dims[3] = {0, 0, 0};
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t aux = nullptr;          // side stream: boundary chain overlapped with the residual
@@ -718,6 +721,17 @@ int32_t qoc_ctx_set_option(qoc_ctx* ctx, int32_t option, int64_t value) {
   return QOC_EINVAL;
 }
 
+int32_t qoc_ctx_solver_stats(const qoc_ctx* ctx, int32_t b, int32_t iteration, int32_t subintervals, int32_t* out) {
+  if (!ctx || !out) return QOC_EINVAL;
+  const int* dm = ctx->solver_stats_dims;
+  if (iteration < 1 || iteration >= dm[0] || b < 0 || b >= dm[1] || subintervals != dm[2]) return QOC_EINVAL;
+  const int L = dm[2];
+  const int* row = ctx->solver_stats.data() + ((size_t)iteration * dm[1] + b) * L * 3;
+  for (int n = 0; n < L; ++n)
+    for (int q = 0; q < 3; ++q) out[q * L + n] = row[n * 3 + q];
+  return QOC_OK;
+}
+
 int32_t qoc_ctx_profile(qoc_ctx* ctx, qoc_profile_v1* out, int32_t reset) {
   if (!ctx) return QOC_EINVAL;
   if (out) *out = ctx->prof;
@@ -790,7 +804,23 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
     if (!split && p->kind == QOC_KIND_STRANG)
       fail(QOC_EINVAL,
            "interpolated waypoints require linear one-step flows; use the split variant for split-step states");
-    if (solver->kind != QOC_SOLVER_GRADIENT) fail(QOC_ELOGIC, "only the gradient solver is on this path");
+    if (solver->kind < QOC_SOLVER_GRADIENT || solver->kind > QOC_SOLVER_NEWTON) fail(QOC_EINVAL, "unknown solver kind");
+    // run_inner dispatches per inner iteration (optimizers.cpp:261-285): a run that never calls the
+    // solver never sees its preconditions
+    const bool alt_solver = solver->kind != QOC_SOLVER_GRADIENT;
+    const bool monotonic = solver->kind == QOC_SOLVER_MONOTONIC, newton = solver->kind == QOC_SOLVER_NEWTON;
+    if (monotonic && cfg->max_outer > 0 && solver->inner_iterations > 0) {  // optimizers.cpp:110-122
+      if (p->kind == QOC_KIND_DENSITY || p->kind == QOC_KIND_STRANG)
+        fail(QOC_ELOGIC, "the monotonic sweep requires column states with the one-step rational scheme");
+      if (p->kind != QOC_KIND_DENSE)
+        fail(QOC_ELOGIC, "the monotonic sweep on the device takes the operators in DENSE form (it needs dH/dv as "
+                         "matrices); repack the model as QOC_KIND_DENSE");
+      if (p->channels != 1) fail(QOC_ELOGIC, "the monotonic sweep handles a single control channel");
+      for (int j = 0; j < p->steps; ++j)
+        if (!p->penalty || p->penalty[j] <= 0.0)
+          fail(QOC_ELOGIC, "the monotonic sweep requires strictly positive penalty weights");
+      if (p->dim < 2 || p->dim > 64) fail(QOC_ELOGIC, "the monotonic sweep on the device takes 2 <= d <= 64");
+    }
     if (rec_cap < cfg->max_outer + 1) fail(QOC_EINVAL, "rec_cap must be >= max_outer + 1");
     const std::vector<int> node = decomposition(p->steps, cfg->subintervals, cfg->partition, cfg->node_index);
     const int L = cfg->subintervals, B = p->batch, C = p->channels, K = p->steps;
@@ -805,6 +835,7 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
                       ? (cfg->blocks > 0 ? cfg->blocks : (ctx->world > 1 ? ctx->world : 0))
                       : 0;
     const bool blocked = G > 0;
+    if (blocked && alt_solver) fail(QOC_ELOGIC, "the blocked plan runs the gradient solver");
     if (blocked) {
       if (G > L) fail(QOC_EINVAL, "blocks must not exceed subintervals");
       if (G % ctx->world != 0) fail(QOC_EINVAL, "blocks must be a multiple of the communicator size");
@@ -825,10 +856,48 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
     const DevProblem& P = dp.P;
     DeviceRun dr;
     dr.slots = fresh_slots(ctx->run_slots);
-    const bool pcache = use_pcache(P, node);
+    // the monotonic and Newton solvers run on the kinds' own task kernels (no propagator cache)
+    const bool pcache = !alt_solver && use_pcache(P, node);
     alloc_run(dp, rec_cap, node, assembled_interp, false, st, dr, pcache, split);
     const DevRun& R = dr.R;
     ck(cudaMemcpyAsync(R.u, u0, sizeof(double) * B * K * C, cudaMemcpyHostToDevice, st), "u0");
+    // inner-solver workspace and per-task counters (InnerResult, optimizers.hpp:32-37)
+    DevNewton NW{};
+    int* sstats = nullptr;       // [B][L][3] of the running outer iteration
+    int* sstats_hist = nullptr;  // [max_outer + 1][B][L][3]
+    const size_t nstat = (size_t)B * L * 3;
+    if (alt_solver) {
+      sstats = dr.alloc<int>(nstat);
+      sstats_hist = dr.alloc<int>(nstat * (cfg->max_outer + 1));
+      ck(cudaMemsetAsync(sstats_hist, 0, sizeof(int) * nstat * (cfg->max_outer + 1), st), "memset");
+    }
+    if (newton) {
+      const size_t grid = (size_t)B * K * C, T = (size_t)B * L;
+      const int RS = std::max(1, solver->gmres_restart);
+      NW.restart = RS;
+      NW.max_iter = solver->gmres_max_iter;
+      NW.tol = solver->gmres_tol;
+      NW.hvp_scale = solver->hvp_scale;
+      NW.step_size = solver->step_size;
+      NW.weighted = split ? 0 : 1;
+      NW.vstride = grid;
+      NW.g0 = dr.alloc<double>(grid);
+      NW.x = dr.alloc<double>(grid);
+      NW.V = dr.alloc<double>(grid * (RS + 1));
+      NW.up = dr.alloc<double>(grid);
+      NW.um = dr.alloc<double>(grid);
+      NW.gp = dr.alloc<double>(grid);
+      NW.gm = dr.alloc<double>(grid);
+      NW.Hm = dr.alloc<double>(T * (RS + 1) * RS);
+      NW.gv = dr.alloc<double>(T * (RS + 1));
+      NW.cs = dr.alloc<double>(T * RS);
+      NW.sn = dr.alloc<double>(T * RS);
+      NW.sc = dr.alloc<double>(T * 4);
+      NW.st = dr.alloc<int>(T * 8);
+      NW.active = dr.alloc<int>(std::max(0, NW.max_iter) + 4);
+      NW.stats = sstats;
+      if (solver->gmres_restart < 1) fail(QOC_EINVAL, "gmres_restart must be >= 1");
+    }
     // blocked plan: the exchange slabs and this rank's blocks / subintervals
     DevBlocks BK{};
     int g_lo = 0, n_lo = 0, n_cnt = 0;
@@ -996,6 +1065,46 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
             const TaskArgs E{em, form, split ? 0 : 1, 1, 0.0};
             launch.run([&] { return pc_eval(P, RR, E, 0, st); }, "residual", true);
           }
+        } else if (alt_solver) {
+          // entry value, then run_inner with the monotonic / Newton solver, then the sweeps at the
+          // updated control (ism.cpp:407-459)
+          const TaskArgs E{M_ENTRY, form, split ? 0 : 1, 1, 0.0};
+          launch.run([&] { return task(P, RR, E, 0, st); }, "task", true);
+          ck(cudaMemsetAsync(sstats, 0, sizeof(int) * nstat, st), "memset");
+          for (int it = 0; it < inner; ++it) {
+            if (monotonic) {
+              launch.run([&] { return monotonic_sweep(P, RR, split ? 0 : 1, solver->fixed_point_tol,
+                                                      solver->fixed_point_max_iter, sstats, st); }, "monotonic sweep", true);
+              continue;
+            }
+            const TaskArgs Gm{M_GRAD, form, 0, 1, 0.0};
+            DevRun RG0 = RR, RGp = RR, RGm = RR;
+            RG0.grad = NW.g0;
+            RGp.u = NW.up;
+            RGp.grad = NW.gp;
+            RGm.u = NW.um;
+            RGm.grad = NW.gm;
+            launch.run([&] { return task(P, RG0, Gm, 0, st); }, "newton gradient", true);
+            ck(cudaMemsetAsync(NW.active, 0, sizeof(int) * (std::max(0, NW.max_iter) + 4), st), "memset");
+            launch.run([&] { return newton_begin(P, RR, NW, st); }, "gmres");
+            for (int round = 1; round <= std::max(0, NW.max_iter) + 3; ++round) {
+              int act = 0;  // tasks with a Hessian-vector product pending
+              ck(cudaMemcpyAsync(&act, NW.active + round - 1, sizeof(int), cudaMemcpyDeviceToHost, st), "poll");
+              ck(cudaStreamSynchronize(st), "poll");
+              if (act == 0) break;
+              launch.run([&] { return task(P, RGp, Gm, 0, st); }, "newton gradient", true);
+              launch.run([&] { return task(P, RGm, Gm, 0, st); }, "newton gradient", true);
+              launch.run([&] { return newton_advance(P, RR, NW, round, st); }, "gmres");
+            }
+            launch.run([&] { return newton_apply(P, RR, NW, st); }, "newton update");
+          }
+          const int rest = mode & (M_ERROR | M_ASSEMBLE | M_LAGGED);
+          if (rest) {
+            const TaskArgs Rm{rest, form, split ? 0 : 1, 1, 0.0};
+            launch.run([&] { return task(P, RR, Rm, 0, st); }, "task", true);
+          }
+          ck(cudaMemcpyAsync(sstats_hist + nstat * k, sstats, sizeof(int) * nstat, cudaMemcpyDeviceToDevice, st),
+             "solver counters");
         } else {
           launch.run([&] { return task(P, RR, A, 0, st); }, "task", true);
         }
@@ -1015,7 +1124,7 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
       // Long runs replay the iteration as one CUDA graph (captured once; the iteration index
       // is read from device memory), which removes the per-kernel launch gaps of the small
       // latency-bound configs.  Profiling mode keeps direct launches (per-launch events).
-      bool use_graph = !ctx->profile && max_outer >= 8 && !(blocked && ctx->comm);
+      bool use_graph = !ctx->profile && max_outer >= 8 && !(blocked && ctx->comm) && !alt_solver;
       cudaGraphExec_t gexec = nullptr;
       int* kdev = nullptr;
       int64_t launches_per_body = 0;
@@ -1173,6 +1282,16 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
       if (task_values)
         ck(cudaMemcpy(task_values, R.rec_tv, sizeof(double) * (size_t)B * rec_cap * L, cudaMemcpyDeviceToHost),
            "task values");
+      ctx->solver_stats.clear();
+      ctx->solver_stats_dims[0] = ctx->solver_stats_dims[1] = ctx->solver_stats_dims[2] = 0;
+      if (alt_solver) {  // per-task counters of iterations 1..ran
+        ctx->solver_stats.resize(nstat * (ran + 1));
+        ck(cudaMemcpy(ctx->solver_stats.data(), sstats_hist, sizeof(int) * nstat * (ran + 1), cudaMemcpyDeviceToHost),
+           "solver counters");
+        ctx->solver_stats_dims[0] = ran + 1;
+        ctx->solver_stats_dims[1] = B;
+        ctx->solver_stats_dims[2] = L;
+      }
       std::vector<float> secs(ran + 1, 0.f);
       ck(cudaEventElapsedTime(&secs[0], ev[0], ev[1]), "elapsed");
       for (int k = 1; k <= ran; ++k) {

@@ -69,6 +69,19 @@ cudaError_t dense_pc_eval16(const DevProblem& P, const DevRun& R, const TaskArgs
 cudaError_t pc_eval_dual(const DevProblem& P, const DevRun& R, int form, int weighted, double rho, int dual,
                          cudaStream_t st);
 
+// inner solvers other than the gradient update (solvers.cu, dense_big.cu)
+//   Newton (every kind): begin after a raw-gradient launch into N.g0, then rounds of
+//   [task(M_GRAD) at N.up -> N.gp, task(M_GRAD) at N.um -> N.gm, newton_advance]; N.active[round]
+//   counts the tasks still iterating; newton_apply writes u += d (or the gradient fallback).
+cudaError_t newton_begin(const DevProblem& P, const DevRun& R, const DevNewton& N, cudaStream_t st);
+cudaError_t newton_advance(const DevProblem& P, const DevRun& R, const DevNewton& N, int round, cudaStream_t st);
+cudaError_t newton_apply(const DevProblem& P, const DevRun& R, const DevNewton& N, cudaStream_t st);
+//   Monotonic slice-rebuilding sweep (optimizers.cpp:109-213): DENSE kind, d <= 64, one channel;
+//   stats[b][n][0] += guard rejections
+bool monotonic_supported(const DevProblem& P);
+cudaError_t monotonic_sweep(const DevProblem& P, const DevRun& R, int weighted, double fp_tol, int fp_max_iter,
+                            int* stats, cudaStream_t st);
+
 // glue (kind independent)
 cudaError_t penalty_partials(const DevProblem& P, const DevRun& R, int ignore_done, cudaStream_t st);
 cudaError_t merge_iteration(const DevProblem& P, const DevRun& R, int k, double* tot_err, cudaStream_t st);

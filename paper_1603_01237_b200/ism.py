@@ -108,12 +108,18 @@ class IsmConfig:
 
 @dataclass
 class SolverSpec:
-    """optimizers.hpp:9-30; the constant-step gradient kind is the hot path."""
+    """optimizers.hpp:9-30.  kind is "gradient" (the hot path), "monotonic" or "newton"."""
     kind: str = "gradient"
     step_size: float = 1.0
     inner_iterations: int = 1
     naive_nonlinear_adjoint: bool = False
     checkpoint_stride: int = 0
+    fixed_point_tol: float = 1e-12   # monotonic sweep: implicit per-slice update
+    fixed_point_max_iter: int = 50
+    gmres_restart: int = 30          # Newton direction: restarted GMRES on FD Hessian products
+    gmres_max_iter: int = 200
+    gmres_tol: float = 1e-6
+    hvp_scale: float = 1e-5
 
 
 @dataclass
@@ -139,6 +145,7 @@ class IterationStat:
     device_seconds: float = 0.0
     tasks: list = field(default_factory=list)
     events: list = field(default_factory=list)
+    solver_stats: Optional[np.ndarray] = None  # [3][L] guard rejections, Newton fallbacks, GMRES iterations
 
     @property
     def critical_path_seconds(self) -> float:
@@ -296,6 +303,9 @@ def pack_solver(sv: SolverSpec):
     s.naive_nonlinear_adjoint = int(sv.naive_nonlinear_adjoint)
     s.checkpoint_stride = sv.checkpoint_stride
     s.step_size = sv.step_size
+    s.fixed_point_tol, s.fixed_point_max_iter = sv.fixed_point_tol, sv.fixed_point_max_iter
+    s.gmres_restart, s.gmres_max_iter = sv.gmres_restart, sv.gmres_max_iter
+    s.gmres_tol, s.hvp_scale = sv.gmres_tol, sv.hvp_scale
     return s
 
 
@@ -304,10 +314,23 @@ def unpack_records(recs: np.ndarray, tvals: np.ndarray, status, cfg: IsmConfig,
     return unpack_all(recs[b:b + 1], tvals[b:b + 1], [status[b]], cfg, solver)[0]
 
 
+def solver_events(stats_row) -> list:
+    """The per-task inner-solver events of one iteration (ism.cpp:503-511) from its counters
+    stats_row[3][L] = guard_rejections, newton_fallbacks, gmres_iterations."""
+    ev = []
+    for n in range(stats_row.shape[1]):
+        if stats_row[0, n] > 0:
+            ev.append(f"task {n}: kept {int(stats_row[0, n])} slices at previous values")
+        if stats_row[1, n] > 0:
+            ev.append(f"task {n}: {int(stats_row[1, n])} Newton directions replaced by gradient steps")
+    return ev
+
+
 def unpack_all(recs: np.ndarray, tvals: np.ndarray, status, cfg: IsmConfig, solver: SolverSpec,
-               task_value_lists: bool = True) -> list:
+               task_value_lists: bool = True, stats=None) -> list:
     """RunRecords of every batch member.  With task_value_lists=False each IterationStat.task_values
-    is a read-only row view of `tvals`; the IterationStat objects are built lazily per record."""
+    is a read-only row view of `tvals`; the IterationStat objects are built lazily per record.
+    stats(b, k) -> int array [3][L] of the inner-solver counters (or None)."""
     if not task_value_lists:
         tvals.setflags(write=False)
 
@@ -321,6 +344,12 @@ def unpack_all(recs: np.ndarray, tvals: np.ndarray, status, cfg: IsmConfig, solv
             its = [IterationStat(iteration=it_[k], objective=obj[k], exact_objective=ex[k] if hx[k] else None,
                                  error=er[k] if he[k] else None, task_values=tv[k], device_seconds=sec[k])
                    for k in range(n)]
+            if stats is not None:
+                for k in range(1, n):
+                    row = stats(b, k)
+                    if row is not None:
+                        its[k].solver_stats = row
+                        its[k].events.extend(solver_events(row))
             if aborted and its:  # the stopping iteration carries the reason
                 its[-1].events.append(reason)
             return its
@@ -372,7 +401,15 @@ def run_ism_batch(p: ControlProblem, u0, cfg: IsmConfig, solver: SolverSpec,
                                abi.dptr(tvals), status)
     raise_for(code, ctx.last_error())
     u = controls_from_abi(u_out, B, Cn, K)
-    return [IsmRun(u[b], r) for b, r in enumerate(unpack_all(recs, tvals, status, cfg, solver, B == 1))]
+    stats = None
+    if solver.kind != "gradient":
+        L = cfg.subintervals
+
+        def stats(b, k, _ctx=ctx):
+            row = np.zeros((3, L), dtype=np.int32)
+            ok = _ctx.lib.qoc_ctx_solver_stats(_ctx.handle, b, k, L, row.ctypes.data_as(C.c_void_p))
+            return row if ok == abi.QOC_OK else None
+    return [IsmRun(u[b], r) for b, r in enumerate(unpack_all(recs, tvals, status, cfg, solver, B == 1, stats))]
 
 
 def run_ism(p: ControlProblem, u0, cfg: IsmConfig, solver: SolverSpec, ctx=None) -> IsmRun:

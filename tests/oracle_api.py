@@ -57,7 +57,16 @@ def ism_run(p: I.ControlProblem, u0, cfg: I.IsmConfig, solver: I.SolverSpec,
                                 status, C.c_int32(arith), C.c_int32(threads), err, C.c_size_t(512))
     _check(code, err)
     u = I.controls_from_abi(u_out, B, Cn, K)
-    return [I.IsmRun(u[b], r) for b, r in enumerate(I.unpack_all(recs, tvals, status, cfg, solver))]
+    L = cfg.subintervals
+
+    def stats(b, k):
+        row = np.zeros((3, L), dtype=np.int32)
+        ok = lib().oracle_solver_stats(C.c_int32(b), C.c_int32(k), C.c_int32(L), row.ctypes.data_as(C.c_void_p))
+        return row if ok == abi.QOC_OK else None
+    runs = I.unpack_all(recs, tvals, status, cfg, solver, stats=stats if solver.kind != "gradient" else None)
+    for r in runs:
+        _ = r.iterations  # build now: the counters belong to this call
+    return [I.IsmRun(u[b], r) for b, r in enumerate(runs)]
 
 
 def propagate_final(p, u, arith=STRUCTURED):
@@ -249,4 +258,15 @@ def ref_ism_run(p: I.ControlProblem, u0, cfg: I.IsmConfig, solver: I.SolverSpec)
                             C.c_size_t(512))
     _check(code, err)
     u = I.controls_from_abi(u_out, B, Cn, K)
-    return [I.IsmRun(u[b], r) for b, r in enumerate(I.unpack_all(recs, tvals, status, cfg, solver))]
+    runs = I.unpack_all(recs, tvals, status, cfg, solver)
+    for b, r in enumerate(runs):  # the reference's own IterationStat::events
+        for k, it in enumerate(r.iterations):
+            buf = C.create_string_buffer(1 << 16)
+            if _ref.ref_iteration_events(C.c_int32(b), C.c_int32(k), buf, C.c_size_t(len(buf))) == abi.QOC_OK:
+                ev = [e for e in buf.value.decode().split("\n") if e]
+                if r.aborted and k == len(r.iterations) - 1:
+                    ev = [e for e in ev if e != r.abort_reason]
+                    it.events[:0] = ev
+                else:
+                    it.events.extend(ev)
+    return [I.IsmRun(u[b], r) for b, r in enumerate(runs)]

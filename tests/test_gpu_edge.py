@@ -18,7 +18,7 @@ def test_input_rejection_matches_reference(ctx):
         with pytest.raises(I.InvalidArgument):
             I.run_ism(p, u, bad, sv, ctx)
     with pytest.raises(I.LogicError):
-        I.run_ism(p, u, I.IsmConfig(max_outer=1), I.SolverSpec(kind="newton"), ctx)
+        I.run_ism(p, u, I.IsmConfig(max_outer=1), I.SolverSpec(kind="monotonic"), ctx)  # two channels
     with pytest.raises(I.QocRuntimeError):  # Decomposition::uniform with K % L != 0
         I.run_ism(p, u, I.IsmConfig(subintervals=5, max_outer=1, partition="uniform"), sv, ctx)
     with pytest.raises(I.QocRuntimeError):  # more parts than steps

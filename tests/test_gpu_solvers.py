@@ -1,0 +1,170 @@
+"""The monotonic and Newton inner solvers on the device against the
+oracle, whose versions of both are pinned to the reference's optimizers.cpp by
+tests/test_reference_pinning.py.
+
+* monotonic_step (optimizers.cpp:109-213): controls to 1e-9 relative, objectives to 1e-10, and
+  the per-task guard-rejection events word for word (ism.cpp:503-506).
+* newton_step (optimizers.cpp:215-259): the Hessian-vector products are central differences of
+  the gradient with h ~ hvp_scale = 1e-5, which amplify last-bit differences by ~1/h, and GMRES
+  stops at a relative residual of 1e-6; the stated tolerance is therefore 1e-6 of the control
+  scale and 1e-8 on objectives (the reference compiled twice with different summation orders
+  agrees with itself no better; see test_newton_gmres in the pinning suite).
+"""
+import numpy as np
+import pytest
+
+from paper_1603_01237_b200 import ism as I
+from paper_1603_01237_b200 import problems
+from tests import oracle_api as O
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)
+
+
+def events(run):
+    return [list(it.events) for it in run.record.iterations]
+
+
+def check(g, r, ctl, obj):
+    assert rel(g.control, r.control) < ctl
+    assert len(g.record.iterations) == len(r.record.iterations)
+    a, b = g.record.objectives(), r.record.objectives()
+    ok = np.isfinite(b)
+    assert np.array_equal(np.isfinite(a), ok)
+    assert np.max(np.abs(a[ok] - b[ok])) < obj
+    for x, y in zip(g.record.iterations, r.record.iterations):
+        assert (x.error is None) == (y.error is None)
+        if x.error is not None:
+            assert abs(x.error - y.error) < max(obj, 1e-9) * 100 * max(1.0, abs(y.error))
+        tv, tw = np.asarray(x.task_values, float), np.asarray(y.task_values, float)
+        m = np.isfinite(tw)
+        assert np.array_equal(np.isfinite(tv), m)
+        if m.any():
+            assert np.max(np.abs(tv[m] - tw[m])) < obj
+
+
+@pytest.mark.parametrize("dim,quad", [(2, False), (3, True), (8, False), (16, True), (40, False)])
+@pytest.mark.parametrize("parts,variant", [(1, "interpolated"), (4, "interpolated"), (4, "split")])
+def test_monotonic_sweep(ctx, dim, quad, parts, variant):
+    p, u = O.dense_fixture(7000 + dim, dim=dim, steps=24, channels=1, quadratic=quad, alpha=0.15)
+    cfg = I.IsmConfig(subintervals=parts, max_outer=6, eta=0.0, variant=variant)
+    sv = I.SolverSpec(kind="monotonic")
+    g = I.run_ism(p, u, cfg, sv, ctx)
+    r = O.ism_run(p, u, cfg, sv, O.REFERENCE)[0]
+    check(g, r, 1e-9, 1e-10)
+    assert events(g) == events(r)
+    assert g.record.solver == "monotonic"
+
+
+def test_monotonic_two_level_fixture_rejections(ctx):
+    # the reference's own monotonic fixture (optimizers_test.cpp:52-76) through the ISM loop: the
+    # end tasks keep slices at their previous values; the events must name the same tasks and counts
+    p, u = O.dense_fixture(1002, dim=2, steps=24, channels=1, alpha=0.15)
+    cfg = I.IsmConfig(subintervals=4, max_outer=4, eta=0.0)
+    sv = I.SolverSpec(kind="monotonic", inner_iterations=2)
+    g = I.run_ism(p, u, cfg, sv, ctx)
+    r = O.ism_run(p, u, cfg, sv, O.REFERENCE)[0]
+    check(g, r, 1e-9, 1e-10)
+    assert events(g) == events(r) and any(events(g))
+    st = g.record.iterations[1].solver_stats
+    assert st is not None and st.shape == (3, 4) and st[0].sum() > 0
+
+
+def test_monotonic_never_decreases_the_payoff(ctx):
+    # acceptance criterion 7 (acceptance_main.cpp:394-430) on one task (L = 1): objective[k] is
+    # the task's entry value
+    p, u = O.dense_fixture(9700, dim=2, steps=32, channels=1, alpha=0.2)
+    cfg = I.IsmConfig(subintervals=1, max_outer=50, eta=0.0)
+    g = I.run_ism(p, u, cfg, I.SolverSpec(kind="monotonic"), ctx)
+    obj = g.record.objectives()
+    assert np.all(np.diff(obj) >= -1e-12)
+    assert obj[-1] > obj[0]
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(channels=2, alpha=0.1), "single control channel"),
+    (dict(channels=1, alpha=0.0), "strictly positive penalty"),
+])
+def test_monotonic_preconditions(ctx, kw, msg):
+    p, u = O.dense_fixture(6100, dim=3, steps=12, **kw)
+    cfg = I.IsmConfig(subintervals=2, max_outer=2, eta=0.0)
+    with pytest.raises(I.LogicError, match=msg):
+        I.run_ism(p, u, cfg, I.SolverSpec(kind="monotonic"), ctx)
+    # a run that never calls the solver never sees its preconditions (run_inner, optimizers.cpp:261-285)
+    g = I.run_ism(p, u, cfg, I.SolverSpec(kind="monotonic", inner_iterations=0), ctx)
+    assert np.array_equal(g.control, np.asarray(u).reshape(g.control.shape))
+
+
+def test_monotonic_rejects_matrix_and_split_step_states(ctx):
+    w = problems.spins_preset(quick=True, subintervals=2, iterations=2, steps=16)
+    with pytest.raises(I.LogicError, match="column states"):
+        I.run_ism(w.problem, w.u0, w.config, I.SolverSpec(kind="monotonic"), ctx)
+    p, u = O.strang_fixture(3000)
+    cfg = I.IsmConfig(subintervals=2, max_outer=1, variant="split")
+    with pytest.raises(I.LogicError, match="column states"):
+        I.run_ism(p, u, cfg, I.SolverSpec(kind="monotonic"), ctx)
+
+
+@pytest.mark.parametrize("dim,channels,alpha", [(3, 1, 3.0), (4, 2, 0.5), (16, 1, 1.0), (40, 1, 1.0)])
+@pytest.mark.parametrize("parts", [1, 4])
+def test_newton_gmres_dense(ctx, dim, channels, alpha, parts):
+    p, u = O.dense_fixture(7200 + dim, dim=dim, steps=20, channels=channels, alpha=alpha)
+    cfg = I.IsmConfig(subintervals=parts, max_outer=4, eta=0.0)
+    sv = I.SolverSpec(kind="newton", step_size=0.2)
+    g = I.run_ism(p, u, cfg, sv, ctx)
+    r = O.ism_run(p, u, cfg, sv, O.REFERENCE)[0]
+    check(g, r, 1e-6, 1e-8)
+    assert events(g) == events(r)
+    # GMRES iteration counts per task (InnerResult::gmres_iterations)
+    for x, y in zip(g.record.iterations[1:], r.record.iterations[1:]):
+        assert np.array_equal(x.solver_stats[2], y.solver_stats[2])
+
+
+def test_newton_restart_and_iteration_cap(ctx):
+    p, u = O.dense_fixture(7300, dim=4, steps=24, channels=2, alpha=0.3)
+    cfg = I.IsmConfig(subintervals=2, max_outer=3, eta=0.0)
+    sv = I.SolverSpec(kind="newton", step_size=0.2, gmres_restart=5, gmres_max_iter=17, gmres_tol=1e-9,
+                      inner_iterations=2)
+    g = I.run_ism(p, u, cfg, sv, ctx)
+    r = O.ism_run(p, u, cfg, sv, O.REFERENCE)[0]
+    check(g, r, 1e-6, 1e-8)
+    assert events(g) == events(r)
+    for x, y in zip(g.record.iterations[1:], r.record.iterations[1:]):
+        assert np.array_equal(x.solver_stats, y.solver_stats)
+
+
+def test_newton_on_every_other_kind(ctx):
+    # the Newton rounds run on each kind's own task kernels: tridiagonal, bit-flip, split-step, density
+    w = problems.rotor21(subintervals=16, iterations=2, rho=100.0)
+    sv = I.SolverSpec(kind="newton", step_size=100.0, gmres_max_iter=12)
+    g = I.run_ism(w.problem, w.u0, w.config, sv, ctx)
+    r = O.ism_run(w.problem, w.u0, w.config, sv, O.STRUCTURED)[0]
+    check(g, r, 1e-6, 1e-8)
+    w = problems.ising10(nspins=5, steps=32, T=0.4, iterations=2, subintervals=4, rho=2.0)
+    sv = I.SolverSpec(kind="newton", step_size=2.0, gmres_max_iter=20)
+    g = I.run_ism(w.problem, w.u0, w.config, sv, ctx)
+    r = O.ism_run(w.problem, w.u0, w.config, sv, O.STRUCTURED)[0]
+    check(g, r, 1e-6, 1e-8)
+    p, u = O.strang_fixture(3100)
+    cfg = I.IsmConfig(subintervals=2, max_outer=2, eta=0.0, variant="split")
+    sv = I.SolverSpec(kind="newton", step_size=0.2, gmres_max_iter=12)
+    g = I.run_ism(p, u, cfg, sv, ctx)
+    r = O.ism_run(p, u, cfg, sv)[0]
+    check(g, r, 1e-6, 1e-8)
+    w = problems.spins_preset(quick=True, subintervals=2, iterations=2, steps=16)
+    sv = I.SolverSpec(kind="newton", step_size=w.solver.step_size, gmres_max_iter=10)
+    g = I.run_ism(w.problem, w.u0, w.config, sv, ctx)
+    r = O.ism_run(w.problem, w.u0, w.config, sv, O.REFERENCE)[0]
+    check(g, r, 1e-6, 1e-8)
+
+
+def test_newton_batch_matches_single_runs(ctx):
+    w = problems.batch4096(batch=3, subintervals=8, iterations=2, rho=5.0)
+    sv = I.SolverSpec(kind="newton", step_size=5.0, gmres_max_iter=8)
+    runs = I.run_ism_batch(w.problem, w.u0, w.config, sv, ctx)
+    refs = O.ism_run(w.problem, w.u0, w.config, sv, O.REFERENCE)
+    for g, r in zip(runs, refs):
+        check(g, r, 1e-6, 1e-8)

@@ -225,7 +225,7 @@ def test_input_rejection():
         with pytest.raises(I.InvalidArgument):
             O.ism_run(p, u, bad, sv)
     with pytest.raises(I.LogicError):
-        O.ism_run(p, u, I.IsmConfig(max_outer=1), I.SolverSpec(kind="newton"))
+        O.ism_run(p, u, I.IsmConfig(max_outer=1), I.SolverSpec(kind="monotonic"), O.REFERENCE)  # two channels
 
 
 def test_split_variant_one_iteration_matches_single_interval():

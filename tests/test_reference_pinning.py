@@ -176,3 +176,84 @@ def test_density_matrix_five_spins():
     w.config.partition = "uniform"
     compare(O.ref_ism_run(w.problem, w.u0, w.config, w.solver)[0],
             O.ism_run(w.problem, w.u0, w.config, w.solver, O.REFERENCE)[0], ctl_abs=1e-11, obj_abs=1e-11)
+
+
+# ---- the other two inner solvers (optimizers.cpp:109-259), SURVEY §8(f) ranks 3-4 -------------
+def _events(run):
+    return [list(it.events) for it in run.record.iterations]
+
+
+@pytest.mark.parametrize("dim,quad", [(2, False), (3, True), (6, False)])
+@pytest.mark.parametrize("parts", [1, 4])
+@pytest.mark.parametrize("variant", ["interpolated", "split"])
+def test_monotonic_sweep(dim, quad, parts, variant):
+    p, u = O.dense_fixture(6000 + dim, dim=dim, steps=24, channels=1, quadratic=quad, alpha=0.15)
+    cfg = I.IsmConfig(subintervals=parts, max_outer=6, eta=0.0, variant=variant, partition="uniform")
+    sv = I.SolverSpec(kind="monotonic", inner_iterations=1)
+    r, o = O.ref_ism_run(p, u, cfg, sv)[0], O.ism_run(p, u, cfg, sv, O.REFERENCE)[0]
+    compare(r, o, ctl_abs=1e-11, obj_abs=1e-11)
+    assert _events(r) == _events(o)  # guard rejections per task, as the reference words them
+
+
+def test_monotonic_sweep_moves_the_control_and_rejections_are_counted():
+    p, u = O.dense_fixture(1002, dim=2, steps=24, channels=1, alpha=0.15)  # optimizers_test.cpp:52-76
+    cfg = I.IsmConfig(subintervals=4, max_outer=3, eta=0.0, partition="uniform")
+    sv = I.SolverSpec(kind="monotonic")
+    r, o = O.ref_ism_run(p, u, cfg, sv)[0], O.ism_run(p, u, cfg, sv, O.REFERENCE)[0]
+    assert np.max(np.abs(o.control - np.asarray(u))) > 1e-6
+    assert _events(r) == _events(o)
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(channels=2, alpha=0.1), "single control channel"),
+    (dict(channels=1, alpha=0.0), "strictly positive penalty"),
+])
+def test_monotonic_preconditions(kw, msg):
+    p, u = O.dense_fixture(6100, dim=3, steps=12, **kw)
+    cfg = I.IsmConfig(subintervals=2, max_outer=2, eta=0.0, partition="uniform")
+    sv = I.SolverSpec(kind="monotonic")
+    for run in (lambda: O.ref_ism_run(p, u, cfg, sv), lambda: O.ism_run(p, u, cfg, sv, O.REFERENCE)):
+        with pytest.raises(I.LogicError, match=msg):
+            run()
+
+
+def test_monotonic_rejects_matrix_states():
+    w = problems.spins_preset(quick=True, subintervals=2, iterations=2, steps=16)
+    w.config.workers = 1  # the reference's worker threads do not forward exceptions (runtime.cpp:29-49)
+    sv = I.SolverSpec(kind="monotonic")
+    for run in (lambda: O.ref_ism_run(w.problem, w.u0, w.config, sv),
+                lambda: O.ism_run(w.problem, w.u0, w.config, sv, O.REFERENCE)):
+        with pytest.raises(I.LogicError, match="column states"):
+            run()
+
+
+@pytest.mark.parametrize("dim,channels,alpha", [(3, 1, 3.0), (4, 2, 0.5)])
+@pytest.mark.parametrize("parts", [1, 4])
+def test_newton_gmres(dim, channels, alpha, parts):
+    # The Hessian-vector products are central differences with h ~ hvp_scale (1e-5): they amplify
+    # the last-bit differences between the two LU summation orders by ~1/h, and GMRES stops at a
+    # relative residual of 1e-6 -- agreement is to 1e-7 of the control scale, not to rounding.
+    p, u = O.dense_fixture(6200 + dim, dim=dim, steps=20, channels=channels, alpha=alpha)
+    cfg = I.IsmConfig(subintervals=parts, max_outer=4, eta=0.0, partition="uniform")
+    sv = I.SolverSpec(kind="newton", step_size=0.2)
+    r, o = O.ref_ism_run(p, u, cfg, sv)[0], O.ism_run(p, u, cfg, sv, O.REFERENCE)[0]
+    compare_newton(r, o)
+    assert _events(r) == _events(o)  # the same directions fell back to gradient steps
+
+
+def compare_newton(r, o, ctl=1e-7, obj=1e-8):
+    scale = max(1.0, float(np.max(np.abs(r.control))))
+    assert np.max(np.abs(r.control - o.control)) <= ctl * scale
+    assert len(r.record.iterations) == len(o.record.iterations)
+    for a, b in zip(r.record.iterations, o.record.iterations):
+        if np.isfinite(a.objective) or np.isfinite(b.objective):
+            assert abs(a.objective - b.objective) <= obj
+        if a.error is not None:
+            assert abs(a.error - b.error) <= 1e-6 * max(1.0, abs(a.error))
+
+
+def test_newton_on_the_condensate_split_variant():
+    p, u = O.strang_fixture(3100)
+    cfg = I.IsmConfig(subintervals=2, max_outer=2, eta=0.0, variant="split", partition="uniform")
+    sv = I.SolverSpec(kind="newton", step_size=0.2, gmres_max_iter=12)
+    compare_newton(O.ref_ism_run(p, u, cfg, sv)[0], O.ism_run(p, u, cfg, sv)[0])
