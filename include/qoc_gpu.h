@@ -77,11 +77,21 @@ enum qoc_kind { QOC_KIND_DENSE = 0, QOC_KIND_TRIDIAG = 1, QOC_KIND_BITFLIP = 2, 
  *             to rounding, ism_test.cpp:248-265). */
 #define QOC_MAX_DENSITY_CHANNELS 32
 
-/* Sampled potentials for QOC_KIND_STRANG.
+/* Potentials of QOC_KIND_STRANG: the device side of the reference's virtual
+ * potential(u) / potential_derivative(c, u) plugin (propagation.hpp:35-36).
  *   TRAP    : models.cpp:95-127, pot_params = {trap_distance}
  *   LATTICE : V(x,u) = 0.5*w2*x^2 + v0*cos^2(k (x - u)),  dV/du = v0*k*sin(2 k (x - u)),
- *             pot_params = {w2, v0, k}  (BASELINE config 4) */
-enum qoc_potential { QOC_POT_TRAP = 0, QOC_POT_LATTICE = 1 };
+ *             pot_params = {w2, v0, k}  (BASELINE config 4)
+ *   BASIS   : any model of the separable form V(x_i, u) = sum_m a_m[i] f_m(u),
+ *             dV/du = sum_m a_m[i] f_m'(u), with pot_terms <= QOC_MAX_POT_TERMS sampled profiles
+ *             pot_basis[m][i] and f_m named by pot_term_type[m] / pot_term_param[m]:
+ *               QOC_TERM_POWER  f = u^k,       param = k (integer >= 0; k = 0 is the static part)
+ *               QOC_TERM_COS    f = cos(w u),  param = w
+ *               QOC_TERM_SIN    f = sin(w u),  param = w
+ *             (shifted or modulated lattices, tilted / breathing traps, polynomial couplings). */
+enum qoc_potential { QOC_POT_TRAP = 0, QOC_POT_LATTICE = 1, QOC_POT_BASIS = 2 };
+enum qoc_pot_term { QOC_TERM_POWER = 0, QOC_TERM_COS = 1, QOC_TERM_SIN = 2 };
+#define QOC_MAX_POT_TERMS 8
 
 typedef struct qoc_problem_v1 {
   int32_t abi_version; /* QOC_ABI_VERSION */
@@ -118,6 +128,11 @@ typedef struct qoc_problem_v1 {
   int32_t potential;     /* enum qoc_potential */
   double pot_params[4];
   double kappa;          /* nonlinearity() */
+  int32_t pot_terms;             /* QOC_POT_BASIS: number of terms M */
+  int32_t pot_reserved;
+  const int32_t* pot_term_type;  /* [M] enum qoc_pot_term */
+  const double* pot_term_param;  /* [M] */
+  const double* pot_basis;       /* [M][d] sampled profiles a_m(x_i) */
 
   /* States and penalty (ControlProblem, objective.hpp:18-24). */
   const double* initial; /* [B][d] complex */

@@ -537,6 +537,29 @@ struct StrangM : Model {
   int pot = 0;
   double pp[4] = {0, 0, 0, 0};
   double kappa = 0.0;
+  // QOC_POT_BASIS: V = sum_m a_m(x) f_m(u) -- a caller-supplied potential()/potential_derivative()
+  // of the HamiltonianModel plugin (propagation.hpp:35-36) in separable form
+  std::vector<RV> basis;
+  std::vector<int> term_type;
+  RV term_param;
+  double term_value(size_t m2, double u0, bool deriv) const {
+    const double q = term_param[m2];
+    if (term_type[m2] == QOC_TERM_POWER) {
+      const int k = static_cast<int>(q);
+      if (deriv) return k > 0 ? k * std::pow(u0, k - 1) : 0.0;
+      return std::pow(u0, k);
+    }
+    if (term_type[m2] == QOC_TERM_COS) return deriv ? -q * std::sin(q * u0) : std::cos(q * u0);
+    return deriv ? q * std::cos(q * u0) : std::sin(q * u0);
+  }
+  RV basis_sum(double u0, bool deriv) const {
+    RV v(static_cast<size_t>(d), 0.0);
+    for (size_t m2 = 0; m2 < basis.size(); ++m2) {
+      const double f = term_value(m2, u0, deriv);
+      for (int i = 0; i < d; ++i) v[i] += basis[m2][i] * f;
+    }
+    return v;
+  }
   bool linear() const override { return false; }
   void cayley(const double*, double, CMat&, bool) const override {
     throw LogicErr("no dense one-step matrices to assemble for this propagator kind");
@@ -545,6 +568,7 @@ struct StrangM : Model {
     throw LogicErr("model does not provide dense control derivatives");
   }
   RV potential(const double* u) const {
+    if (pot == QOC_POT_BASIS) return basis_sum(u[0], false);
     RV v(static_cast<size_t>(d));
     if (pot == QOC_POT_TRAP) {  // models.cpp:95-110
       const double ld = u[0] * pp[0];
@@ -566,6 +590,7 @@ struct StrangM : Model {
     return v;
   }
   RV potential_derivative(const double* u) const {
+    if (pot == QOC_POT_BASIS) return basis_sum(u[0], true);
     RV dv(static_cast<size_t>(d));
     if (pot == QOC_POT_TRAP) {  // models.cpp:112-127
       const double l = u[0], dd = pp[0], ld = l * dd;
@@ -772,6 +797,17 @@ static Prob make_prob(const qoc_problem_v1* p, int b, int arith) {
       s->pot = p->potential;
       for (int i = 0; i < 4; ++i) s->pp[i] = p->pot_params[i];
       s->kappa = p->kappa;
+      if (p->potential == QOC_POT_BASIS) {
+        if (p->pot_terms < 1 || p->pot_terms > QOC_MAX_POT_TERMS || !p->pot_term_type || !p->pot_term_param ||
+            !p->pot_basis)
+          throw InvalidArg("basis potential needs 1..QOC_MAX_POT_TERMS terms with type, parameter and profile arrays");
+        for (int m2 = 0; m2 < p->pot_terms; ++m2) {
+          s->term_type.push_back(p->pot_term_type[m2]);
+          s->term_param.push_back(p->pot_term_param[m2]);
+          s->basis.emplace_back(p->pot_basis + static_cast<size_t>(m2) * p->dim,
+                                p->pot_basis + static_cast<size_t>(m2 + 1) * p->dim);
+        }
+      }
       P.m = s;
       break;
     }

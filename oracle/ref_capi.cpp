@@ -82,6 +82,60 @@ class LatticeCondensate : public qoc::HamiltonianModel {
   double dx_, w2_, v0_, k_, kappa_;
 };
 
+// A user plugin of the reference's HamiltonianModel contract whose potential has the separable
+// form V(x_i, u) = sum_m a_m[i] f_m(u) (qoc_gpu.h QOC_POT_BASIS): run by the REFERENCE's own
+// strang path through its virtual potential() / potential_derivative().
+class BasisCondensate : public qoc::HamiltonianModel {
+ public:
+  explicit BasisCondensate(const qoc_problem_v1* p) : x_(p->dim), kin_(p->dim), kappa_(p->kappa) {
+    const int n = p->dim;
+    for (int i = 0; i < n; ++i) {
+      x_[i] = p->grid_x[i];
+      kin_[i] = p->kinetic[i];
+    }
+    dx_ = n > 1 ? x_[1] - x_[0] : 1.0;
+    for (int m = 0; m < p->pot_terms; ++m) {
+      type_.push_back(p->pot_term_type[m]);
+      param_.push_back(p->pot_term_param[m]);
+      RVec a(n);
+      for (int i = 0; i < n; ++i) a[i] = p->pot_basis[(size_t)m * n + i];
+      basis_.push_back(a);
+    }
+  }
+  qoc::PropagatorKind kind() const override { return qoc::PropagatorKind::strang; }
+  int state_dim() const override { return static_cast<int>(x_.size()); }
+  int channels() const override { return 1; }
+  double ip_weight() const override { return dx_; }
+  const RVec& kinetic_spectrum() const override { return kin_; }
+  RVec potential(const RVec& u) const override { return sum(u[0], false); }
+  RVec potential_derivative(int, const RVec& u) const override { return sum(u[0], true); }
+  double nonlinearity() const override { return kappa_; }
+
+ private:
+  RVec sum(double u, bool deriv) const {
+    RVec v = RVec::Zero(x_.size());
+    for (size_t m = 0; m < basis_.size(); ++m) {
+      const double q = param_[m];
+      double f;
+      if (type_[m] == QOC_TERM_POWER) {
+        const int k = static_cast<int>(q);
+        f = deriv ? (k > 0 ? k * std::pow(u, k - 1) : 0.0) : std::pow(u, k);
+      } else if (type_[m] == QOC_TERM_COS) {
+        f = deriv ? -q * std::sin(q * u) : std::cos(q * u);
+      } else {
+        f = deriv ? q * std::cos(q * u) : std::sin(q * u);
+      }
+      for (Eigen::Index i = 0; i < v.size(); ++i) v[i] += basis_[m][i] * f;
+    }
+    return v;
+  }
+  RVec x_, kin_;
+  double dx_, kappa_;
+  std::vector<int> type_;
+  std::vector<double> param_;
+  std::vector<RVec> basis_;
+};
+
 std::shared_ptr<const qoc::HamiltonianModel> make_model(const qoc_problem_v1* p, int b) {
   const int d = p->dim, C = p->channels;
   const size_t dd = static_cast<size_t>(d) * d;
@@ -147,6 +201,7 @@ std::shared_ptr<const qoc::HamiltonianModel> make_model(const qoc_problem_v1* p,
       const double x0 = p->grid_x[0], dx = p->grid_x[1] - p->grid_x[0];
       if (p->potential == QOC_POT_TRAP)
         return std::make_shared<qoc::TrappedCondensateModel>(d, x0, x0 + d * dx, p->pot_params[0], p->kappa);
+      if (p->potential == QOC_POT_BASIS) return std::make_shared<BasisCondensate>(p);
       return std::make_shared<LatticeCondensate>(p->grid_x, p->kinetic, d, p->pot_params[0], p->pot_params[1],
                                                  p->pot_params[2], p->kappa);
     }

@@ -16,7 +16,9 @@ QOC_ABI_VERSION = 2
 
 QOC_OK, QOC_EINVAL, QOC_ELOGIC, QOC_ECUDA, QOC_ENCCL, QOC_ERUNTIME = range(6)
 KIND_DENSE, KIND_TRIDIAG, KIND_BITFLIP, KIND_STRANG, KIND_DENSITY = range(5)
-POT_TRAP, POT_LATTICE = range(2)
+POT_TRAP, POT_LATTICE, POT_BASIS = range(3)
+TERM_POWER, TERM_COS, TERM_SIN = range(3)
+MAX_POT_TERMS = 8
 VARIANT_INTERPOLATED, VARIANT_SPLIT = range(2)
 PLAN_ASSEMBLED, PLAN_DIRECT = range(2)
 PARTITION_BALANCED, PARTITION_UNIFORM, PARTITION_EXPLICIT = range(3)
@@ -37,6 +39,8 @@ class ProblemV1(C.Structure):
         ("nspins", C.c_int32), ("bf_axis", _ip), ("bf_coef", _dp),
         ("kinetic", _dp), ("grid_x", _dp), ("potential", C.c_int32),
         ("pot_params", C.c_double * 4), ("kappa", C.c_double),
+        ("pot_terms", C.c_int32), ("pot_reserved", C.c_int32),
+        ("pot_term_type", _ip), ("pot_term_param", _dp), ("pot_basis", _dp),
         ("initial", _dp), ("target", _dp), ("penalty", _dp),
     ]
 

@@ -133,6 +133,10 @@ struct DevProblem {
   int potential;
   double pp[4];
   double kappa;
+  int pot_terms;               // QOC_POT_BASIS: V = sum_m pot_basis[m][i] f_m(u)
+  int pot_type[8];
+  double pot_param[8];
+  const double* pot_basis;     // [pot_terms][d]
   int naive;  // GradientOptions::naive_nonlinear_adjoint (split-step adjoints, propagation.cpp:159-166)
   // states and penalty
   const double2* init;  // [B][d]

@@ -350,6 +350,23 @@ void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaS
       P.potential = p->potential;
       for (int i = 0; i < 4; ++i) P.pp[i] = p->pot_params[i];
       P.kappa = p->kappa;
+      if (p->potential < QOC_POT_TRAP || p->potential > QOC_POT_BASIS) fail(QOC_EINVAL, "unknown potential kind");
+      if (p->potential == QOC_POT_BASIS) {  // caller-supplied potential()/potential_derivative(), separable form
+        if (p->pot_terms < 1 || p->pot_terms > QOC_MAX_POT_TERMS || !p->pot_term_type || !p->pot_term_param ||
+            !p->pot_basis)
+          fail(QOC_EINVAL, "basis potential needs 1..QOC_MAX_POT_TERMS terms with type, parameter and profile arrays");
+        P.pot_terms = p->pot_terms;
+        for (int m = 0; m < p->pot_terms; ++m) {
+          const int ty = p->pot_term_type[m];
+          const double q = p->pot_term_param[m];
+          if (ty < QOC_TERM_POWER || ty > QOC_TERM_SIN) fail(QOC_EINVAL, "unknown potential term type");
+          if (ty == QOC_TERM_POWER && (q < 0.0 || q != std::floor(q)))
+            fail(QOC_EINVAL, "power terms take a non-negative integer exponent");
+          P.pot_type[m] = ty;
+          P.pot_param[m] = q;
+        }
+        P.pot_basis = out.put<double>(p->pot_basis, (size_t)p->pot_terms * d);
+      }
       break;
     }
     default:

@@ -42,6 +42,7 @@ struct StrangCtx {
   double2 *A, *B, *S, *Q;  // smem work vectors [d]
   double* red;           // smem [ST_T / 32]
   double2* kx;           // smem [d] (cos k x_i, sin k x_i) of the lattice potential
+  double* pf;            // smem [2][QOC_MAX_POT_TERMS]: f_m(u), f_m'(u) of the basis potential (per step)
 };
 
 // V(x_i, u) and dV/du for grid point i.  The cos^2 lattice uses cos/sin(k(x_i - u)) by angle
@@ -49,14 +50,40 @@ struct StrangCtx {
 struct PotStep {
   double2 cs;
 };
-__device__ __forceinline__ PotStep pot_step(const DevProblem& P, double u) {
+__device__ __forceinline__ PotStep pot_step(const StrangCtx& X, const DevProblem& P, double u) {
   PotStep S{cx(1.0, 0.0)};
-  if (P.potential != QOC_POT_TRAP) {
+  if (P.potential == QOC_POT_LATTICE) {
     double sn, cn;
     sincos(P.pp[2] * u, &sn, &cn);
     S.cs = cx(cn, sn);
+  } else if (P.potential == QOC_POT_BASIS) {
+    // the terms' control factors once per step (block-uniform call sites)
+    __syncthreads();
+    const int m = threadIdx.x;
+    if (m < P.pot_terms) {
+      const double q = P.pot_param[m];
+      double f, df;
+      if (P.pot_type[m] == QOC_TERM_POWER) {
+        const int k = (int)q;
+        f = pow(u, (double)k);
+        df = k > 0 ? k * pow(u, (double)(k - 1)) : 0.0;
+      } else {
+        double sn, cn;
+        sincos(q * u, &sn, &cn);
+        f = P.pot_type[m] == QOC_TERM_COS ? cn : sn;
+        df = P.pot_type[m] == QOC_TERM_COS ? -q * sn : q * cn;
+      }
+      X.pf[m] = f;
+      X.pf[QOC_MAX_POT_TERMS + m] = df;
+    }
+    __syncthreads();
   }
   return S;
+}
+__device__ __forceinline__ double basis_sum(const StrangCtx& X, const DevProblem& P, int i, int deriv) {
+  double v = 0.0;
+  for (int m = 0; m < P.pot_terms; ++m) v = fma(P.pot_basis[(size_t)m * X.d + i], X.pf[deriv * QOC_MAX_POT_TERMS + m], v);
+  return v;
 }
 
 // dst = DFT_sign(pre . src) unnormalised (sign -1 forward, +1 inverse); pre may be null.
@@ -189,6 +216,7 @@ __device__ __forceinline__ double potential_du(const DevProblem& P, double x, do
 
 __device__ __forceinline__ double potential_at(const StrangCtx& X, const DevProblem& P, int i, double u,
                                                const PotStep& S) {
+  if (P.potential == QOC_POT_BASIS) return basis_sum(X, P, i, 0);
   const double x = P.grid_x[i];
   if (P.potential == QOC_POT_TRAP) return potential(P, x, u);
   const double2 k = X.kx[i];
@@ -197,6 +225,7 @@ __device__ __forceinline__ double potential_at(const StrangCtx& X, const DevProb
 }
 __device__ __forceinline__ double potential_du_at(const StrangCtx& X, const DevProblem& P, int i, double u,
                                                   const PotStep& S) {
+  if (P.potential == QOC_POT_BASIS) return basis_sum(X, P, i, 1);
   if (P.potential == QOC_POT_TRAP) return potential_du(P, P.grid_x[i], u);
   const double2 k = X.kx[i];
   const double c = fma(k.x, S.cs.x, k.y * S.cs.y);   // cos(k(x - u))
@@ -208,7 +237,7 @@ __device__ __forceinline__ double potential_du_at(const StrangCtx& X, const DevP
 __device__ void strang_forward(const StrangCtx& X, const DevProblem& P, double u, double dt) {
   transform(X, X.A, X.B, -1, nullptr, 1.0);
   transform(X, X.B, X.S, +1, P.kin_fwd, X.inv_n);  // psi_a
-  const PotStep ps = pot_step(P, u);
+  const PotStep ps = pot_step(X, P, u);
   for (int i = threadIdx.x; i < X.d; i += ST_T) {
     const double2 pa = X.S[i];
     const double w = potential_at(X, P, i, u, ps) + P.kappa * cabs2(pa);
@@ -230,7 +259,7 @@ __device__ double strang_backward(const StrangCtx& X, const DevProblem& P, doubl
   transform(X, X.A, X.B, -1, nullptr, 1.0);
   transform(X, X.B, X.A, +1, P.kin_adj, X.inv_n);  // chi_b in A
   double g = 0.0;
-  const PotStep pst = pot_step(P, u);
+  const PotStep pst = pot_step(X, P, u);
   for (int i = threadIdx.x; i < d; i += ST_T) {
     const double2 pa = X.S[i], cb = X.A[i];
     const double dens = cabs2(pa);
@@ -280,6 +309,7 @@ __device__ __forceinline__ StrangCtx make_ctx(const DevProblem& P, unsigned char
     X.red = reinterpret_cast<double*>(tw);
   }
   X.kx = reinterpret_cast<double2*>(X.red + ST_T / 32);
+  X.pf = reinterpret_cast<double*>(X.kx + d);
   for (int i = threadIdx.x; i < d; i += ST_T) {
     double sn, cn;
     sincos(P.pp[2] * P.grid_x[i], &sn, &cn);
@@ -292,7 +322,7 @@ __device__ __forceinline__ StrangCtx make_ctx(const DevProblem& P, unsigned char
 size_t strang_smem(int d) {
   const bool pow2 = (d & (d - 1)) == 0;
   return sizeof(double2) * (4 * (size_t)d + (pow2 ? (d / 2 > 0 ? d / 2 : 1) : 0)) + sizeof(double) * (ST_T / 32) +
-         sizeof(double2) * (size_t)d;
+         sizeof(double2) * (size_t)d + sizeof(double) * 2 * QOC_MAX_POT_TERMS;
 }
 
 __device__ __forceinline__ void load_vec(double2* dst, const double2* src, int d) {
@@ -303,7 +333,7 @@ __device__ __forceinline__ void store_vec(double2* dst, const double2* src, int 
   for (int i = threadIdx.x; i < d; i += ST_T) dst[i] = src[i];
 }
 
-__global__ void __launch_bounds__(ST_T) strang_task_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done) {
+__global__ void __launch_bounds__(ST_T, 1) strang_task_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done) {
   const int n = blockIdx.x, b = blockIdx.y;
   if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
   extern __shared__ __align__(16) unsigned char smem[];

@@ -287,3 +287,60 @@ class CondensateModel(HamiltonianModel):
         for i in range(4):
             s.pot_params[i] = float(self.params[i])
         s.kappa = self.kappa
+
+
+class BasisCondensateModel(CondensateModel):
+    """A condensate whose potential is supplied by the caller -- the device side of the
+    reference's virtual potential(u) / potential_derivative(c, u) (propagation.hpp:35-36) -- in
+    the separable form V(x_i, u) = sum_m a_m[i] f_m(u) with f_m in {u^k, cos(w u), sin(w u)}.
+
+    terms: list of (profile a_m sampled on the grid, kind "power" | "cos" | "sin", parameter)."""
+
+    _KINDS = {"power": abi.TERM_POWER, "cos": abi.TERM_COS, "sin": abi.TERM_SIN}
+
+    def __init__(self, points: int, x_min: float, x_max: float, terms, kappa: float):
+        super().__init__(points, x_min, x_max, abi.POT_BASIS, (), kappa)
+        if not 1 <= len(terms) <= abi.MAX_POT_TERMS:
+            raise ValueError(f"1..{abi.MAX_POT_TERMS} potential terms")
+        self.basis = np.ascontiguousarray([np.broadcast_to(np.asarray(a, dtype=np.float64), (points,))
+                                           for a, _, _ in terms])
+        self.term_type = np.array([self._KINDS[k] for _, k, _ in terms], dtype=np.int32)
+        self.term_param = np.array([float(q) for _, _, q in terms])
+        for t, q in zip(self.term_type, self.term_param):
+            if t == abi.TERM_POWER and (q < 0 or q != int(q)):
+                raise ValueError("power terms take a non-negative integer exponent")
+
+    @classmethod
+    def lattice(cls, points, x_min, x_max, w2, v0, k, kappa):
+        """The cos^2 lattice of BASELINE config 4 in basis form:
+        v0 cos^2(k(x - u)) = v0/2 + v0/2 [cos(2kx) cos(2ku) + sin(2kx) sin(2ku)]."""
+        x = x_min + np.arange(points) * ((x_max - x_min) / points)
+        return cls(points, x_min, x_max, [(0.5 * w2 * x * x + 0.5 * v0, "power", 0),
+                                          (0.5 * v0 * np.cos(2 * k * x), "cos", 2 * k),
+                                          (0.5 * v0 * np.sin(2 * k * x), "sin", 2 * k)], kappa)
+
+    def _f(self, u0: float, deriv: bool) -> np.ndarray:
+        out = np.empty(len(self.term_type))
+        for m, (t, q) in enumerate(zip(self.term_type, self.term_param)):
+            if t == abi.TERM_POWER:
+                k = int(q)
+                out[m] = (k * u0 ** (k - 1) if k > 0 else 0.0) if deriv else u0 ** k
+            elif t == abi.TERM_COS:
+                out[m] = -q * np.sin(q * u0) if deriv else np.cos(q * u0)
+            else:
+                out[m] = q * np.cos(q * u0) if deriv else np.sin(q * u0)
+        return out
+
+    def potential(self, u) -> np.ndarray:
+        return self._f(float(np.asarray(u).reshape(-1)[0]), False) @ self.basis
+
+    def potential_derivative(self, c, u) -> np.ndarray:
+        return self._f(float(np.asarray(u).reshape(-1)[0]), True) @ self.basis
+
+    def pack_into(self, s, keep):
+        super().pack_into(s, keep)
+        keep += [self.basis, self.term_type, self.term_param]
+        s.pot_terms = len(self.term_type)
+        s.pot_term_type = abi.iptr(self.term_type)
+        s.pot_term_param = abi.dptr(self.term_param)
+        s.pot_basis = abi.dptr(self.basis)
