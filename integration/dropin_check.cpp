@@ -59,6 +59,59 @@ static bool throws_logic(const char* name, F&& f) {
   return ok;
 }
 
+// A user plugin: a condensate in a tilted, breathing trap.  The reference steps it through its
+// virtual potential()/potential_derivative(); the device reads the separable form.
+class TiltedTrap : public HamiltonianModel, public DevicePotentialBasis {
+ public:
+  TiltedTrap(int n, double x_min, double x_max, double kappa) : x_(n), kin_(n), kappa_(kappa) {
+    const double len = x_max - x_min;
+    dx_ = len / n;
+    const double pi = std::acos(-1.0);
+    for (int i = 0; i < n; ++i) {
+      x_[i] = x_min + i * dx_;
+      const int f = i <= n / 2 ? i : i - n;
+      const double k = 2.0 * pi * f / len;
+      kin_[i] = 0.5 * k * k;
+    }
+  }
+  PropagatorKind kind() const override { return PropagatorKind::strang; }
+  int state_dim() const override { return static_cast<int>(x_.size()); }
+  int channels() const override { return 1; }
+  double ip_weight() const override { return dx_; }
+  const RVec& kinetic_spectrum() const override { return kin_; }
+  double nonlinearity() const override { return kappa_; }
+  RVec potential(const RVec& u) const override {  // x^2/2 + 0.3 x u + 0.05 x^2 u^2 + 0.4 sin(1.3 u) cos(x)
+    RVec v(x_.size());
+    for (Eigen::Index i = 0; i < x_.size(); ++i)
+      v[i] = 0.5 * x_[i] * x_[i] + 0.3 * x_[i] * u[0] + 0.05 * x_[i] * x_[i] * u[0] * u[0] +
+             0.4 * std::sin(1.3 * u[0]) * std::cos(x_[i]);
+    return v;
+  }
+  RVec potential_derivative(int, const RVec& u) const override {
+    RVec v(x_.size());
+    for (Eigen::Index i = 0; i < x_.size(); ++i)
+      v[i] = 0.3 * x_[i] + 0.1 * x_[i] * x_[i] * u[0] + 0.4 * 1.3 * std::cos(1.3 * u[0]) * std::cos(x_[i]);
+    return v;
+  }
+  std::vector<PotentialTerm> potential_terms() const override {
+    const Eigen::Index n = x_.size();
+    RVec a(n), b(n), c(n), e(n);
+    for (Eigen::Index i = 0; i < n; ++i) {
+      a[i] = 0.5 * x_[i] * x_[i];
+      b[i] = 0.3 * x_[i];
+      c[i] = 0.05 * x_[i] * x_[i];
+      e[i] = 0.4 * std::cos(x_[i]);
+    }
+    return {{a, PotentialTerm::Kind::power, 0.0}, {b, PotentialTerm::Kind::power, 1.0},
+            {c, PotentialTerm::Kind::power, 2.0}, {e, PotentialTerm::Kind::sine, 1.3}};
+  }
+  const RVec& potential_grid() const override { return x_; }
+
+ private:
+  RVec x_, kin_;
+  double dx_ = 1.0, kappa_;
+};
+
 int main() {
   bool all = true;
   {  // BASELINE config 1 physics from the reference's spin operators (sigma/2): two spins
@@ -135,6 +188,20 @@ int main() {
     all &= compare("condensate_preset_kat8", run_ism(p, u0, cfg, sv), run_ism_gpu(p, u0, cfg, sv), 1e-9, 1e-10);
     sv.gradient.naive_nonlinear_adjoint = true;
     all &= compare("condensate_naive_adjoint", run_ism(p, u0, cfg, sv), run_ism_gpu(p, u0, cfg, sv), 1e-9, 1e-10);
+  }
+  {  // a user-defined split-step model (virtual potential on the reference side, basis form on the device)
+    ControlProblem p = condensate_problem(50, -10.0, 10.0, 6.0, 1.0, 8.0, 256);  // grid, states, penalty
+    p.model = std::make_shared<TiltedTrap>(50, -10.0, 10.0, 1.0);
+    const ControlField u0 = ramp_control(p.grid, 1.0, 0.0);
+    IsmConfig cfg;
+    cfg.subintervals = 4;
+    cfg.max_outer = 6;
+    cfg.eta = 0.0;
+    cfg.variant = IsmConfig::Variant::split;
+    cfg.log_exact_objective = true;
+    SolverSpec sv;
+    sv.step_size = 0.1;
+    all &= compare("user_potential_plugin", run_ism(p, u0, cfg, sv), run_ism_gpu(p, u0, cfg, sv), 1e-9, 1e-10);
   }
   {  // the density-matrix spin chain (cn_conjugation, the reference's `spins` preset builder)
     ControlProblem p = spin_chain_problem(3, {{1, 2}, {2, 3}}, 1.0, 1.0, 64, 0.0);

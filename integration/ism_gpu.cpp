@@ -67,7 +67,8 @@ IsmRun run_ism_gpu(const ControlProblem& p, const ControlField& u0, const IsmCon
   // keep-alive buffers of the operator payload
   CMat h0;
   std::vector<Complex> lin, quad;
-  std::vector<double> grid_x;
+  std::vector<double> grid_x, pot_basis, pot_param;
+  std::vector<int32_t> pot_type;
   switch (m.kind()) {
     case PropagatorKind::cn_dense:
     case PropagatorKind::cn_conjugation: {  // same DenseModel payload; states are d x d matrices
@@ -94,14 +95,35 @@ IsmRun run_ism_gpu(const ControlProblem& p, const ControlField& u0, const IsmCon
       break;
     }
     case PropagatorKind::strang: {
-      const auto* tc = dynamic_cast<const TrappedCondensateModel*>(&m);
-      if (!tc) throw std::logic_error("split-step model without a device potential payload");
       q.kind = QOC_KIND_STRANG;
-      q.kinetic = tc->kinetic_spectrum().data();
-      q.grid_x = tc->grid_points().data();
-      q.potential = QOC_POT_TRAP;
-      q.pot_params[0] = tc->trap_distance();
-      q.kappa = tc->nonlinearity();
+      q.kinetic = m.kinetic_spectrum().data();
+      q.kappa = m.nonlinearity();
+      if (const auto* tc = dynamic_cast<const TrappedCondensateModel*>(&m)) {
+        q.grid_x = tc->grid_points().data();
+        q.potential = QOC_POT_TRAP;
+        q.pot_params[0] = tc->trap_distance();
+      } else if (const auto* pb = dynamic_cast<const DevicePotentialBasis*>(&m)) {
+        // a user-defined potential in separable form (ism_gpu.hpp)
+        const std::vector<PotentialTerm> terms = pb->potential_terms();
+        if (terms.empty() || terms.size() > QOC_MAX_POT_TERMS)
+          throw std::logic_error("between 1 and QOC_MAX_POT_TERMS potential terms are supported");
+        pot_basis.resize(terms.size() * size_t(d));
+        for (size_t t = 0; t < terms.size(); ++t) {
+          if (terms[t].profile.size() != d) throw std::invalid_argument("potential profile length != grid size");
+          std::copy(terms[t].profile.data(), terms[t].profile.data() + d, pot_basis.begin() + t * size_t(d));
+          pot_type.push_back(static_cast<int32_t>(terms[t].kind));
+          pot_param.push_back(terms[t].parameter);
+        }
+        q.grid_x = pb->potential_grid().data();
+        q.potential = QOC_POT_BASIS;
+        q.pot_terms = static_cast<int32_t>(terms.size());
+        q.pot_term_type = pot_type.data();
+        q.pot_term_param = pot_param.data();
+        q.pot_basis = pot_basis.data();
+      } else {
+        throw std::logic_error("split-step model without a device potential payload: derive from "
+                               "qoc::DevicePotentialBasis (integration/ism_gpu.hpp)");
+      }
       break;
     }
   }

@@ -270,3 +270,24 @@ def ref_ism_run(p: I.ControlProblem, u0, cfg: I.IsmConfig, solver: I.SolverSpec)
                 else:
                     it.events.extend(ev)
     return [I.IsmRun(u[b], r) for b, r in enumerate(runs)]
+
+
+def basis_fixture(seed, points=32, steps=16, duration=0.4, kappa=1.5, alpha=0.05):
+    """A caller-defined condensate potential through the basis plugin (QOC_POT_BASIS): a breathing,
+    tilted trap in a modulated lattice,
+        V(x, u) = x^2/2 + 0.3 x u + 0.05 x^2 u^2 + 1.2 cos^2(0.8 (x - u)),
+    with states and control drawn like fixtures::strang_fixture."""
+    from paper_1603_01237_b200.models import BasisCondensateModel
+    x_min, x_max = -8.0, 8.0
+    x = x_min + np.arange(points) * ((x_max - x_min) / points)
+    k, v0 = 0.8, 1.2
+    terms = [(0.5 * x * x + 0.5 * v0, "power", 0), (0.3 * x, "power", 1), (0.05 * x * x, "power", 2),
+             (0.5 * v0 * np.cos(2 * k * x), "cos", 2 * k), (0.5 * v0 * np.sin(2 * k * x), "sin", 2 * k)]
+    model = BasisCondensateModel(points, x_min, x_max, terms, kappa)
+    ini, tgt, ctl = np.empty(2 * points), np.empty(2 * points), np.empty(steps)
+    lib().oracle_strang_fixture(C.c_uint32(seed), points, C.c_double(x_min), C.c_double(x_max), steps,
+                                C.c_double(0.9), abi.dptr(ini), abi.dptr(tgt), abi.dptr(ctl))
+    grid = I.TimeGrid.over(0.0, duration, steps)
+    problem = I.ControlProblem(model, grid, ini.view(np.complex128).copy(), tgt.view(np.complex128).copy(),
+                               np.full(steps, alpha))
+    return problem, ctl.reshape(1, steps)

@@ -21,6 +21,6 @@ def test_reference_run_ism_vs_device_dropin():
     cases = {c["case"]: c for c in lines if "case" in c}
     for name in ("spin2_config1_200it", "spin2_direct_plan", "rotor_preset_quadratic", "condensate_preset_kat8",
                  "condensate_naive_adjoint", "monotonic_solver_rejected", "monotonic_solver_rejected_reference",
-                 "spin2_monotonic", "spin2_monotonic_events", "spin2_newton", "density_matrix_spin_chain"):
+                 "spin2_monotonic", "spin2_monotonic_events", "spin2_newton", "density_matrix_spin_chain", "user_potential_plugin"):
         assert name in cases and cases[name]["ok"], (name, cases.get(name), out.stderr[-2000:])
     assert out.returncode == 0 and lines[-1] == {"all_ok": True}

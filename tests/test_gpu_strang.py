@@ -101,3 +101,48 @@ def test_gpe1024_config4(ctx, tag):
     compare_run(g, fx, tag, ctl_tol=1e-9 if tag == "literal" else 5e-9, tv_tol=None if tag == "literal" else 2e-9)
     ex = np.array([it.exact_objective for it in g.record.iterations[1:]])
     assert np.max(np.abs(ex - fx[f"{tag}_exact"][1:])) < 1e-10
+
+
+@pytest.mark.parametrize("parts", [1, 4])
+@pytest.mark.parametrize("naive", [False, True])
+def test_basis_potential_plugin(ctx, parts, naive):
+    # a caller-defined potential (the reference's virtual potential()/potential_derivative(),
+    # propagation.hpp:35-36) in separable form; the oracle's version is pinned to the reference
+    # running a HamiltonianModel subclass (test_reference_pinning.py::test_basis_potential_plugin)
+    p, u = O.basis_fixture(6400)
+    fin = I.propagate_final(p, u, ctx)
+    assert np.max(np.abs(fin - O.propagate_final(p, u))) < 1e-13
+    for form in ("overlap", "tracking"):
+        v, g = I.objective_gradient(p, u, form, naive=naive, ctx=ctx)
+        vr, gr = O.objective_gradient(p, u, form, naive=naive)
+        assert abs(v[0] - vr[0]) < 1e-13 and np.max(np.abs(g - gr)) < 1e-13
+    cfg = I.IsmConfig(subintervals=parts, max_outer=5, eta=0.0, variant="split", log_exact_objective=True)
+    sv = I.SolverSpec(step_size=0.3, naive_nonlinear_adjoint=naive)
+    g = I.run_ism(p, u, cfg, sv, ctx)
+    r = O.ism_run(p, u, cfg, sv)[0]
+    assert rel(g.control, r.control) < 1e-9
+    assert np.nanmax(np.abs(g.record.objectives() - r.record.objectives())) < 1e-10
+    ex = np.array([it.exact_objective for it in g.record.iterations[1:]])
+    exr = np.array([it.exact_objective for it in r.record.iterations[1:]])
+    assert np.max(np.abs(ex - exr)) < 1e-10
+
+
+def test_basis_form_of_config4_lattice(ctx):
+    # BASELINE config 4's potential expressed through the plugin reproduces the built-in kind
+    from paper_1603_01237_b200 import abi
+    from paper_1603_01237_b200.models import BasisCondensateModel
+    w = problems.gpe1024(subintervals=8, iterations=3, rho=5.0, points=256, steps=400, T=0.2)
+    a = I.run_ism(w.problem, w.u0, w.config, w.solver, ctx)
+    bas = BasisCondensateModel.lattice(256, -16.0, 16.0, 1.0, 5.0, 1.0, 10.0)
+    pb = I.ControlProblem(bas, w.problem.grid, w.problem.initial, w.problem.target, w.problem.penalty)
+    b = I.run_ism(pb, w.u0, w.config, w.solver, ctx)
+    assert rel(b.control, a.control) < 1e-10 or np.max(np.abs(b.control - a.control)) < 1e-12
+    assert np.nanmax(np.abs(a.record.objectives() - b.record.objectives())) < 1e-11
+
+
+def test_basis_potential_rejections(ctx):
+    from paper_1603_01237_b200.models import BasisCondensateModel
+    with pytest.raises(ValueError):
+        BasisCondensateModel(16, -1.0, 1.0, [(1.0, "power", 1.5)], 0.0)
+    with pytest.raises(ValueError):
+        BasisCondensateModel(16, -1.0, 1.0, [(1.0, "power", 0)] * 9, 0.0)

@@ -257,3 +257,29 @@ def test_newton_on_the_condensate_split_variant():
     cfg = I.IsmConfig(subintervals=2, max_outer=2, eta=0.0, variant="split", partition="uniform")
     sv = I.SolverSpec(kind="newton", step_size=0.2, gmres_max_iter=12)
     compare_newton(O.ref_ism_run(p, u, cfg, sv)[0], O.ism_run(p, u, cfg, sv)[0])
+
+
+# ---- a caller-defined potential (the virtual potential()/potential_derivative() plugin) ---------
+@pytest.mark.parametrize("parts", [1, 2, 4])
+@pytest.mark.parametrize("naive", [False, True])
+def test_basis_potential_plugin(parts, naive):
+    # the reference runs its own split-step path on a HamiltonianModel subclass defined in
+    # oracle/ref_capi.cpp (BasisCondensate); the oracle evaluates the same separable form
+    p, u = O.basis_fixture(6400)
+    cfg = I.IsmConfig(subintervals=parts, max_outer=4, eta=0.0, variant="split", log_exact_objective=True,
+                      partition="uniform")
+    sv = I.SolverSpec(step_size=0.3, naive_nonlinear_adjoint=naive)
+    compare(O.ref_ism_run(p, u, cfg, sv)[0], O.ism_run(p, u, cfg, sv)[0])
+
+
+def test_basis_form_of_the_lattice_equals_the_lattice_kind():
+    from paper_1603_01237_b200 import abi
+    from paper_1603_01237_b200.models import BasisCondensateModel, CondensateModel
+    p, u = O.basis_fixture(6401)
+    lat = CondensateModel(32, -8.0, 8.0, abi.POT_LATTICE, [1.0, 5.0, 1.0], 1.5)
+    bas = BasisCondensateModel.lattice(32, -8.0, 8.0, 1.0, 5.0, 1.0, 1.5)
+    cfg = I.IsmConfig(subintervals=2, max_outer=3, eta=0.0, variant="split")
+    sv = I.SolverSpec(step_size=0.3)
+    a = O.ism_run(I.ControlProblem(lat, p.grid, p.initial, p.target, p.penalty), u, cfg, sv)[0]
+    b = O.ism_run(I.ControlProblem(bas, p.grid, p.initial, p.target, p.penalty), u, cfg, sv)[0]
+    compare(a, b, ctl_abs=1e-12, obj_abs=1e-12)

@@ -25,18 +25,23 @@ fi
 if [[ " $sections " == *" ncu "* ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file "$out/launches_default.csv" \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-ttf > "$out/ncu_launch.log" 2>&1; echo "launches rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:dense_nm_assemble|dense_pc_eval16" -c 2 \
-    -o "$out/full_batch4096" python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-ttf > "$out/ncu_full_batch.log" 2>&1
-  echo "full batch rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:bitflip_horizon_cluster" -c 1 \
-    -o "$out/full_ising10" python bench.py --workload ising10 --steps 1 --warmup 3 --no-cpu-baseline --no-ttf \
-    > "$out/ncu_full_ising.log" 2>&1; echo "full ising rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:strang_task" -c 1 \
-    -o "$out/full_gpe1024" python bench.py --workload gpe1024 --steps 1 --warmup 3 --no-cpu-baseline --no-ttf \
-    > "$out/ncu_full_gpe.log" 2>&1; echo "full gpe rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:tri_pc_assemble" -c 1 \
-    -o "$out/full_rotor21" python bench.py --workload rotor21 --steps 1 --warmup 3 --no-cpu-baseline --no-ttf \
-    > "$out/ncu_full_rotor.log" 2>&1; echo "full rotor rc=$?"
+  # one --set full capture per dominant kernel, taken inside the outer iterations (the bootstrap's
+  # launches of the same kernels are skipped)
+  cap() {  # cap NAME REGEX SKIP bench-args...
+    local name=$1 re=$2 skip=$3; shift 3
+    timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$re" --launch-skip "$skip" -c 1 \
+      -o "$out/full_$name" python bench.py "$@" --steps 2 --warmup 3 --no-cpu-baseline --no-ttf > "$out/ncu_full_$name.log" 2>&1
+    echo "full $name rc=$?"
+  }
+  cap batch4096_assembly dense_nm_assemble 2
+  cap batch4096_evaluation dense_pc_eval16 2
+  cap ising10_node_sweeps bitflip_horizon_cluster 2 --workload ising10
+  cap ising10_block_products bitflip_block_kernel 1 --workload ising10 --blocks 8
+  cap gpe1024_task strang_task 2 --workload gpe1024
+  cap rotor21_assembly tri_pc_assemble 2 --workload rotor21
+  for f in "$out"/full_*.ncu-rep; do
+    [ -f "$f" ] && python tools/ncu_brief.py "$f" >> "$out/ncu_brief.txt" 2>&1
+  done
 fi
 if [[ " $sections " == *" sanitize "* ]]; then
   timeout 1200 compute-sanitizer --tool memcheck --leak-check full python __graft_entry__.py > "$out/memcheck.log" 2>&1
