@@ -297,13 +297,37 @@ def cpu_reference(name: str, warmup: int, steps: int, world: int = 1):
         w.problem.model = w.problem.model.to_dense()
     w.solver.step_size = w.rho_fast
     w.config.max_outer = warmup + steps
+    p = w.problem
+    work = 2.0 * p.grid.steps * p.batch * steps
+    # The reference ITSELF where it was compiled (oracle/_ref/libqocref.so: /root/reference's own
+    # run_ism and everything under it, built from source against oracle/eigen_shim; it travels
+    # with the snapshot): its WorkerPool runs the L tasks on `workers` threads, problems of the
+    # batch one after another.  Config 3 stays on the oracle port: the reference's dense LU at
+    # d = 1024 is ~1.4e14 flop per iteration.
+    if arith == O.REFERENCE and O.REF_LIBPATH.exists() and not os.environ.get("QOC_BENCH_PORT"):
+        w.config.partition = "balanced"
+        if p.grid.steps % w.config.subintervals:  # Decomposition::uniform throws (ism.cpp:234): largest divisor
+            w.config.subintervals = max(L for L in range(1, w.config.subintervals + 1) if p.grid.steps % L == 0)
+        # the reference's own WorkerPool (runtime.cpp:72-90) over the L tasks, the sample's problems
+        # one after another (one run_ism per host thread with workers = 1 measured slower here:
+        # 1.7e5 vs 2.05e5 steps/s on 8 cores)
+        w.config.workers = threads
+        t0 = time.perf_counter()
+        runs = O.ref_ism_run(p, w.u0, w.config, w.solver)
+        wall = time.perf_counter() - t0
+        secs = sum(it.device_seconds for r in runs for it in r.record.iterations[warmup + 1:warmup + steps + 1])
+        how = f"WorkerPool of {threads} threads, problems in sequence"
+        return {"value": work / secs, "unit": "steps/s", "cores": threads, "kind": "reference",
+                "sample": f"{desc}; the reference's own run_ism compiled from /root/reference (Eigen-subset shim), "
+                          f"L = {w.config.subintervals}, {steps} timed outer iterations after {warmup} warm-up, {how}",
+                "seconds": secs, "wall": wall, "seconds_per_iteration": secs / steps, "sample_problems": p.batch}
     t0 = time.perf_counter()
     runs = O.ism_run(w.problem, w.u0, w.config, w.solver, arith, threads=threads)
     wall = time.perf_counter() - t0
     its = runs[0].record.iterations
     secs = sum(it.device_seconds for it in its[warmup + 1:warmup + steps + 1])
-    p = w.problem
-    work = 2.0 * p.grid.steps * p.batch * steps
+    if p.batch > 1:  # problems run concurrently on the threads: the sample's wall clock, not one problem's
+        secs = wall * steps / float(warmup + steps)
     return {"value": work / secs, "unit": "steps/s", "cores": threads, "kind": "port",
             "sample": f"{desc}; {steps} timed outer iterations after {warmup} warm-up, "
                       f"{'dense-LU reference' if arith == O.REFERENCE else 'structured (Neumann) Cayley'} "

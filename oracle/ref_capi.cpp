@@ -212,7 +212,7 @@ std::shared_ptr<const qoc::HamiltonianModel> make_model(const qoc_problem_v1* p,
 }  // namespace
 
 // IterationStat::events of the last ref_ism_run, newline-joined: [b][k]
-static std::vector<std::vector<std::string>> g_events;
+static thread_local std::vector<std::vector<std::string>> g_events;
 
 extern "C" int32_t ref_iteration_events(int32_t b, int32_t k, char* out, size_t len) {
   if (b < 0 || b >= static_cast<int>(g_events.size()) || k < 0 ||
@@ -295,7 +295,7 @@ extern "C" int32_t ref_ism_run(const qoc_problem_v1* p, const qoc_ism_config_v1*
         o.error = it.error.value_or(0.0);
         o.has_exact_objective = it.exact_objective.has_value();
         o.exact_objective = it.exact_objective.value_or(0.0);
-        o.device_seconds = it.critical_path_seconds;
+        o.device_seconds = it.wall_seconds;  // measured wall time of the iteration (runtime.hpp:61)
         double* tv = task_values + ((size_t)b * rec_cap + k) * L;
         for (int m = 0; m < L; ++m) tv[m] = m < static_cast<int>(it.task_values.size()) ? it.task_values[m] : NAN;
       }
