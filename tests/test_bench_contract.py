@@ -1,5 +1,5 @@
-"""bench.py contract on CPU: the reference arm runs the oracle port (no GPU) and prints one
-JSON line with the driver's keys."""
+"""bench.py contract on CPU: the reference arm runs the reference's own compiled run_ism
+(oracle/_ref, where it was built) or the oracle port, and prints one JSON line with the driver's keys."""
 import json
 import subprocess
 import sys
@@ -20,8 +20,19 @@ def test_reference_arm_json_line():
                 "higher_is_better", "cpu_baseline", "e2e", "config"):
         assert key in j, key
     assert j["impl"] == "reference" and j["value"] > 0 and j["unit"] == "steps/s"
-    assert j["cpu_baseline"]["kind"] == "port" and j["cpu_baseline"]["cores"] >= 1
+    ref_built = (ROOT / "oracle" / "_ref" / "libqocref.so").exists()
+    assert j["cpu_baseline"]["kind"] == ("reference" if ref_built else "port") and j["cpu_baseline"]["cores"] >= 1
     assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_reference_arm_port_fallback():
+    import os
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--workload", "spin2",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT,
+                         env={**os.environ, "QOC_BENCH_PORT": "1"})
+    assert out.returncode == 0, out.stderr[-2000:]
+    j = json.loads([ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")][0])
+    assert j["cpu_baseline"]["kind"] == "port" and j["value"] > 0
 
 
 def test_gpus_flag_spawns_ranks():
