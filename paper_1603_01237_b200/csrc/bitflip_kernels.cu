@@ -421,8 +421,8 @@ __global__ void __launch_bounds__(1 << LOG2T) bitflip_horizon_kernel(DevProblem 
 // assembly of propagation.cpp:236-249 on the bit-flip operator: d independent column sweeps
 // instead of one dense LU per step).  blockIdx.x = column, blockIdx.y = local block,
 // blockIdx.z = problem (B = 1 on this path).  Writes column-major into the rank's slab.
-template <int LOG2E, int LOG2T>
-__global__ void __launch_bounds__(1 << LOG2T) bitflip_block_kernel(DevProblem P, DevRun R, DevBlocks BK, int g0) {
+template <int LOG2E, int LOG2T, int MINB>
+__global__ void __launch_bounds__(1 << LOG2T, MINB) bitflip_block_kernel(DevProblem P, DevRun R, DevBlocks BK, int g0) {
   using F_ = Bf<LOG2E, LOG2T>;
   constexpr int E = 1 << LOG2E, T = 1 << LOG2T;
   const int col = blockIdx.x, g = g0 + blockIdx.y, b = blockIdx.z;
@@ -468,11 +468,11 @@ cudaError_t launch_horizon(const DevProblem& P, const DevRun& R, int which, int 
   return cudaGetLastError();
 }
 
-template <int LOG2E, int LOG2T>
+template <int LOG2E, int LOG2T, int MINB = 1>
 cudaError_t launch_blocks(const DevProblem& P, const DevRun& R, const DevBlocks& BK, int g0, int nloc,
                           cudaStream_t st) {
   const size_t smem = bf_smem(P.d);
-  auto kern = bitflip_block_kernel<LOG2E, LOG2T>;
+  auto kern = bitflip_block_kernel<LOG2E, LOG2T, MINB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<dim3(P.d, nloc, P.B), 1 << LOG2T, smem, st>>>(P, R, BK, g0);
@@ -528,7 +528,10 @@ cudaError_t bitflip_horizon(const DevProblem& P, const DevRun& R, int which, int
   return bitflip_horizon_range(P, R, which, k, SweepRange{nullptr, 0, 0}, st);
 }
 
-// QOC_BF_BLOCK_SHAPE = "8" selects 256 threads x 4 amplitudes for d = 1024 (default 128 x 8).
+// d = 1024: 128 threads x 8 amplitudes capped at 128 registers (4 CTAs per SM) measured fastest
+// per outer iteration of config 3 with 8 blocks: 119.4 ms, vs 123.2 (3 CTAs per SM), 127.0
+// (uncapped, 208 registers) and 162.5 / 172.0 for 256 threads x 4 amplitudes (gpurun ab_blocks).
+// QOC_BF_BLOCK_SHAPE = 1 | 3 | 8 | 9 selects the other shapes for A/B runs (tools/ab_blocks.sh).
 cudaError_t bitflip_block_products(const DevProblem& P, const DevRun& R, const DevBlocks& BK, int g0, int nloc,
                                    cudaStream_t st) {
   if (P.C > 4) return cudaErrorNotSupported;
@@ -542,7 +545,10 @@ cudaError_t bitflip_block_products(const DevProblem& P, const DevRun& R, const D
     case 10: {
       const char* e = std::getenv("QOC_BF_BLOCK_SHAPE");
       if (e && e[0] == '8') return launch_blocks<2, 8>(P, R, BK, g0, nloc, st);
-      return launch_blocks<3, 7>(P, R, BK, g0, nloc, st);
+      if (e && e[0] == '9') return launch_blocks<2, 8, 3>(P, R, BK, g0, nloc, st);
+      if (e && e[0] == '3') return launch_blocks<3, 7, 3>(P, R, BK, g0, nloc, st);
+      if (e && e[0] == '1') return launch_blocks<3, 7, 1>(P, R, BK, g0, nloc, st);
+      return launch_blocks<3, 7, 4>(P, R, BK, g0, nloc, st);
     }
     case 11: return launch_blocks<3, 8>(P, R, BK, g0, nloc, st);
     case 12: return launch_blocks<3, 9>(P, R, BK, g0, nloc, st);
