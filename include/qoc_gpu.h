@@ -257,6 +257,20 @@ int32_t qoc_objective_gradient(qoc_ctx* ctx, const qoc_problem_v1* problem, cons
 int32_t qoc_assemble_propagator(qoc_ctx* ctx, const qoc_problem_v1* problem, const double* u,
                                 double* prop_out);
 
+/* Stationary states of a QOC_KIND_STRANG model by normalized imaginary-time splitting -- the first
+ * stage of ground_state (models.cpp:129-182) -- for `states` frozen controls at once (one CTA
+ * each).  psi_io [states][d] complex holds the starting guesses and returns the states
+ * (normalised to dx sum |psi|^2 = 1); with n_lower > 0 every iteration first projects out
+ * lower [states][n_lower][d] (Gram-Schmidt in the dx-weighted inner product; excited states).
+ * Stops when the discrete energy moves by less than energy_tol between iterations or after
+ * max_iterations; energy_out [states], iterations_out [states].  The problem's grid, kinetic
+ * spectrum, potential payload, kappa and ip_weight (= dx) are used; steps / states / penalty are
+ * ignored.  The residual polish of models.cpp:184-262 (gradient flow, dense self-consistent
+ * diagonalisation) stays with the caller. */
+int32_t qoc_imaginary_time(qoc_ctx* ctx, const qoc_problem_v1* problem, int32_t states, const double* u_frozen,
+                           double imaginary_dt, double energy_tol, int32_t max_iterations, int32_t n_lower,
+                           const double* lower, double* psi_io, double* energy_out, int32_t* iterations_out);
+
 /* Multi-GPU: one process and one context per GPU.  Rank 0 draws the NCCL unique
  * id (QOC_COMM_ID_BYTES bytes), the host side broadcasts it, and every rank binds its context
  * with qoc_ctx_init_comm.  A bit-flip run with plan ASSEMBLED then shards its subinterval blocks

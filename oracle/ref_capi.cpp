@@ -222,6 +222,29 @@ extern "C" int32_t ref_iteration_events(int32_t b, int32_t k, char* out, size_t 
   return QOC_OK;
 }
 
+// The reference's own ground_state (models.cpp:129-294) on a TrappedCondensateModel.
+extern "C" int32_t ref_ground_state(int32_t points, double x_min, double x_max, double distance, double kappa,
+                                    double u_frozen, double imaginary_dt, double energy_tol, int32_t max_iterations,
+                                    double* psi_out, double* scalars_out /* energy, mu, residual, iterations */) {
+  try {
+    const qoc::TrappedCondensateModel m(points, x_min, x_max, distance, kappa);
+    RVec u(1);
+    u << u_frozen;
+    const qoc::StationaryState s = qoc::ground_state(m, u, imaginary_dt, energy_tol, max_iterations);
+    for (int i = 0; i < points; ++i) {
+      psi_out[2 * i] = s.psi[i].real();
+      psi_out[2 * i + 1] = s.psi[i].imag();
+    }
+    scalars_out[0] = s.energy;
+    scalars_out[1] = s.chemical_potential;
+    scalars_out[2] = s.residual;
+    scalars_out[3] = s.iterations;
+    return QOC_OK;
+  } catch (const std::exception&) {
+    return QOC_ERUNTIME;
+  }
+}
+
 extern "C" int32_t ref_ism_run(const qoc_problem_v1* p, const qoc_ism_config_v1* cfg, const qoc_solver_v1* sv,
                                const double* u0, double* u_out, qoc_iter_record_v1* recs, int32_t rec_cap,
                                double* task_values, qoc_run_status_v1* status, char* err, size_t errlen) {

@@ -48,6 +48,8 @@ def lib():
         L.qoc_ism_run.restype = i32
         L.qoc_ctx_solver_stats.argtypes = [vp, i32, i32, i32, vp]
         L.qoc_ctx_solver_stats.restype = i32
+        L.qoc_imaginary_time.argtypes = [vp, vp, i32, dp, C.c_double, C.c_double, i32, i32, dp, dp, dp, vp]
+        L.qoc_imaginary_time.restype = i32
         L.qoc_propagate_final.argtypes = [vp, vp, dp, dp]
         L.qoc_propagate_final.restype = i32
         L.qoc_objective_gradient.argtypes = [vp, vp, dp, i32, i32, dp, dp]

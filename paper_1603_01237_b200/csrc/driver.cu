@@ -1408,6 +1408,52 @@ int32_t qoc_objective_gradient(qoc_ctx* ctx, const qoc_problem_v1* p, const doub
   });
 }
 
+int32_t qoc_imaginary_time(qoc_ctx* ctx, const qoc_problem_v1* p, int32_t states, const double* u_frozen, double tau,
+                           double tol, int32_t max_iter, int32_t n_lower, const double* lower, double* psi_io,
+                           double* energy_out, int32_t* iterations_out) {
+  return guarded(ctx, [&] {
+    validate_problem(p);
+    if (p->kind != QOC_KIND_STRANG) fail(QOC_ELOGIC, "imaginary-time stationary states need the split-step kind");
+    if (states < 1 || !u_frozen || !psi_io || !energy_out || !iterations_out || n_lower < 0 || (n_lower && !lower))
+      fail(QOC_EINVAL, "null or empty argument");
+    if (!(tau > 0.0) || tol < 0.0 || max_iter < 0) fail(QOC_EINVAL, "imaginary_dt > 0, energy_tol >= 0, max_iterations >= 0");
+    cudaStream_t st = ctx->stream;
+    DeviceProblem dp;
+    dp.slots = fresh_slots(ctx->prob_slots);
+    qoc_problem_v1 q = *p;
+    q.batch = 1;
+    upload_problem(&q, std::vector<int>{0, q.steps}, st, dp);
+    DeviceRun dr;
+    dr.slots = fresh_slots(ctx->run_slots);
+    const int d = p->dim;
+    std::vector<double> hk(2 * (size_t)d);
+    for (int i = 0; i < d; ++i) {
+      hk[2 * i] = std::exp(-0.5 * tau * p->kinetic[i]);  // models.cpp:138-139
+      hk[2 * i + 1] = 0.0;
+    }
+    double* kin = dr.alloc<double>(d);
+    double2* half_kin = dr.alloc<double2>(d);
+    double* uf = dr.alloc<double>(states);
+    double2* psi = dr.alloc<double2>((size_t)states * d);
+    double2* low = dr.alloc<double2>((size_t)states * std::max(1, n_lower) * d);
+    double* en = dr.alloc<double>(states);
+    int* it = dr.alloc<int>(states);
+    ck(cudaMemcpyAsync(kin, p->kinetic, sizeof(double) * d, cudaMemcpyHostToDevice, st), "kinetic");
+    ck(cudaMemcpyAsync(half_kin, hk.data(), sizeof(double2) * d, cudaMemcpyHostToDevice, st), "half kinetic");
+    ck(cudaMemcpyAsync(uf, u_frozen, sizeof(double) * states, cudaMemcpyHostToDevice, st), "controls");
+    ck(cudaMemcpyAsync(psi, psi_io, sizeof(double2) * states * d, cudaMemcpyHostToDevice, st), "states");
+    if (n_lower)
+      ck(cudaMemcpyAsync(low, lower, sizeof(double2) * states * n_lower * d, cudaMemcpyHostToDevice, st), "lower states");
+    Launcher launch{ctx};
+    launch(strang_imaginary_time(dp.P, states, uf, tau, tol, max_iter, n_lower, low, kin, half_kin, psi, en, it, st),
+           "imaginary time");
+    ck(cudaMemcpyAsync(psi_io, psi, sizeof(double2) * states * d, cudaMemcpyDeviceToHost, st), "states");
+    ck(cudaMemcpyAsync(energy_out, en, sizeof(double) * states, cudaMemcpyDeviceToHost, st), "energy");
+    ck(cudaMemcpyAsync(iterations_out, it, sizeof(int) * states, cudaMemcpyDeviceToHost, st), "iterations");
+    ck(cudaStreamSynchronize(st), "imaginary time");
+  });
+}
+
 int32_t qoc_assemble_propagator(qoc_ctx* ctx, const qoc_problem_v1* p, const double* u, double* prop_out) {
   return guarded(ctx, [&] {
     validate_problem(p);

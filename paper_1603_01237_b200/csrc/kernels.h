@@ -45,6 +45,13 @@ cudaError_t exact_from_nodes(const DevProblem& P, const DevRun& R, int k, cudaSt
 cudaError_t strang_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
 cudaError_t strang_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st);
 
+// stationary states of the condensate by imaginary-time splitting (models.cpp:146-182), one CTA
+// per state; psi_io [states][d], lower [states][nlower][d]
+cudaError_t strang_imaginary_time(const DevProblem& P, int states, const double* u_frozen, double tau, double tol,
+                                  int max_iter, int nlower, const double2* lower, const double* kin,
+                                  const double2* half_kin, double2* psi_io, double* energy_out, int* iter_out,
+                                  cudaStream_t st);
+
 // propagator-cache engine for the linear kinds (d <= 32)
 int pc_nchunk(const DevProblem& P, const DevRun& R);
 cudaError_t pc_eval(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);

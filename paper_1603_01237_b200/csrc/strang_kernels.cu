@@ -501,6 +501,93 @@ __global__ void __launch_bounds__(ST_T) strang_horizon_kernel(DevProblem P, DevR
   }
 }
 
+
+// ---- stationary states by imaginary-time splitting (ground_state, models.cpp:146-182) ----------
+// One CTA per state (blockIdx.x): psi <- normalise(K_h exp(-tau (V + kappa |psi_a|^2)) K_h psi),
+// K_h = idft(exp(-tau/2 k) dft(.)), optionally Gram-Schmidt-orthogonalised against `nlower` fixed
+// states first (excited states; BASELINE config 4's target), until the discrete energy
+//   E = dx (sum k |hat|^2 + sum V |psi|^2 + kappa/2 sum |psi|^4)           (models.cpp:152-163)
+// moves by less than `tol` between iterations, or max_iter iterations.  The spectrum of the new
+// state from the energy evaluation is the first transform of the next iteration.
+__global__ void __launch_bounds__(ST_T, 1) imag_time_kernel(DevProblem P, const double* u_frozen, double tau, double tol,
+                                                            int max_iter, int nlower, const double2* lower,
+                                                            const double* kin, const double2* half_kin, double2* psi_io,
+                                                            double* energy_out, int* iter_out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const StrangCtx X = make_ctx(P, smem_raw);
+  const int d = X.d, s = blockIdx.x;
+  const double u = u_frozen[s], dx = P.ip_w, kappa = P.kappa;
+  double2* psi_g = psi_io + (size_t)s * d;
+  const double2* low = lower + (size_t)s * nlower * d;
+  load_vec(X.A, psi_g, d);
+  const PotStep ps = pot_step(X, P, u);
+  // V(x_i, u) is fixed: keep it in the Q vector's real parts
+  for (int i = threadIdx.x; i < d; i += ST_T) X.Q[i] = cx(potential_at(X, P, i, u, ps), 0.0);
+  __syncthreads();
+  auto normalise = [&]() {  // psi (in A) <- orth(psi) / (sqrt(dx) ||psi||)
+    for (int q = 0; q < nlower; ++q) {
+      double re = 0.0, im = 0.0;
+      for (int i = threadIdx.x; i < d; i += ST_T) {
+        const double2 t = cconjmul(low[(size_t)q * d + i], X.A[i]);
+        re += t.x;
+        im += t.y;
+      }
+      const double2 ov = cx(dx * block_sum(X, re), dx * block_sum(X, im));
+      for (int i = threadIdx.x; i < d; i += ST_T) X.A[i] = csub(X.A[i], cmul(ov, low[(size_t)q * d + i]));
+      __syncthreads();
+    }
+    double nn = 0.0;
+    for (int i = threadIdx.x; i < d; i += ST_T) nn += cabs2(X.A[i]);
+    const double inv = 1.0 / (sqrt(dx) * sqrt(block_sum(X, nn)));
+    for (int i = threadIdx.x; i < d; i += ST_T) X.A[i] = cscale(X.A[i], inv);
+    __syncthreads();
+  };
+  // energy of psi (in A); leaves the unnormalised spectrum of psi in B and psi untouched in A
+  auto energy = [&]() {
+    double pe = 0.0, ie = 0.0;
+    for (int i = threadIdx.x; i < d; i += ST_T) {
+      const double den = cabs2(X.A[i]);
+      pe += X.Q[i].x * den;
+      ie += den * den;
+      X.S[i] = X.A[i];
+    }
+    __syncthreads();
+    transform(X, X.S, X.B, -1, nullptr, 1.0);
+    double ke = 0.0;
+    for (int i = threadIdx.x; i < d; i += ST_T) ke += kin[i] * cabs2(X.B[i]);
+    ke = block_sum(X, ke) * X.inv_n;  // unitary dft: |hat|^2 / n
+    pe = block_sum(X, pe);
+    ie = block_sum(X, ie);
+    return dx * (ke + pe + 0.5 * kappa * ie);
+  };
+  normalise();
+  double e = energy();
+  int k = 0;
+  for (; k < max_iter; ++k) {
+    transform(X, X.B, X.S, +1, half_kin, X.inv_n);  // psi_a = K_h psi (B holds dft(psi))
+    for (int i = threadIdx.x; i < d; i += ST_T) {
+      const double2 pa = X.S[i];
+      X.S[i] = cscale(pa, exp(-tau * (X.Q[i].x + kappa * cabs2(pa))));
+    }
+    __syncthreads();
+    transform(X, X.S, X.B, -1, nullptr, 1.0);
+    transform(X, X.B, X.A, +1, half_kin, X.inv_n);
+    normalise();
+    const double next = energy();
+    const bool done = fabs(next - e) < tol;
+    e = next;
+    if (done) {
+      ++k;
+      break;
+    }
+  }
+  for (int i = threadIdx.x; i < d; i += ST_T) psi_g[i] = X.A[i];
+  if (threadIdx.x == 0) {
+    energy_out[s] = e;
+    iter_out[s] = k;
+  }
+}
+
 }  // namespace
 
 cudaError_t strang_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
@@ -533,6 +620,19 @@ cudaError_t strang_horizon(const DevProblem& P, const DevRun& R, int which, int 
   cudaError_t e = cudaFuncSetAttribute(strang_horizon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   strang_horizon_kernel<<<P.B, ST_T, smem, st>>>(P, R, which, k);
+  return cudaGetLastError();
+}
+
+cudaError_t strang_imaginary_time(const DevProblem& P, int states, const double* u_frozen, double tau, double tol,
+                                  int max_iter, int nlower, const double2* lower, const double* kin,
+                                  const double2* half_kin, double2* psi_io, double* energy_out, int* iter_out,
+                                  cudaStream_t st) {
+  if (P.d > ST_MAXD) return cudaErrorNotSupported;
+  const size_t smem = strang_smem(P.d);
+  cudaError_t e = cudaFuncSetAttribute(imag_time_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  imag_time_kernel<<<states, ST_T, smem, st>>>(P, u_frozen, tau, tol, max_iter, nlower, lower, kin, half_kin, psi_io,
+                                               energy_out, iter_out);
   return cudaGetLastError();
 }
 

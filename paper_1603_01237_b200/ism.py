@@ -434,6 +434,39 @@ def unpack_states(flat: np.ndarray, model, lead: tuple) -> np.ndarray:
     return z.reshape(lead + shp)
 
 
+def imaginary_time(model, u_frozen, psi0, imaginary_dt: float = 1e-2, energy_tol: float = 1e-10,
+                   max_iterations: int = 200000, lower=None, ctx=None):
+    """Stationary states of a condensate model by normalized imaginary-time splitting on the
+    device (the first stage of ground_state, models.cpp:129-182), one CTA per frozen control.
+
+    u_frozen: (S,) controls; psi0: (S, d) or (d,) starting guesses; lower: optional (S, Q, d) or
+    (Q, d) states projected out every iteration (excited states).  Returns (psi (S, d),
+    energy (S,), iterations (S,))."""
+    from . import _native
+    u = np.ascontiguousarray(np.atleast_1d(np.asarray(u_frozen, dtype=np.float64)))
+    S, d = u.size, model.state_dim()
+    psi = np.ascontiguousarray(np.broadcast_to(np.asarray(psi0, dtype=np.complex128), (S, d))).copy()
+    grid = TimeGrid.over(0.0, 1.0, 1)
+    prob = ControlProblem(model, grid, psi[0], psi[0], None)
+    packed = pack_problem(prob)
+    nl, low = 0, None
+    if lower is not None:
+        low = np.asarray(lower, dtype=np.complex128)
+        if low.ndim == 2:
+            low = np.broadcast_to(low, (S,) + low.shape)
+        low = np.ascontiguousarray(low)
+        nl = low.shape[1]
+    buf = abi.cplx(psi)
+    lowbuf = abi.cplx(low) if nl else None
+    en, its = np.empty(S), np.empty(S, dtype=np.int32)
+    ctx = ctx or _native.default_context()
+    raise_for(ctx.lib.qoc_imaginary_time(ctx.handle, packed.ref, S, abi.dptr(u), float(imaginary_dt),
+                                         float(energy_tol), int(max_iterations), nl,
+                                         abi.dptr(lowbuf) if nl else None, abi.dptr(buf), abi.dptr(en),
+                                         its.ctypes.data_as(C.c_void_p)), ctx.last_error())
+    return buf.view(np.complex128).reshape(S, d), en, its
+
+
 def propagate_final(p: ControlProblem, u, ctx=None) -> np.ndarray:
     """propagation.cpp:194-200, on the device: (B,) + state shape final states."""
     from . import _native

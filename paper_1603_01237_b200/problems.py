@@ -206,13 +206,14 @@ def _uidft(x):
 
 
 def stationary_state(model: CondensateModel, u: float, excited: int = 0, lower=None,
-                     imaginary_dt: float = 1e-2, energy_tol: float = 1e-10) -> np.ndarray:
+                     imaginary_dt: float = 1e-2, energy_tol: float = 1e-10, device: bool = False,
+                     ctx=None) -> np.ndarray:
     """Self-consistent stationary state number `excited` (0 = ground) at frozen control u.
 
-    Ground state: normalized imaginary-time splitting (models.cpp:146-200), then damped
-    self-consistent diagonalization at frozen density until the residual stops improving
-    (models.cpp:245-262); the gradient-flow polish of models.cpp:203-242 only improves the
-    starting density and is subsumed by the SCF stage.  Excited state (BASELINE config 4 has
+    Ground state: normalized imaginary-time splitting (models.cpp:146-182; on the device with
+    device=True, qoc_imaginary_time), the normalized gradient-flow polish (models.cpp:184-242),
+    then damped self-consistent diagonalization at frozen density until the residual stops
+    improving (models.cpp:245-262).  Excited state (BASELINE config 4 has
     no reference code; pinned here): the same SCF selecting eigenvector `excited`, started from
     imaginary time with Gram-Schmidt against `lower`.  Phase (models.cpp:265-272): the first
     component within 1e-8 of the largest magnitude is made real positive.
@@ -242,7 +243,12 @@ def stationary_state(model: CondensateModel, u: float, excited: int = 0, lower=N
 
     psi = orth(psi)
     e = energy(psi)
-    for _ in range(200000):
+    if device:  # the imaginary-time stage on the GPU (qoc_imaginary_time), the SCF polish below on the host
+        from . import ism as _ism
+        out, _, _ = _ism.imaginary_time(model, [u], psi, imaginary_dt, energy_tol, 200000,
+                                        lower=np.asarray(lower) if lower else None, ctx=ctx)
+        psi = out[0]
+    for _ in range(0 if device else 200000):
         pa = _uidft(half_kin * _udft(psi))
         pa = pa * np.exp(-imaginary_dt * (v + kappa * np.abs(pa) ** 2))
         psi = orth(_uidft(half_kin * _udft(pa)))
@@ -251,6 +257,26 @@ def stationary_state(model: CondensateModel, u: float, excited: int = 0, lower=N
         e = e2
         if done:
             break
+
+    # normalized gradient flow on the exact discrete energy (models.cpp:184-242): backtracked steps
+    # along -(H[psi] - mu) psi remove the O(dt^2) splitting bias of the imaginary-time fixed point
+    step, e_now = imaginary_dt, energy(psi)
+    for _ in range(20000):
+        hs = apply_h(psi)
+        r = hs - dx * np.real(np.vdot(psi, hs)) * psi
+        if np.sqrt(dx) * np.linalg.norm(r) < 1e-12:
+            break
+        accepted = False
+        for _back in range(60):
+            trial = orth(psi - step * r)
+            e_trial = energy(trial)
+            if e_trial <= e_now + 4e-16 * (1.0 + abs(e_now)):
+                psi, e_now, accepted = trial, e_trial, True
+                step *= 1.25
+                break
+            step *= 0.5
+        if not accepted:
+            break  # descent stalled at the rounding floor
 
     eye = np.eye(n)
     kd = np.stack([_uidft(kin * _udft(eye[:, c])) for c in range(n)], axis=1)

@@ -1,8 +1,9 @@
-"""Regenerates tests/golden/*.npz from the CPU oracle (oracle/oracle.cpp), itself pinned by
-tests/test_oracle_kats.py against the reference's known answers.  The reference C++ library
-cannot be built in this image (Eigen3 is absent), so these vectors are the oracle's
-outputs on the BASELINE-shaped inputs: they freeze the checker (CPU tests) and let the GPU
-tests run without re-running long oracle jobs.
+"""Regenerates tests/golden/*.npz from the CPU oracle (oracle/oracle.cpp), itself pinned to the
+reference's compiled run_ism (tests/test_reference_pinning.py) and its known answers
+(tests/test_oracle_kats.py).  The vectors freeze the checker (CPU tests) and let the GPU tests
+run without re-running long oracle jobs.  The condensate case starts from the stationary states
+of problems.stationary_state, which agree with the reference's ground_state to 1e-11
+(test_stationary_state_matches_reference_ground_state).
 
     python tests/golden/make_golden.py
 """

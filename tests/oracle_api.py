@@ -291,3 +291,19 @@ def basis_fixture(seed, points=32, steps=16, duration=0.4, kappa=1.5, alpha=0.05
     problem = I.ControlProblem(model, grid, ini.view(np.complex128).copy(), tgt.view(np.complex128).copy(),
                                np.full(steps, alpha))
     return problem, ctl.reshape(1, steps)
+
+
+def ref_ground_state(points, x_min, x_max, distance, kappa, u_frozen, imaginary_dt=1e-2, energy_tol=1e-10,
+                     max_iterations=200000):
+    """qoc::ground_state of the reference itself (models.cpp:129-294) on a TrappedCondensateModel:
+    (psi, energy, chemical_potential, residual, iterations)."""
+    global _ref
+    if _ref is None:
+        _ref = C.CDLL(str(REF_LIBPATH))
+        _ref.ref_ism_run.restype = C.c_int32
+    psi, sc = np.empty(2 * points), np.empty(4)
+    code = _ref.ref_ground_state(C.c_int32(points), C.c_double(x_min), C.c_double(x_max), C.c_double(distance),
+                                 C.c_double(kappa), C.c_double(u_frozen), C.c_double(imaginary_dt),
+                                 C.c_double(energy_tol), C.c_int32(max_iterations), abi.dptr(psi), abi.dptr(sc))
+    assert code == abi.QOC_OK
+    return psi.view(np.complex128).copy(), sc[0], sc[1], sc[2], int(sc[3])

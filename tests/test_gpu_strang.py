@@ -146,3 +146,63 @@ def test_basis_potential_rejections(ctx):
         BasisCondensateModel(16, -1.0, 1.0, [(1.0, "power", 1.5)], 0.0)
     with pytest.raises(ValueError):
         BasisCondensateModel(16, -1.0, 1.0, [(1.0, "power", 0)] * 9, 0.0)
+
+
+def _imag_time_numpy(model, u, psi, tau, iters, lower=()):
+    """models.cpp:163-181 restated with numpy for a fixed iteration count."""
+    v, kin, dx, kappa = model.potential([u]), model.kinetic, model.dx, model.kappa
+    hk = np.exp(-0.5 * tau * kin)
+
+    def orth(s):
+        for q in lower:
+            s = s - dx * np.vdot(q, s) * q
+        return s / (np.sqrt(dx) * np.linalg.norm(s))
+
+    def energy(s):
+        hat = np.fft.fft(s, norm="ortho")
+        den = np.abs(s) ** 2
+        return dx * (np.sum(kin * np.abs(hat) ** 2) + np.sum(v * den) + 0.5 * kappa * np.sum(den * den))
+
+    psi = orth(psi)
+    for _ in range(iters):
+        pa = np.fft.ifft(hk * np.fft.fft(psi))
+        pa = pa * np.exp(-tau * (v + kappa * np.abs(pa) ** 2))
+        psi = orth(np.fft.ifft(hk * np.fft.fft(pa)))
+    return psi, energy(psi)
+
+
+@pytest.mark.parametrize("points", [50, 256, 1024])
+def test_imaginary_time_on_the_device(ctx, points):
+    # ground_state's first stage (models.cpp:146-182) for several frozen controls in one launch,
+    # a fixed iteration count (energy_tol = 0) against the numpy restatement
+    from paper_1603_01237_b200 import abi
+    from paper_1603_01237_b200.models import CondensateModel
+    lattice = points != 50
+    m = (CondensateModel(points, -16.0, 16.0, abi.POT_LATTICE, [1.0, 5.0, 1.0], 10.0) if lattice
+         else CondensateModel(points, -10.0, 10.0, abi.POT_TRAP, [6.0], 1.0))
+    us = np.array([0.0, 0.4, 1.0])
+    psi0 = np.exp(-0.5 * m.x * m.x).astype(complex)
+    psi, en, its = I.imaginary_time(m, us, psi0, 1e-2, 0.0, 300, ctx=ctx)
+    assert np.all(its == 300)
+    for s, u in enumerate(us):
+        ref, e = _imag_time_numpy(m, float(u), psi0, 1e-2, 300)
+        assert np.max(np.abs(psi[s] - ref)) < 1e-11
+        assert abs(en[s] - e) < 1e-10 * max(1.0, abs(e))
+    # first excited state: the odd guess with the ground state projected out every iteration
+    g, _, _ = I.imaginary_time(m, [0.0], psi0, 1e-2, 1e-12, 20000, ctx=ctx)
+    ex, ee, _ = I.imaginary_time(m, [0.0], psi0 * m.x, 1e-2, 0.0, 200, lower=g, ctx=ctx)
+    ref, e = _imag_time_numpy(m, 0.0, psi0 * m.x, 1e-2, 200, lower=[g[0]])
+    assert np.max(np.abs(ex[0] - ref)) < 1e-10
+    assert abs(m.dx * np.vdot(g[0], ex[0])) < 1e-12
+
+
+def test_device_ground_state_matches_the_host_pipeline(ctx):
+    # imaginary time on the device + the host's self-consistent polish = the host-only pipeline
+    # (which tests/test_reference_pinning.py pins to the reference's ground_state)
+    from paper_1603_01237_b200 import abi
+    from paper_1603_01237_b200.models import CondensateModel
+    m = CondensateModel(50, -10.0, 10.0, abi.POT_TRAP, [6.0], 1.0)
+    for u in (0.0, 1.0):
+        a = problems.stationary_state(m, u)
+        b = problems.stationary_state(m, u, device=True, ctx=ctx)
+        assert np.max(np.abs(a - b)) < 1e-10

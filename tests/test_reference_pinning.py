@@ -283,3 +283,16 @@ def test_basis_form_of_the_lattice_equals_the_lattice_kind():
     a = O.ism_run(I.ControlProblem(lat, p.grid, p.initial, p.target, p.penalty), u, cfg, sv)[0]
     b = O.ism_run(I.ControlProblem(bas, p.grid, p.initial, p.target, p.penalty), u, cfg, sv)[0]
     compare(a, b, ctl_abs=1e-12, obj_abs=1e-12)
+
+
+def test_stationary_state_matches_reference_ground_state():
+    # problems.stationary_state (imaginary time + self-consistent diagonalisation) against the
+    # reference's own ground_state (models.cpp:129-294): same discrete stationary state
+    from paper_1603_01237_b200 import abi
+    from paper_1603_01237_b200.models import CondensateModel
+    for u in (0.0, 1.0):
+        m = CondensateModel(50, -10.0, 10.0, abi.POT_TRAP, [6.0], 1.0)
+        psi = problems.stationary_state(m, u)
+        ref, energy, mu, residual, _ = O.ref_ground_state(50, -10.0, 10.0, 6.0, 1.0, u)
+        assert residual < 1e-10
+        assert np.max(np.abs(psi - ref)) < 1e-9
