@@ -829,9 +829,9 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
     if (monotonic && cfg->max_outer > 0 && solver->inner_iterations > 0) {  // optimizers.cpp:110-122
       if (p->kind == QOC_KIND_DENSITY || p->kind == QOC_KIND_STRANG)
         fail(QOC_ELOGIC, "the monotonic sweep requires column states with the one-step rational scheme");
-      if (p->kind != QOC_KIND_DENSE)
-        fail(QOC_ELOGIC, "the monotonic sweep on the device takes the operators in DENSE form (it needs dH/dv as "
-                         "matrices); repack the model as QOC_KIND_DENSE");
+      if (p->kind == QOC_KIND_BITFLIP)
+        fail(QOC_ELOGIC, "the monotonic sweep on the device takes the operators as matrices; repack the spin "
+                         "register as QOC_KIND_DENSE (d <= 64)");
       if (p->channels != 1) fail(QOC_ELOGIC, "the monotonic sweep handles a single control channel");
       for (int j = 0; j < p->steps; ++j)
         if (!p->penalty || p->penalty[j] <= 0.0)
@@ -864,6 +864,39 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
     cudaStream_t st = ctx->stream;
     Launcher launch{ctx};
 
+    // The monotonic sweep needs dH/dv as matrices: a tridiagonal model (the reference's rotor is a
+    // DenseModel, models.cpp:349-380) is expanded to the dense payload for that solver.
+    qoc_problem_v1 dense_view;
+    std::vector<double> tri_h0, tri_lin, tri_quad;
+    if (monotonic && p->kind == QOC_KIND_TRIDIAG && cfg->max_outer > 0 && solver->inner_iterations > 0) {
+      const int d = p->dim;
+      const size_t dd = (size_t)d * d;
+      const int nq = p->tri_has_quadratic ? C : 0, nops = 1 + C + nq;
+      tri_h0.assign(2 * dd * B, 0.0);
+      tri_lin.assign(2 * dd * B * C, 0.0);
+      tri_quad.assign(2 * dd * B * std::max(nq, 1), 0.0);
+      for (int b = 0; b < B; ++b)
+        for (int o = 0; o < nops; ++o) {
+          double* dst = o == 0 ? tri_h0.data() + 2 * dd * b
+                               : (o <= C ? tri_lin.data() + 2 * dd * ((size_t)b * C + o - 1)
+                                         : tri_quad.data() + 2 * dd * ((size_t)b * C + o - 1 - C));
+          const double* dg = p->tri_diag + ((size_t)b * nops + o) * d;
+          const double* sb = p->tri_sub + 2 * ((size_t)b * nops + o) * (d - 1);
+          for (int j = 0; j < d; ++j) dst[2 * (j + (size_t)j * d)] = dg[j];
+          for (int j = 0; j + 1 < d; ++j) {  // column-major: entry (j+1, j) and its conjugate at (j, j+1)
+            dst[2 * ((j + 1) + (size_t)j * d)] = sb[2 * j];
+            dst[2 * ((j + 1) + (size_t)j * d) + 1] = sb[2 * j + 1];
+            dst[2 * (j + (size_t)(j + 1) * d)] = sb[2 * j];
+            dst[2 * (j + (size_t)(j + 1) * d) + 1] = -sb[2 * j + 1];
+          }
+        }
+      dense_view = *p;
+      dense_view.kind = QOC_KIND_DENSE;
+      dense_view.h0 = tri_h0.data();
+      dense_view.linear = tri_lin.data();
+      dense_view.quadratic = nq ? tri_quad.data() : nullptr;
+      p = &dense_view;
+    }
     DeviceProblem dp;
     dp.slots = fresh_slots(ctx->prob_slots);
     upload_problem(p, node, st, dp);

@@ -177,3 +177,28 @@ def test_newton_batch_matches_single_runs(ctx):
     refs = O.ism_run(w.problem, w.u0, w.config, sv, O.REFERENCE)
     for g, r in zip(runs, refs):
         check(g, r, 2e-5, 1e-7)
+
+
+def test_monotonic_on_a_tridiagonal_model(ctx):
+    # the reference's rotor is a DenseModel (models.cpp:349-380) and its preset uses the monotonic
+    # solver; the device expands the tridiagonal payload to dense matrices for this solver
+    from paper_1603_01237_b200.models import TridiagonalModel
+    d, K = 7, 48
+    j = np.arange(d, dtype=np.float64)
+    diag = np.stack([j * (j + 1.0), np.zeros(d)])
+    sub = np.stack([np.zeros(d - 1, complex), -problems.rotor_coupling(d - 1).astype(complex)])
+    model = TridiagonalModel(diag, sub, channels=1)
+    rng = np.random.default_rng(11)
+    psi_i = np.zeros(d, complex); psi_i[0] = 1.0
+    t = rng.standard_normal(3) + 1j * rng.standard_normal(3)
+    psi_t = np.zeros(d, complex); psi_t[:3] = t / np.linalg.norm(t)
+    grid = I.TimeGrid.over(0.0, 1.2, K)
+    p = I.ControlProblem(model, grid, psi_i, psi_t, np.full(K, 0.8))
+    u0 = rng.uniform(-0.5, 0.5, K).reshape(1, K)
+    cfg = I.IsmConfig(subintervals=4, max_outer=5, eta=0.0)
+    sv = I.SolverSpec(kind="monotonic")
+    g = I.run_ism(p, u0, cfg, sv, ctx)
+    r = O.ism_run(p, u0, cfg, sv, O.REFERENCE)[0]  # reference arithmetic: the dense model
+    assert np.max(np.abs(r.control - u0)) > 0.05
+    check(g, r, 1e-9, 1e-10)
+    assert events(g) == events(r)
