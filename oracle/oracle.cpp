@@ -1460,9 +1460,7 @@ static RunOut run_ism(const Prob& P, const double* u0, const qoc_ism_config_v1& 
   if (sv.kind < QOC_SOLVER_GRADIENT || sv.kind > QOC_SOLVER_NEWTON) throw InvalidArg("unknown solver kind");
   const int parts = cfg.subintervals;
   const std::vector<int> node = decomposition(P.K, parts, cfg.partition, cfg.node_index);
-  // the density kind refreshes its boundaries by direct node sweeps (as the device does;
-  // assembled and direct agree to rounding, ism_test.cpp:248-265)
-  const bool direct = cfg.plan == QOC_PLAN_DIRECT || m.kind == QOC_KIND_DENSITY;
+  const bool direct = cfg.plan == QOC_PLAN_DIRECT;
   const int stride = cfg.checkpoint_stride > 0 ? cfg.checkpoint_stride : sv.checkpoint_stride;
   const bool naive = sv.naive_nonlinear_adjoint != 0;
   const int C = P.C;
@@ -1505,18 +1503,23 @@ static RunOut run_ism(const Prob& P, const double* u0, const qoc_ism_config_v1& 
   auto compose = [&]() {  // ism.cpp:298-312
     psi.assign(static_cast<size_t>(parts) + 1, CV());
     chi.assign(static_cast<size_t>(parts) + 1, CV());
+    // apply_propagator (propagation.cpp:251-261): prop * state for column states,
+    // prop * state * prop^dag for the density kind's dm x dm matrix states
+    auto apply = [&](const CMat& prop, const CV& state) {
+      if (m.kind == QOC_KIND_DENSITY) {
+        const int dm = prop.rows;
+        CMat s(dm, dm);
+        s.v = state;
+        return matmul(matmul(prop, s), adjoint(prop)).v;
+      }
+      CMat s(m.d, 1);
+      s.v = state;
+      return matmul(prop, s).v;
+    };
     psi[0] = P.init;
-    for (int n = 0; n < parts; ++n) {
-      CMat s(m.d, 1);
-      s.v = psi[n];
-      psi[n + 1] = matmul(props[n], s).v;
-    }
+    for (int n = 0; n < parts; ++n) psi[n + 1] = apply(props[n], psi[n]);
     chi[static_cast<size_t>(parts)] = P.targ;
-    for (int n = parts - 1; n >= 0; --n) {
-      CMat s(m.d, 1);
-      s.v = chi[n + 1];
-      chi[n] = matmul(adjoint(props[n]), s).v;
-    }
+    for (int n = parts - 1; n >= 0; --n) chi[n] = apply(adjoint(props[n]), chi[n + 1]);
   };
   auto finite_controls = [&]() {
     for (double v : out.u)

@@ -704,6 +704,39 @@ __global__ void __launch_bounds__(BT) density_horizon_kernel(DevProblem P, DevRu
 }
 
 
+// Boundary chain of the density kind's assembled plan (compose_from_propagators with
+// apply_propagator = prop * state * prop^dag, ism.cpp:298-312, propagation.cpp:251-261): the
+// tasks' dm x dm products P_n (row-major in R.prop) carry the matrix states across the nodes,
+//   rho_{n+1} = P_n rho_n P_n^dag   (blockIdx.y = 0),     X_n = P_n^dag X_{n+1} P_n   (blockIdx.y = 1).
+__global__ void __launch_bounds__(BT) density_chain_kernel(DevProblem P, DevRun R) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int b = blockIdx.x;
+  if (R.done[b] || R.status[b]) return;
+  DensSmem D = carve_dens(smem_raw, P.dm);
+  const int dm = P.dm, sl = P.d, L = P.L;
+  const size_t nb = (size_t)b * (L + 1) * sl;
+  const double2* props = R.prop + (size_t)b * L * (size_t)dm * dm;
+  if (blockIdx.y == 0) {
+    dens_copy(sl, P.init + (size_t)b * sl, D.S);
+    dens_copy(sl, D.S, R.psi_nodes + nb);
+    for (int n = 0; n < L; ++n) {
+      dens_copy(dm * dm, props + (size_t)n * dm * dm, D.W);
+      mm(dm, D.W, ROW, D.S, COL, 1.0, nullptr, 0.0, D.G);    // G = P rho
+      mm(dm, D.G, COL, D.W, ROW_H, 1.0, nullptr, 0.0, D.S);  // rho' = G P^dag
+      dens_copy(sl, D.S, R.psi_nodes + nb + (size_t)(n + 1) * sl);
+    }
+  } else {
+    dens_copy(sl, P.targ + (size_t)b * sl, D.X);
+    dens_copy(sl, D.X, R.chi_nodes + nb + (size_t)L * sl);
+    for (int n = L - 1; n >= 0; --n) {
+      dens_copy(dm * dm, props + (size_t)n * dm * dm, D.W);
+      mm(dm, D.W, ROW_H, D.X, COL, 1.0, nullptr, 0.0, D.G);  // G = P^dag X
+      mm(dm, D.G, COL, D.W, ROW, 1.0, nullptr, 0.0, D.X);    // X' = G P
+      dens_copy(sl, D.X, R.chi_nodes + nb + (size_t)n * sl);
+    }
+  }
+}
+
 // ---- monotonic slice-rebuilding sweep (monotonic_step, optimizers.cpp:109-213) ----------------
 // A CTA per task.  The adjoint nodes chi_j along the previous control go to the task's
 // trajectory workspace; the forward sweep then rebuilds the control slice by slice: with
@@ -872,6 +905,14 @@ cudaError_t density_horizon(const DevProblem& P, const DevRun& R, int which, int
       cudaFuncSetAttribute(density_horizon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   density_horizon_kernel<<<P.B, BT, smem, st>>>(P, R, which, k);
+  return cudaGetLastError();
+}
+
+cudaError_t density_chain(const DevProblem& P, const DevRun& R, cudaStream_t st) {
+  const size_t smem = dens_smem(P.dm);
+  cudaError_t e = cudaFuncSetAttribute(density_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  density_chain_kernel<<<dim3(P.B, 2), BT, smem, st>>>(P, R);
   return cudaGetLastError();
 }
 

@@ -427,7 +427,9 @@ void alloc_run(const DeviceProblem& dp, int cap, const std::vector<int>& node, b
   R.task_targ = out.alloc<double2>(B * L * d);
   R.psi_nodes = out.alloc<double2>(B * (L + 1) * d);
   R.chi_nodes = out.alloc<double2>(B * (L + 1) * d);
-  R.prop = need_prop ? out.alloc<double2>(B * L * d * d) : nullptr;
+  // task propagators: d x d, or dm x dm for the density kind (its states are dm x dm matrices)
+  const size_t pe = P.kind == QOC_KIND_DENSITY ? (size_t)P.dm * P.dm : d * d;
+  R.prop = need_prop ? out.alloc<double2>(B * L * pe) : nullptr;
   R.psi_end = out.alloc<double2>(B * L * d);
   R.chi_start = out.alloc<double2>(B * L * d);
   // the split-step kind runs its residual and lagged sweeps as concurrent CTAs, each with its
@@ -858,8 +860,10 @@ int32_t qoc_ism_run(qoc_ctx* ctx, const qoc_problem_v1* p, const qoc_ism_config_
       if (G % ctx->world != 0) fail(QOC_EINVAL, "blocks must be a multiple of the communicator size");
       if (B != 1) fail(QOC_ELOGIC, "the blocked plan runs one problem per call (batch = 1)");
     }
+    // the density kind's assembled plan chains the tasks' dm x dm products as prop * rho * prop^dag
+    // (apply_propagator, propagation.cpp:251-261); QOC_DISABLE=denschain keeps the serial node sweeps
     const bool direct = !blocked && (cfg->plan == QOC_PLAN_DIRECT || p->kind == QOC_KIND_BITFLIP ||
-                                     p->kind == QOC_KIND_DENSITY);
+                                     (p->kind == QOC_KIND_DENSITY && disabled_path("denschain")));
     const bool assembled_interp = L > 1 && !split && !direct && !blocked;
     cudaStream_t st = ctx->stream;
     Launcher launch{ctx};

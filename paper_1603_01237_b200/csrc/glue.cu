@@ -365,6 +365,7 @@ cudaError_t merge_iteration(const DevProblem& P, const DevRun& R, int k, double*
   return cudaGetLastError();
 }
 cudaError_t chain_propagators(const DevProblem& P, const DevRun& R, cudaStream_t st) {
+  if (P.kind == 4 /* QOC_KIND_DENSITY */) return density_chain(P, R, st);
   const size_t slot = (sizeof(double2) * P.d * P.d + 127) & ~(size_t)127;
   auto go = [&](auto kern, int S) -> cudaError_t {
     const size_t smem = 128 + 16 * 32 + S * slot;

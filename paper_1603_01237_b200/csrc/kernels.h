@@ -19,6 +19,8 @@ cudaError_t dense_big_horizon(const DevProblem& P, const DevRun& R, int which, i
 bool density_supported(int dm);
 cudaError_t density_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
 cudaError_t density_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st);
+// boundary chain of the assembled plan: rho_{n+1} = P_n rho_n P_n^dag, X_n = P_n^dag X_{n+1} P_n
+cudaError_t density_chain(const DevProblem& P, const DevRun& R, cudaStream_t st);
 
 // tridiagonal (d <= 32)
 cudaError_t tridiag_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st);
