@@ -488,10 +488,43 @@ size_t dens_smem(int dm) {
          sizeof(int) * (dm + BT / 32 + 2);
 }
 
+// Gauss-Jordan inverse without row interchanges: two barriers per pivot instead of the pivot
+// search, swap and unscramble of invert().  Valid when B = I + i dt/2 H(u) is strictly column
+// diagonally dominant, where partial pivoting never swaps (the same test as dense.cuh).
+__device__ void invert_nopivot(int d, const BigSmem& S) {
+  double2* W = S.W;
+  for (int k = 0; k < d; ++k) {
+    const double2 pinv = crcp(W[k * d + k]);
+    for (int j = threadIdx.x; j < d; j += BT) {
+      S.prow[j] = (j == k) ? pinv : cmul(W[k * d + j], pinv);
+      S.colk[j] = W[j * d + k];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < d * d; e += BT) {
+      const int i = e / d, j = e % d;
+      if (i == k) {
+        W[e] = S.prow[j];
+      } else {
+        const double2 f = S.colk[i];
+        W[e] = (j == k) ? cneg(cmul(f, pinv)) : cfms(f, S.prow[j], W[e]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // W = B_j^-1 at control uj
 __device__ void dens_inverse(const DevProblem& P, int b, const double* uj, DensSmem& D) {
   build(P, b, uj, 0.5 * P.dt, D.W, P.dm);
-  invert(P.dm, D.lin);
+  // dt/2 ||H(u_j)||_1 < 1 (column sums bounded through the operators' 1-norms)
+  const double* nb = P.norm1 + (size_t)b * (1 + 2 * P.C);
+  double bound = nb[0];
+  for (int c = 0; c < P.C; ++c) {
+    bound += fabs(uj[c]) * nb[1 + c];
+    if (P.has_quad) bound += 0.5 * uj[c] * uj[c] * nb[1 + P.C + c];
+  }
+  if (0.5 * P.dt * bound < 1.0) invert_nopivot(P.dm, D.lin);
+  else invert(P.dm, D.lin);
 }
 // rho (column-major in/out) <- A rho A^dag ; uses G
 __device__ void dens_forward(int dm, DensSmem& D, double2* rho) {
@@ -507,26 +540,52 @@ __device__ void dens_copy(int n, const double2* src, double2* dst) {
   for (int i = threadIdx.x; i < n; i += BT) dst[i] = src[i];
   __syncthreads();
 }
-// Im tr(r1^dag dH_c r2) summed into trace_im[c]; r1 in T, r2 in G (column-major); uses S? no: scratch X2
-__device__ double dens_trace_im(const DevProblem& P, int b, int c, double uc, const double2* r1, const double2* r2,
-                                double* red) {
-  const int dm = P.dm;
+// All channels' Im tr(r1^dag dH_c r2) at once: tr(r1^dag dH_c r2) = tr(dH_c M) with
+// M = r2 r1^dag (one dm^3 product, column-major in Mx), so each channel is a dm^2 contraction
+// sum_{i,k} dH_c[i][k] M[k][i] instead of its own dm^3 product.  out[c] for c < C (all threads).
+constexpr int TRC = 8;  // channels per pass over M
+__device__ void dens_traces(const DevProblem& P, int b, const double* uj, const double2* Mx, double* red,
+                            double* out) {
+  const int dm = P.dm, C = P.C;
   const size_t dd = (size_t)dm * dm;
-  double im = 0.0;
-  for (int e = threadIdx.x; e < dm * dm; e += BT) {
-    const int i = e % dm, j = e / dm;  // (dH r2)(i, j)
-    double2 acc = cx(0.0, 0.0);
-    for (int k = 0; k < dm; ++k) {
-      double2 a = P.lin[((size_t)b * P.C + c) * dd + (size_t)i * dm + k];
-      if (P.has_quad) {
-        const double2 q = P.quad[((size_t)b * P.C + c) * dd + (size_t)i * dm + k];
-        a = cx(fma(uc, q.x, a.x), fma(uc, q.y, a.y));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c0 = 0; c0 < C; c0 += TRC) {
+    double im[TRC];
+#pragma unroll
+    for (int q = 0; q < TRC; ++q) im[q] = 0.0;
+    for (int e = threadIdx.x; e < dm * dm; e += BT) {
+      const int i = e / dm, k = e % dm;       // dH_c[i][k] (row-major) with M[k][i]
+      const double2 m = Mx[k + i * dm];
+#pragma unroll
+      for (int q = 0; q < TRC; ++q) {
+        const int c = c0 + q;
+        if (c < C) {
+          double2 a = P.lin[((size_t)b * C + c) * dd + e];
+          if (P.has_quad) {
+            const double2 qd = P.quad[((size_t)b * C + c) * dd + e];
+            a = cx(fma(uj[c], qd.x, a.x), fma(uj[c], qd.y, a.y));
+          }
+          im[q] += a.x * m.y + a.y * m.x;  // Im(a m)
+        }
       }
-      acc = cfma(a, r2[k + j * dm], acc);
     }
-    im += cconjmul(r1[e], acc).y;  // tr(r1^dag Y) = sum conj(r1_ij) Y_ij
+#pragma unroll
+    for (int q = 0; q < TRC; ++q)
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) im[q] += __shfl_xor_sync(0xffffffffu, im[q], off);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < TRC; ++q) red[warp * TRC + q] = im[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < TRC; ++q) {
+      double sacc = 0.0;
+      for (int w2 = 0; w2 < BT / 32; ++w2) sacc += red[w2 * TRC + q];
+      if (c0 + q < C) out[c0 + q] = sacc;
+    }
+    __syncthreads();
   }
-  return block_sum(im, red);
 }
 
 __global__ void __launch_bounds__(BT) density_task_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done) {
@@ -579,16 +638,17 @@ __global__ void __launch_bounds__(BT) density_task_kernel(DevProblem P, DevRun R
           mm(dm, D.W, ROW_H, D.X, COL, 1.0, nullptr, 0.0, D.T);                          // r1 = W^dag X
           mm(dm, D.W, ROW_H, traj + (size_t)(j + 1) * sl, COL, 1.0, nullptr, 0.0, D.S);  // r2 = W^dag rho_{j+1}
           const double aj = P.alpha[node0 + j] * scale;
-          for (int c = 0; c < C; ++c) {
-            const double uc = uj[c];
-            const double im = dens_trace_im(P, b, c, uc, D.T, D.S, red);
-            const double gc = -aj * dt * uc + 2.0 * dt * im;
-            if (threadIdx.x == 0) {
+          mm(dm, D.S, COL, D.T, COL_H, 1.0, nullptr, 0.0, D.G);  // M = r2 r1^dag
+          double tr[QOC_MAX_DENSITY_CHANNELS];
+          dens_traces(P, b, uj, D.G, red, tr);
+          if (threadIdx.x == 0)
+            for (int c = 0; c < C; ++c) {
+              const double uc = uj[c];
+              const double gc = -aj * dt * uc + 2.0 * dt * tr[c];
               if (mode & M_GRAD) R.grad[((size_t)b * P.K + node0 + j) * C + c] = gc;
               if (mode & M_UPDATE) u[(size_t)j * C + c] = uc + A.rho * (weight * gc);
             }
-            __syncthreads();
-          }
+          __syncthreads();
           for (int i = threadIdx.x; i < sl; i += BT)  // b = 2 r1 - X
             D.G[i] = cx(2.0 * D.T[i].x - D.X[i].x, 2.0 * D.T[i].y - D.X[i].y);
           __syncthreads();
@@ -630,9 +690,11 @@ __global__ void __launch_bounds__(BT) density_task_kernel(DevProblem P, DevRun R
         mm(dm, D.W, ROW_H, traj + (size_t)(j + 1) * sl, COL, 1.0, nullptr, 0.0, D.S);
         const double aj = P.alpha[node0 + j] * scale;
         double sq = 0.0;
+        mm(dm, D.S, COL, D.T, COL_H, 1.0, nullptr, 0.0, D.G);  // M = r2 r1^dag
+        double tr[QOC_MAX_DENSITY_CHANNELS];
+        dens_traces(P, b, uj, D.G, red, tr);
         for (int c = 0; c < C; ++c) {
-          const double uc = uj[c];
-          const double gc = -aj * dt * uc + 2.0 * dt * dens_trace_im(P, b, c, uc, D.T, D.S, red);
+          const double gc = -aj * dt * uj[c] + 2.0 * dt * tr[c];
           sq += gc * gc;
         }
         err += sqrt(sq);
