@@ -73,6 +73,16 @@ def flops_per_iteration(name: str, w) -> float:
         per = 7 * cay + 2 * C * n * 16 * d
         if w.config.plan == "assembled":
             per += d * cay  # blocked plan: the block products carry d columns per grid step
+    elif name == "spins":
+        # density-matrix conjugation kind (dm x dm states, d = dm^2): per grid step and sweep one
+        # dm x dm inverse (8/3 dm^3 + build) and complex dm^3 products (8 dm^3 flop each):
+        # forward rho' = A rho A^dag 2 products, adjoint + gradient 5 products (r1, r2, M = r2 r1^dag,
+        # X' and its half) + C dm^2 contractions, assembly 1 product.  Entry, gradient (fwd + bwd),
+        # residual (fwd + bwd), assembly = 3 forward + 2 backward + 1 assembly sweeps.
+        dm = int(round(np.sqrt(d)))
+        inv = (8 / 3) * dm ** 3 + (4 * C + 4) * dm ** 2
+        fwd, bwd, asm = inv + 2 * 8 * dm ** 3, inv + 5 * 8 * dm ** 3 + C * 8 * dm ** 2, inv + 8 * dm ** 3
+        per = 3 * fwd + 2 * bwd + asm
     elif name == "gpe1024":
         # split variant: entry, gradient (fwd + bwd), residual (fwd + bwd), lagged refresh
         # (fwd + bwd) = 4 forward + 3 backward stages per grid step; FFT = 5 n log2 n
@@ -170,6 +180,12 @@ def build_workload(name: str, iterations: int, rank: int, world: int, rho_fast: 
         w = problems.ising10(iterations=iterations)
         if ising_blocked(world):
             w.config.plan, w.config.blocks = "assembled", BLOCKS or 0
+    elif name == "spins":
+        # the reference's `spins` preset at full size (5 spins, 32 x 32 density matrices, 10 x/y
+        # controls, 2^15 steps, rho = 1e4; config.cpp:132-146) -- the paper's 5-spin case -- on 256
+        # subintervals; rho of the preset kept (rho_fast would be 0.1/dt = 234)
+        w = problems.spins_preset(quick=False, subintervals=256, iterations=iterations)
+        w.rho_fast = w.solver.step_size
     elif name == "gpe1024":
         w = problems.gpe1024(iterations=iterations)
         # the exact-payoff instrumentation (a serial K-step sweep per iteration) is outside the
@@ -282,6 +298,13 @@ def cpu_reference(name: str, warmup: int, steps: int, world: int = 1):
         sample_b = CPU_SAMPLE_PROBLEMS[name]
         w = problems.batch4096(batch=sample_b, iterations=warmup + steps)
         desc = f"{sample_b} of the 4096 problems (d=16, K=2000, L=128); steps/s of the sample"
+    elif name == "spins":
+        # 1/16 of the horizon: 2048 of the 2^15 grid steps on 16 subintervals (the same 128 steps
+        # per task); the work per grid step does not depend on the step's position or size
+        w = problems.spins_preset(quick=False, subintervals=16, steps=2048, iterations=warmup + steps)
+        w.rho_fast = w.solver.step_size
+        steps, warmup = min(steps, 2), 0
+        desc = "2048 of the 32768 grid steps of the 5-spin preset on 16 subintervals (128 steps per task)"
     else:
         w = build_workload(name, warmup + steps, 0, 1)
         desc = f"full {name} workload"
@@ -320,7 +343,8 @@ def cpu_reference(name: str, warmup: int, steps: int, world: int = 1):
         return {"value": work / secs, "unit": "steps/s", "cores": threads, "kind": "reference",
                 "sample": f"{desc}; the reference's own run_ism compiled from /root/reference (Eigen-subset shim), "
                           f"L = {w.config.subintervals}, {steps} timed outer iterations after {warmup} warm-up, {how}",
-                "seconds": secs, "wall": wall, "seconds_per_iteration": secs / steps, "sample_problems": p.batch}
+                "seconds": secs, "wall": wall, "seconds_per_iteration": secs / steps, "sample_problems": p.batch,
+                "horizon_scale": (32768.0 / p.grid.steps) if name == "spins" else 1.0}
     t0 = time.perf_counter()
     runs = O.ism_run(w.problem, w.u0, w.config, w.solver, arith, threads=threads)
     wall = time.perf_counter() - t0
@@ -347,7 +371,8 @@ def run_reference_arm(args, world, rank, dist):
     line = {"metric": METRIC, "value": ref["value"], "unit": "steps/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             # one outer iteration of the whole workload at the sample's rate
-            "ms_per_step": 1e3 * ref["seconds_per_iteration"] * full_batch(args.workload) / ref["sample_problems"],
+            "ms_per_step": 1e3 * ref["seconds_per_iteration"] * full_batch(args.workload) / ref["sample_problems"]
+                           * ref.get("horizon_scale", 1.0),
             "higher_is_better": True,
             "scaling": "strong" if args.workload == "batch4096" else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded, SURVEY §8(d))",
@@ -402,7 +427,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="batch4096",
-                    choices=["batch4096", "rotor21", "spin2", "ising10", "gpe1024"])
+                    choices=["batch4096", "rotor21", "spin2", "ising10", "gpe1024", "spins"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ttf", action="store_true", help="skip the time-to-fidelity run")
     ap.add_argument("--blocks", type=int, default=None,
