@@ -12,6 +12,9 @@
 // (propagation.cpp:236-249).  The task body is the same as dense_task_kernel's (ism.cpp:401-479):
 // entry value, gradient sweep with the fused update (objective.cpp:48-60, optimizers.cpp:102-107),
 // residual sweep (error_norm), assembly and the split-variant lagged refresh.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "qoc_gpu.h"
@@ -439,9 +442,60 @@ __device__ __forceinline__ double2 at(const double2* M, int dm, int i, int j, MO
     default: return cconj(M[j + i * dm]);
   }
 }
+// fp64 tensor-core form of mm for dm = 32 (the 5-spin density matrices): the complex product as
+// four real m8n8k4 products per 8 x 8 output tile and k-chunk.  Warp w of the CTA's eight owns the
+// 8 x 16 strip of tile row w / 2, tile columns 2 (w % 2) and 2 (w % 2) + 1, so one A fragment
+// feeds two tiles.  Fragments (PTX m8n8k4 f64): lane l holds A[l / 4][l % 4], B[l % 4][l / 4]
+// and C[l / 4][2 (l % 4) + {0, 1}]; operands are read straight from their row- / column-major,
+// plain / conjugate-transposed buffers through at().  1 = on (QOC_DISABLE=densmma switches off).
+__constant__ int c_dens_dmma = 1;
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ void mm_dmma32(const double2* A, MOp oa, const double2* Bm, MOp ob, double alpha, const double2* Cin,
+                          double beta, double2* out) {
+  constexpr int dm = 32;
+  const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int q = l >> 2, r = l & 3;
+  const int i = 8 * (warp >> 1) + q;  // A row of this lane's fragment element
+  const int tc0 = 2 * (warp & 1);
+  double cr[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, ci[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int kc = 0; kc < dm / 4; ++kc) {
+    const int k = 4 * kc + r;
+    const double2 a = at(A, dm, i, k, oa);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const double2 b = at(Bm, dm, k, 8 * (tc0 + t) + q, ob);
+      dmma884(cr[t][0], cr[t][1], a.x, b.x);
+      dmma884(cr[t][0], cr[t][1], -a.y, b.y);
+      dmma884(ci[t][0], ci[t][1], a.x, b.y);
+      dmma884(ci[t][0], ci[t][1], a.y, b.x);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = 8 * (tc0 + t) + 2 * r + h, e = i + j * dm;
+      double2 v = cx(alpha * cr[t][h], alpha * ci[t][h]);
+      if (beta != 0.0) v = cx(fma(beta, Cin[e].x, v.x), fma(beta, Cin[e].y, v.y));
+      out[e] = v;
+    }
+  __syncthreads();
+}
+
 // out (column-major) = alpha * op(A) op(B) + beta * Cin (column-major, may alias out only if beta == 0)
 __device__ void mm(int dm, const double2* A, MOp oa, const double2* Bm, MOp ob, double alpha, const double2* Cin,
                    double beta, double2* out) {
+  if (dm == 32 && c_dens_dmma) {
+    mm_dmma32(A, oa, Bm, ob, alpha, Cin, beta, out);
+    return;
+  }
   for (int e = threadIdx.x; e < dm * dm; e += BT) {
     const int i = e % dm, j = e / dm;
     double2 acc = cx(0.0, 0.0);
@@ -659,7 +713,10 @@ __global__ void __launch_bounds__(BT) density_task_kernel(DevProblem P, DevRun R
   }
 
   const bool do_err = (mode & M_ERROR) != 0, do_asm = (mode & M_ASSEMBLE) != 0, do_lag = (mode & M_LAGGED) != 0;
-  if (do_asm) {  // product of the one-step A's (row-major dm x dm; assemble_propagator, 236-249)
+  // product of the one-step A's (row-major dm x dm; assemble_propagator, 236-249): rides on the
+  // residual's forward sweep when both run (same controls, same inverses), else its own sweep
+  const bool fuse_asm = do_asm && do_err;
+  if (do_asm && !fuse_asm) {
     for (int e = threadIdx.x; e < dm * dm; e += BT) D.S[e] = cx((e / dm) == (e % dm) ? 1.0 : 0.0, 0.0);
     __syncthreads();
     for (int j = 0; j < len; ++j) {
@@ -675,10 +732,22 @@ __global__ void __launch_bounds__(BT) density_task_kernel(DevProblem P, DevRun R
     if (do_err) {
       dens_copy(sl, init, D.S);
       dens_copy(sl, D.S, traj);
+      if (fuse_asm) {  // the product lives in X (free until the adjoint seed), T is its scratch
+        for (int e = threadIdx.x; e < dm * dm; e += BT) D.X[e] = cx((e / dm) == (e % dm) ? 1.0 : 0.0, 0.0);
+        __syncthreads();
+      }
       for (int j = 0; j < len; ++j) {
         dens_inverse(P, b, u + (size_t)j * C, D);
         dens_forward(dm, D, D.S);
         dens_copy(sl, D.S, traj + (size_t)(j + 1) * sl);
+        if (fuse_asm) {
+          mm(dm, D.X, COL, D.W, COL, 2.0, D.X, -1.0, D.T);  // (2 W Pm - Pm)^T as column-major
+          dens_copy(dm * dm, D.T, D.X);
+        }
+      }
+      if (fuse_asm) {
+        for (int e = threadIdx.x; e < dm * dm; e += BT) R.prop[((size_t)b * P.L + n) * (size_t)dm * dm + e] = D.X[e];
+        __syncthreads();
       }
       for (int i = threadIdx.x; i < sl; i += BT) D.X[i] = A.form == 0 ? targ[i] : csub(targ[i], D.S[i]);
       __syncthreads();
@@ -953,7 +1022,18 @@ namespace qoc {
 
 bool density_supported(int dm) { return dm >= 1 && dm <= DENS_MAX; }
 
+// QOC_DISABLE=densmma keeps the CUDA-core products (A/B of the tensor-core path)
+static cudaError_t dens_mma_switch() {
+  static int done = 0;
+  if (done) return cudaSuccess;
+  done = 1;
+  const char* e = std::getenv("QOC_DISABLE");
+  const int on = !(e && std::strstr(e, "densmma"));
+  return cudaMemcpyToSymbol(c_dens_dmma, &on, sizeof(int));
+}
+
 cudaError_t density_task(const DevProblem& P, const DevRun& R, const TaskArgs& A, int ignore_done, cudaStream_t st) {
+  if (cudaError_t e0 = dens_mma_switch(); e0 != cudaSuccess) return e0;
   const size_t smem = dens_smem(P.dm);
   cudaError_t e = cudaFuncSetAttribute(density_task_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -962,6 +1042,7 @@ cudaError_t density_task(const DevProblem& P, const DevRun& R, const TaskArgs& A
 }
 
 cudaError_t density_horizon(const DevProblem& P, const DevRun& R, int which, int k, cudaStream_t st) {
+  if (cudaError_t e0 = dens_mma_switch(); e0 != cudaSuccess) return e0;
   const size_t smem = dens_smem(P.dm);
   cudaError_t e =
       cudaFuncSetAttribute(density_horizon_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -971,6 +1052,7 @@ cudaError_t density_horizon(const DevProblem& P, const DevRun& R, int which, int
 }
 
 cudaError_t density_chain(const DevProblem& P, const DevRun& R, cudaStream_t st) {
+  if (cudaError_t e0 = dens_mma_switch(); e0 != cudaSuccess) return e0;
   const size_t smem = dens_smem(P.dm);
   cudaError_t e = cudaFuncSetAttribute(density_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
