@@ -157,6 +157,8 @@ struct DevRun {
   double2* chi_start;   // [B][L][d]
   double2* traj;        // workspace [B*L][traj_len][d]
   int traj_len;         // >= max len + 1
+  double2* winv;        // density kind: per-task one-step inverses W_j [B*L][traj_len - 1][dm*dm] kept by
+                        // a forward sweep for the adjoint sweep that follows it (or null: recompute)
   double* entry;        // [B][L]
   double* err;          // [B][L]
   double* pen;          // [B][L] sum_j alpha_j |u_j|^2 over the task window (updated control)

@@ -653,6 +653,8 @@ __global__ void __launch_bounds__(BT) density_task_kernel(DevProblem P, DevRun R
   const double dt = P.dt, w = P.ip_w;
   double* u = R.u + ((size_t)b * P.K + node0) * C;
   double2* traj = R.traj + ((size_t)b * P.L + n) * (size_t)R.traj_len * sl;
+  // the forward sweep's inverses W_j, re-read by the adjoint sweep over the same controls
+  double2* winv = R.winv ? R.winv + ((size_t)b * P.L + n) * (size_t)(R.traj_len - 1) * dm * dm : nullptr;
   const size_t tix = ((size_t)b * P.L + n) * sl;
   const double2* init = R.task_init + tix;
   const double2* targ = R.task_targ + tix;
@@ -668,6 +670,7 @@ __global__ void __launch_bounds__(BT) density_task_kernel(DevProblem P, DevRun R
       for (int j = 0; j < len; ++j) {
         const double* uj = u + (size_t)j * C;
         dens_inverse(P, b, uj, D);
+        if (need_traj && winv) dens_copy(dm * dm, D.W, winv + (size_t)j * dm * dm);
         dens_forward(dm, D, D.S);
         if (need_traj) dens_copy(sl, D.S, traj + (size_t)(j + 1) * sl);
         double sq = 0.0;
@@ -688,7 +691,8 @@ __global__ void __launch_bounds__(BT) density_task_kernel(DevProblem P, DevRun R
         __syncthreads();
         for (int j = len - 1; j >= 0; --j) {
           const double* uj = u + (size_t)j * C;
-          dens_inverse(P, b, uj, D);
+          if (winv) dens_copy(dm * dm, winv + (size_t)j * dm * dm, D.W);
+          else dens_inverse(P, b, uj, D);
           mm(dm, D.W, ROW_H, D.X, COL, 1.0, nullptr, 0.0, D.T);                          // r1 = W^dag X
           mm(dm, D.W, ROW_H, traj + (size_t)(j + 1) * sl, COL, 1.0, nullptr, 0.0, D.S);  // r2 = W^dag rho_{j+1}
           const double aj = P.alpha[node0 + j] * scale;
@@ -738,6 +742,7 @@ __global__ void __launch_bounds__(BT) density_task_kernel(DevProblem P, DevRun R
       }
       for (int j = 0; j < len; ++j) {
         dens_inverse(P, b, u + (size_t)j * C, D);
+        if (winv) dens_copy(dm * dm, D.W, winv + (size_t)j * dm * dm);
         dens_forward(dm, D, D.S);
         dens_copy(sl, D.S, traj + (size_t)(j + 1) * sl);
         if (fuse_asm) {
@@ -754,7 +759,8 @@ __global__ void __launch_bounds__(BT) density_task_kernel(DevProblem P, DevRun R
       double err = 0.0;
       for (int j = len - 1; j >= 0; --j) {
         const double* uj = u + (size_t)j * C;
-        dens_inverse(P, b, uj, D);
+        if (winv) dens_copy(dm * dm, winv + (size_t)j * dm * dm, D.W);
+        else dens_inverse(P, b, uj, D);
         mm(dm, D.W, ROW_H, D.X, COL, 1.0, nullptr, 0.0, D.T);
         mm(dm, D.W, ROW_H, traj + (size_t)(j + 1) * sl, COL, 1.0, nullptr, 0.0, D.S);
         const double aj = P.alpha[node0 + j] * scale;

@@ -435,6 +435,12 @@ void alloc_run(const DeviceProblem& dp, int cap, const std::vector<int>& node, b
   // the split-step kind runs its residual and lagged sweeps as concurrent CTAs, each with its
   // own trajectory: two workspaces
   R.traj = out.alloc<double2>(B * L * (size_t)R.traj_len * dp.stride * (P.kind == QOC_KIND_STRANG ? 2 : 1));
+  R.winv = nullptr;
+  if (P.kind == QOC_KIND_DENSITY && R.traj_len > 1) {
+    const size_t need = sizeof(double2) * B * L * (size_t)(R.traj_len - 1) * P.dm * P.dm;
+    size_t freeb = 0, total = 0;
+    if (cudaMemGetInfo(&freeb, &total) == cudaSuccess && need < freeb / 2) R.winv = out.alloc<double2>(need / sizeof(double2));
+  }
   R.entry = out.alloc<double>(B * L);
   R.err = out.alloc<double>(B * L);
   R.pen = out.alloc<double>(B * L);
