@@ -74,12 +74,12 @@ def flops_per_iteration(name: str, w) -> float:
         if w.config.plan == "assembled":
             per += d * cay  # blocked plan: the block products carry d columns per grid step
     elif name == "spins":
-        # density-matrix conjugation kind (dm x dm states, d = dm^2): per grid step and sweep one
+        # density-matrix conjugation kind (dm x dm matrix states): per grid step and sweep one
         # dm x dm inverse (8/3 dm^3 + build) and complex dm^3 products (8 dm^3 flop each):
         # forward rho' = A rho A^dag 2 products, adjoint + gradient 5 products (r1, r2, M = r2 r1^dag,
         # X' and its half) + C dm^2 contractions, assembly 1 product.  Entry, gradient (fwd + bwd),
         # residual (fwd + bwd), assembly = 3 forward + 2 backward + 1 assembly sweeps.
-        dm = int(round(np.sqrt(d)))
+        dm = d  # state_dim() is the matrix edge of the dm x dm states
         inv = (8 / 3) * dm ** 3 + (4 * C + 4) * dm ** 2
         fwd, bwd, asm = inv + 2 * 8 * dm ** 3, inv + 5 * 8 * dm ** 3 + C * 8 * dm ** 2, inv + 8 * dm ** 3
         per = 3 * fwd + 2 * bwd + asm
