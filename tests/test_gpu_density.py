@@ -60,3 +60,46 @@ def test_five_spin_chain(ctx):
     r = O.ism_run(w.problem, w.u0, w.config, w.solver, O.REFERENCE)[0]
     assert rel(g.control - w.u0, r.control - w.u0) < 1e-9
     assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-10
+
+
+@pytest.mark.parametrize("variant", ["interpolated", "split"])
+def test_assembled_and_direct_plans(ctx, variant):
+    # the assembled plan chains the tasks' dm x dm products as prop * rho * prop^dag
+    # (apply_propagator, propagation.cpp:251-261); the direct plan sweeps the nodes serially.
+    # Both match the oracle's plan of the same name and each other (ism_test.cpp:248-265).
+    w = problems.spins_preset(quick=True, subintervals=8, iterations=5)
+    w.config.variant = variant
+    runs = {}
+    for plan in ("assembled", "direct"):
+        w.config.plan = plan
+        g = I.run_ism(w.problem, w.u0, w.config, w.solver, ctx)
+        r = O.ism_run(w.problem, w.u0, w.config, w.solver, O.REFERENCE)[0]
+        assert rel(g.control - w.u0, r.control - w.u0) < 1e-9
+        assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-10
+        assert g.record.plan == plan
+        runs[plan] = g
+    assert rel(runs["assembled"].control - w.u0, runs["direct"].control - w.u0) < 1e-9
+    assert np.max(np.abs(runs["assembled"].record.objectives() - runs["direct"].record.objectives())) < 1e-11
+
+
+def test_five_spin_tensor_core_products_match_cuda_cores(ctx):
+    # QOC_DISABLE=densmma is read once per process, so the A/B runs in a subprocess: the fp64
+    # tensor-core (DMMA) products and the CUDA-core products give the same run to rounding
+    import json, os, subprocess, sys
+    code = ("import json,sys; sys.path.insert(0,'.');"
+            "from paper_1603_01237_b200 import ism as I, problems;"
+            "w=problems.spins_preset(quick=False, subintervals=8, iterations=4, steps=256);"
+            "g=I.run_ism(w.problem,w.u0,w.config,w.solver);"
+            "print(json.dumps({'u':g.control.tolist(),'obj':g.record.objectives().tolist()}))")
+    root = __import__("pathlib").Path(__file__).resolve().parents[1]
+    outs = []
+    for env in ({}, {"QOC_DISABLE": "densmma"}):
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root, timeout=600,
+                           env={**os.environ, **env})
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs.append(json.loads(p.stdout.strip().splitlines()[-1]))
+    a, b = (np.array(o["u"]) for o in outs)
+    assert not np.array_equal(a, b) or True  # different instruction streams; equality is not required
+    w = problems.spins_preset(quick=False, subintervals=8, iterations=4, steps=256)
+    assert rel(a - w.u0, b - w.u0) < 1e-9
+    assert np.nanmax(np.abs(np.array(outs[0]["obj"]) - np.array(outs[1]["obj"]))) < 1e-11
