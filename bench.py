@@ -58,21 +58,15 @@ def flops_per_iteration(name: str, w) -> float:
         w_asm = (56 / 3) * d ** 3 + (4 * C + 4) * d ** 2
         per = 2 * w_cay + 2 * w_bg + w_asm
     elif name == "ising10":
-        # bit-flip Cayley step = (1 + m) sweeps of V y (n complex FMAs per amplitude, 8n flop)
-        # plus ~12 flop/amplitude of diagonal work; m from the a-priori contraction bound at u0
-        # (bitflip_kernels.cu sweep_count).  Direct plan: entry, forward, adjoint, residual
-        # forward + adjoint in the tasks and the two node sweeps = 7 steps per grid step, and
-        # 2 gradient evaluations (C channels x n flips x 16 flop per amplitude).
+        cay = ising_cayley_flops(w)  # summed over the K grid steps
         n = p.model.nspins
-        u = np.asarray(w.u0).reshape(C, K)
-        ax = np.abs(u[0]) * 0.5 * n
-        ay = np.abs(u[1]) * 0.5 * n
-        q = 0.5 * p.grid.dt * np.max(np.sqrt(ax * ax + ay * ay))
-        m = int(np.ceil(53 * np.log(2) / -np.log(q)))
-        cay = (1 + m) * (8 * n + 12) * d
-        per = 7 * cay + 2 * C * n * 16 * d
+        # direct plan: entry, forward, adjoint, residual forward + adjoint in the tasks and the two
+        # node sweeps = 7 Cayley steps per grid step, and 2 gradient evaluations (C channels x n
+        # flips x 16 flop per amplitude)
+        total = 7 * cay + 2 * C * n * 16 * d * K
         if w.config.plan == "assembled":
-            per += d * cay  # blocked plan: the block products carry d columns per grid step
+            total += d * cay  # blocked plan: the block products carry d columns per grid step
+        return total * B
     elif name == "spins":
         # density-matrix conjugation kind (dm x dm matrix states): per grid step and sweep one
         # dm x dm inverse (8/3 dm^3 + build) and complex dm^3 products (8 dm^3 flop each):
@@ -93,6 +87,19 @@ def flops_per_iteration(name: str, w) -> float:
     else:
         return float("nan")
     return per * K * B
+
+
+def ising_cayley_flops(w) -> float:
+    """Flops of one bit-flip Cayley step summed over the grid steps: s_j Jacobi sweeps of
+    z <- (1 + sD)^-1 (x - s V z), each n complex FMAs per amplitude for V z (8n flop) plus 12 flop
+    of diagonal work, with s_j the kernel's a-priori count ceil(54 ln 2 / -ln q_j),
+    q_j = dt/2 sum_i |(ax_i, ay_i)| at u_j (bitflip_kernels.cu begin_step)."""
+    p = w.problem
+    d, C, K, n = p.model.state_dim(), p.model.channels(), p.grid.steps, p.model.nspins
+    u = np.asarray(w.u0).reshape(C, K)
+    q = 0.5 * p.grid.dt * 0.5 * n * np.sqrt(u[0] ** 2 + u[1] ** 2)
+    sweeps = np.where(q > 0, np.ceil(54 * np.log(2) / -np.log(np.maximum(q, 1e-300))), 0.0)
+    return float(np.sum(sweeps) * (8 * n + 12) * d)
 
 
 def dmma_peak():
@@ -404,15 +411,15 @@ def label_flops(name: str, label: str, w, world: int = 1) -> float:
         per = {"assembly": 41 * d * d + 23 * d, "gradient": 64 * d + 64 * d + 24 * d,
                "residual": 64 * d + 64 * d + 24 * d}.get(label)
     elif name == "ising10":
-        # bit-flip Cayley step (1 + m)(8n + 12) d with m from the contraction bound at u0
         n = p.model.nspins
-        u = np.asarray(w.u0).reshape(C, K)
-        q = 0.5 * p.grid.dt * np.max(np.sqrt((np.abs(u[0]) * 0.5 * n) ** 2 + (np.abs(u[1]) * 0.5 * n) ** 2))
-        cay = (1 + int(np.ceil(53 * np.log(2) / -np.log(q)))) * (8 * n + 12) * d
-        per = {"node sweeps": 2 * cay,  # forward + adjoint full-horizon sweeps
-               "task": 5 * cay + 2 * C * n * 16 * d,
+        cay = ising_cayley_flops(w)  # summed over the K grid steps
+        tot = {"node sweeps": 2 * cay,  # forward + adjoint full-horizon sweeps
+               "task": 5 * cay + 2 * C * n * 16 * d * K,
                # blocked plan: d basis columns through this rank's K / W steps
                "block products": d * cay / world}.get(label)
+        if tot is not None:
+            return tot * B
+        per = None
     else:
         per = None
     if per is None:

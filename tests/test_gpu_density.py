@@ -99,7 +99,6 @@ def test_five_spin_tensor_core_products_match_cuda_cores(ctx):
         assert p.returncode == 0, p.stderr[-2000:]
         outs.append(json.loads(p.stdout.strip().splitlines()[-1]))
     a, b = (np.array(o["u"]) for o in outs)
-    assert not np.array_equal(a, b) or True  # different instruction streams; equality is not required
     w = problems.spins_preset(quick=False, subintervals=8, iterations=4, steps=256)
     assert rel(a - w.u0, b - w.u0) < 1e-9
     assert np.nanmax(np.abs(np.array(outs[0]["obj"]) - np.array(outs[1]["obj"]))) < 1e-11

@@ -17,10 +17,13 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > "$
 if [[ " $sections " == *" bench "* ]]; then
   timeout 900 python bench.py > "$out/bench_default.json" 2> "$out/bench_default.err"; echo "default rc=$?"
   timeout 900 python bench.py --impl reference > "$out/bench_reference.json" 2> "$out/bench_reference.err"; echo "reference rc=$?"
-  for wl in spin2 rotor21 ising10 gpe1024; do
+  for wl in spin2 rotor21 ising10 gpe1024 spins; do
     timeout 900 python bench.py --workload $wl --steps 10 --warmup 3 > "$out/bench_$wl.json" 2> "$out/bench_$wl.err"
     echo "$wl rc=$?"
   done
+  # config 3 sharded into 8 subinterval blocks (the 8-GPU layout on one GPU)
+  timeout 900 python bench.py --workload ising10 --blocks 8 --steps 5 --warmup 3 --no-cpu-baseline \
+    > "$out/bench_ising10_b8.json" 2> "$out/bench_ising10_b8.err"; echo "ising10 b8 rc=$?"
 fi
 if [[ " $sections " == *" ncu "* ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file "$out/launches_default.csv" \
