@@ -66,7 +66,8 @@ def test_five_spin_chain(ctx):
 def test_assembled_and_direct_plans(ctx, variant):
     # the assembled plan chains the tasks' dm x dm products as prop * rho * prop^dag
     # (apply_propagator, propagation.cpp:251-261); the direct plan sweeps the nodes serially.
-    # Both match the oracle's plan of the same name and each other (ism_test.cpp:248-265).
+    # Both match the oracle's plan of the same name, and each other in the interpolated variant
+    # (ism_test.cpp:248-265).
     w = problems.spins_preset(quick=True, subintervals=8, iterations=5)
     w.config.variant = variant
     runs = {}
@@ -78,8 +79,9 @@ def test_assembled_and_direct_plans(ctx, variant):
         assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-10
         assert g.record.plan == plan
         runs[plan] = g
-    assert rel(runs["assembled"].control - w.u0, runs["direct"].control - w.u0) < 1e-9
-    assert np.max(np.abs(runs["assembled"].record.objectives() - runs["direct"].record.objectives())) < 1e-11
+    if variant == "interpolated":  # the split variant's assembled plan is the LAGGED refresh: a different iteration
+        assert rel(runs["assembled"].control - w.u0, runs["direct"].control - w.u0) < 1e-9
+        assert np.max(np.abs(runs["assembled"].record.objectives() - runs["direct"].record.objectives())) < 1e-11
 
 
 def test_five_spin_tensor_core_products_match_cuda_cores(ctx):
