@@ -128,6 +128,9 @@ struct DevProblem {
   // STRANG
   const double2* kin_fwd;  // [d] exp(-i dt/2 k)   (kinetic_half_phase, forward)
   const double2* kin_adj;  // [d] exp(+i dt/2 k)
+  const double2* kin_fwd2;  // [d] exp(-i dt k): two consecutive kinetic half steps merged (strang sweeps)
+  const double2* kin_adj2;  // [d] exp(+i dt k)
+  int merge_kinetic;        // 1: sweeps merge the half steps between grid steps (QOC_DISABLE=strangmerge: 0)
   const double2* twiddle;  // FFT twiddles / DFT matrix
   const double* grid_x;
   int potential;

@@ -224,6 +224,8 @@ void hermitian_check(const double* m, int d, const char* what) {  // models.cpp:
   if (!(defect2 <= 1e-20 * scale2)) fail(QOC_EINVAL, std::string(what) + " must be Hermitian");
 }
 
+bool disabled_path(const char* what);
+
 void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaStream_t st, DeviceProblem& out) {
   out.st = st;
   validate_problem(p);
@@ -325,6 +327,18 @@ void upload_problem(const qoc_problem_v1* p, const std::vector<int>& node, cudaS
       }
       P.kin_fwd = out.put<double2>(reinterpret_cast<const double2*>(kf.data()), (size_t)d);
       P.kin_adj = out.put<double2>(reinterpret_cast<const double2*>(ka.data()), (size_t)d);
+      // two consecutive half steps as one spectral multiply: the product of the two half phases
+      // (the same two roundings the separate multiplies apply)
+      std::vector<double> kf2(2 * (size_t)d), ka2(2 * (size_t)d);
+      for (int i = 0; i < d; ++i) {
+        kf2[2 * i] = kf[2 * i] * kf[2 * i] - kf[2 * i + 1] * kf[2 * i + 1];
+        kf2[2 * i + 1] = 2.0 * kf[2 * i] * kf[2 * i + 1];
+        ka2[2 * i] = ka[2 * i] * ka[2 * i] - ka[2 * i + 1] * ka[2 * i + 1];
+        ka2[2 * i + 1] = 2.0 * ka[2 * i] * ka[2 * i + 1];
+      }
+      P.kin_fwd2 = out.put<double2>(reinterpret_cast<const double2*>(kf2.data()), (size_t)d);
+      P.kin_adj2 = out.put<double2>(reinterpret_cast<const double2*>(ka2.data()), (size_t)d);
+      P.merge_kinetic = disabled_path("strangmerge") ? 0 : 1;
       // twiddles of linalg.cpp:26-27 (polar(1, ang * k), ang = -2 pi / n; the inverse
       // transform conjugates) or the direct DFT kernel of linalg.cpp:37-50
       std::vector<double> tw;

@@ -333,6 +333,98 @@ __device__ __forceinline__ void store_vec(double2* dst, const double2* src, int 
   for (int i = threadIdx.x; i < d; i += ST_T) dst[i] = src[i];
 }
 
+// ---- sweeps with the kinetic half steps between grid steps merged -------------------------------
+// Consecutive split steps meet in two kinetic half steps, K_h K_h = one spectral multiply by
+// exp(-i dt k): a forward sweep then costs two transforms per grid step instead of four, and an
+// adjoint sweep two instead of six, because the forward sweep keeps psi_a(j) = K_h psi_j (the
+// state the potential/nonlinear phase acts on, which the backward stage of the reference
+// recomputes from psi_j, propagation.cpp:146-170) instead of psi_j.  Same map as strang_step /
+// strang_backward_stage applied step by step, up to the rounding of the skipped
+// inverse-then-forward transform pair.
+//
+// psi (in X.A) -> psi_a(0) = K_h psi (in X.S)
+__device__ void merged_begin_forward(const StrangCtx& X, const DevProblem& P) {
+  transform(X, X.A, X.B, -1, nullptr, 1.0);
+  transform(X, X.B, X.S, +1, P.kin_fwd, X.inv_n);
+}
+// psi_a(j) in X.S -> potential + nonlinear phase, then either psi_a(j+1) in X.S (last = false)
+// or the step's end state psi_{j+1} in X.A (last = true).  node_out != null also writes
+// psi_{j+1} there when last = false (node sweeps; uses Q).
+__device__ void merged_forward_step(const StrangCtx& X, const DevProblem& P, double u, double dt, bool last,
+                                    double2* node_out) {
+  const PotStep ps = pot_step(X, P, u);
+  for (int i = threadIdx.x; i < X.d; i += ST_T) {
+    const double2 pa = X.S[i];
+    const double w = potential_at(X, P, i, u, ps) + P.kappa * cabs2(pa);
+    double s, c;
+    sincos(-dt * w, &s, &c);
+    X.S[i] = cmul(cx(c, s), pa);  // psi_b
+  }
+  __syncthreads();
+  transform(X, X.S, X.B, -1, nullptr, 1.0);  // spectrum of psi_b
+  if (last) {
+    transform(X, X.B, X.A, +1, P.kin_fwd, X.inv_n);
+    return;
+  }
+  if (node_out) {
+    for (int i = threadIdx.x; i < X.d; i += ST_T) X.Q[i] = X.B[i];
+    __syncthreads();
+    transform(X, X.Q, X.A, +1, P.kin_fwd, X.inv_n);  // psi_{j+1}
+    for (int i = threadIdx.x; i < X.d; i += ST_T) node_out[i] = X.A[i];
+    __syncthreads();
+  }
+  transform(X, X.B, X.S, +1, P.kin_fwd2, X.inv_n);  // psi_a(j+1) = K_h K_h psi_b
+}
+// chi_len (in X.A) -> chi_b(len-1) = K_h^dag chi_len (in X.A)
+__device__ void merged_begin_adjoint(const StrangCtx& X, const DevProblem& P) {
+  transform(X, X.A, X.B, -1, nullptr, 1.0);
+  transform(X, X.B, X.A, +1, P.kin_adj, X.inv_n);
+}
+// chi_b(j) in X.A, psi_a(j) at pa_g (global) -> chi_b(j-1) in X.A (first = false) or chi_j in X.A
+// (first = true, the sweep's last stage); returns Im sum conj(chi_b) dV psi_b.  node_out != null
+// also writes chi_j there when first = false.
+__device__ double merged_adjoint_step(const StrangCtx& X, const DevProblem& P, double u, double dt, bool naive,
+                                      bool want_grad, const double2* pa_g, bool first, double2* node_out) {
+  const int d = X.d;
+  double g = 0.0;
+  const PotStep pst = pot_step(X, P, u);
+  for (int i = threadIdx.x; i < d; i += ST_T) {
+    const double2 pa = pa_g[i], cb = X.A[i];
+    const double dens = cabs2(pa);
+    const double w = potential_at(X, P, i, u, pst) + P.kappa * dens;
+    double s, c;
+    sincos(-dt * w, &s, &c);
+    const double2 flow = cx(c, s);
+    const double2 pb = cmul(flow, pa);
+    if (want_grad) g += potential_du_at(X, P, i, u, pst) * cconjmul(cb, pb).y;
+    double2 ca;
+    if (naive) {
+      ca = cconjmul(flow, cb);
+    } else {
+      const double kd = dt * P.kappa;
+      const double2 p = cmul(flow, cx(1.0, -kd * dens));
+      const double2 q = cmul(cx(0.0, -kd), cmul(flow, cmul(pa, pa)));
+      ca = cadd(cconjmul(p, cb), cmul(q, cconj(cb)));
+    }
+    X.B[i] = ca;
+  }
+  __syncthreads();
+  transform(X, X.B, X.S, -1, nullptr, 1.0);  // spectrum of chi_a
+  if (first) {
+    transform(X, X.S, X.A, +1, P.kin_adj, X.inv_n);
+  } else {
+    if (node_out) {
+      for (int i = threadIdx.x; i < d; i += ST_T) X.Q[i] = X.S[i];
+      __syncthreads();
+      transform(X, X.Q, X.A, +1, P.kin_adj, X.inv_n);  // chi_j
+      for (int i = threadIdx.x; i < d; i += ST_T) node_out[i] = X.A[i];
+      __syncthreads();
+    }
+    transform(X, X.S, X.A, +1, P.kin_adj2, X.inv_n);  // chi_b(j-1) = K_h^dag K_h^dag chi_a
+  }
+  return want_grad ? block_sum(X, g) : 0.0;
+}
+
 __global__ void __launch_bounds__(ST_T, 1) strang_task_kernel(DevProblem P, DevRun R, TaskArgs A, int ignore_done) {
   const int n = blockIdx.x, b = blockIdx.y;
   if (ignore_done ? R.status[b] : (R.done[b] | R.status[b])) return;
@@ -362,6 +454,15 @@ __global__ void __launch_bounds__(ST_T, 1) strang_task_kernel(DevProblem P, DevR
   const size_t tix = ((size_t)b * P.L + n) * d;
 
   auto forward = [&](bool rec, double* pen) {  // state in X.A
+    if (P.merge_kinetic) {  // trajectory = psi_a(j), j = 0..len-1
+      merged_begin_forward(X, P);
+      for (int j = 0; j < len; ++j) {
+        if (rec) store_vec(traj + (size_t)j * d, X.S, d);
+        merged_forward_step(X, P, u[j], dt, j == len - 1, nullptr);
+        if (pen) *pen += (P.alpha[node0 + j] * scale) * (u[j] * u[j]);
+      }
+      return;
+    }
     if (rec) store_vec(traj, X.A, d);
     for (int j = 0; j < len; ++j) {
       strang_forward(X, P, u[j], dt);
@@ -371,6 +472,17 @@ __global__ void __launch_bounds__(ST_T, 1) strang_task_kernel(DevProblem P, DevR
   };
   // adjoint from the seed in X.A along the stored trajectory; act(j, uold, g)
   auto adjoint = [&](bool grad, auto&& act) {
+    if (P.merge_kinetic) {
+      __syncthreads();
+      merged_begin_adjoint(X, P);
+      for (int j = len - 1; j >= 0; --j) {
+        const double uold = u[j];
+        const double im = merged_adjoint_step(X, P, uold, dt, naive, grad, traj + (size_t)j * d, j == 0, nullptr);
+        const double g = -(P.alpha[node0 + j] * scale) * dt * uold + dt * (w * im);
+        act(j, uold, g);
+      }
+      return;
+    }
     for (int j = len - 1; j >= 0; --j) {
       const double uold = u[j];
       __syncthreads();
@@ -447,7 +559,7 @@ __global__ void __launch_bounds__(ST_T, 1) strang_task_kernel(DevProblem P, DevR
 // node_sweeps (ism.cpp:35-84; strang: forward trajectory kept for the nonlinear adjoint) and
 // the exact payoff (which = 1).  One CTA per problem; the trajectory uses the problem's task
 // workspace (L * traj_len >= K + 1 states).
-__global__ void __launch_bounds__(ST_T) strang_horizon_kernel(DevProblem P, DevRun R, int which, int k) {
+__global__ void __launch_bounds__(ST_T, 1) strang_horizon_kernel(DevProblem P, DevRun R, int which, int k) {
   if (R.kdev) k = *R.kdev;
   const int b = blockIdx.x;
   if (R.done[b] || R.status[b]) return;
@@ -464,7 +576,21 @@ __global__ void __launch_bounds__(ST_T) strang_horizon_kernel(DevProblem P, DevR
     store_vec(traj, X.A, d);
   }
   int nxt = 1;
-  for (int j = 0; j < P.K; ++j) {
+  if (P.merge_kinetic) {
+    merged_begin_forward(X, P);
+    for (int j = 0; j < P.K; ++j) {
+      if (which == 0) store_vec(traj + (size_t)j * d, X.S, d);  // psi_a(j)
+      const bool last = j == P.K - 1;
+      const bool at_node = which == 0 && nxt <= P.L && P.node[nxt] == j + 1;
+      merged_forward_step(X, P, u[j], dt, last,
+                          (at_node && !last) ? R.psi_nodes + nb + (size_t)nxt * d : nullptr);
+      if (at_node) {
+        if (last) store_vec(R.psi_nodes + nb + (size_t)nxt * d, X.A, d);
+        ++nxt;
+      }
+    }
+  }
+  for (int j = 0; j < (P.merge_kinetic ? 0 : P.K); ++j) {
     strang_forward(X, P, u[j], dt);
     if (which == 0) {
       store_vec(traj + (size_t)(j + 1) * d, X.A, d);
@@ -489,6 +615,21 @@ __global__ void __launch_bounds__(ST_T) strang_horizon_kernel(DevProblem P, DevR
   load_vec(X.A, P.targ + (size_t)b * d, d);
   store_vec(R.chi_nodes + nb + (size_t)P.L * d, X.A, d);
   int prev = P.L - 1;
+  if (P.merge_kinetic) {
+    __syncthreads();
+    merged_begin_adjoint(X, P);
+    for (int j = P.K - 1; j >= 0; --j) {
+      const bool first = j == 0;
+      const bool at_node = prev >= 0 && P.node[prev] == j;
+      merged_adjoint_step(X, P, u[j], dt, P.naive != 0, false, traj + (size_t)j * d, first,
+                          (at_node && !first) ? R.chi_nodes + nb + (size_t)prev * d : nullptr);
+      if (at_node) {
+        if (first) store_vec(R.chi_nodes + nb + (size_t)prev * d, X.A, d);
+        --prev;
+      }
+    }
+    return;
+  }
   for (int j = P.K - 1; j >= 0; --j) {
     __syncthreads();
     for (int i = t; i < d; i += ST_T) X.Q[i] = traj[(size_t)j * d + i];
