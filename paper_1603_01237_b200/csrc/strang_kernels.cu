@@ -32,6 +32,7 @@ namespace {
 
 constexpr int ST_T = 256;
 constexpr int ST_MAXD = 2048;
+constexpr int ST_STAGE_MAXD = 1024;  // kinetic phase tables staged in shared memory up to this size
 
 struct StrangCtx {
   int d, log2d;
@@ -43,6 +44,9 @@ struct StrangCtx {
   double* red;           // smem [ST_T / 32]
   double2* kx;           // smem [d] (cos k x_i, sin k x_i) of the lattice potential
   double* pf;            // smem [2][QOC_MAX_POT_TERMS]: f_m(u), f_m'(u) of the basis potential (per step)
+  // kinetic phases staged in shared memory (they multiply the first stage's loads of half the
+  // transforms): half step forward / adjoint and the merged full steps
+  const double2 *kf, *ka, *kf2, *ka2;
 };
 
 // V(x_i, u) and dV/du for grid point i.  The cos^2 lattice uses cos/sin(k(x_i - u)) by angle
@@ -88,9 +92,82 @@ __device__ __forceinline__ double basis_sum(const StrangCtx& X, const DevProblem
 
 // dst = DFT_sign(pre . src) unnormalised (sign -1 forward, +1 inverse); pre may be null.
 // src and dst are distinct shared-memory vectors.  Ends with a __syncthreads.
+// Power-of-two sizes known at compile time: the same radix-4 Stockham stages with every stride,
+// twiddle shift and trip count folded to constants and the stage loop unrolled.
+template <int LOG2D, int SIGN>
+__device__ void transform_pow2(const StrangCtx& X, const double2* src, double2* dst, const double2* pre, double scale) {
+  constexpr int d = 1 << LOG2D, NS4 = LOG2D / 2, NST = NS4 + (LOG2D & 1);
+  const int t = threadIdx.x;
+  double2* in = const_cast<double2*>(src);
+  double2* out = dst;
+#pragma unroll
+  for (int s = 0; s < NST; ++s) {
+    const int lNs = 2 * s, Ns = 1 << lNs;
+    const bool r4 = s < NS4;
+    const int lR = r4 ? 2 : 1, R = 1 << lR;
+    const int nb = d >> lR;
+    const int tws = LOG2D - lNs - lR;
+    for (int j = t; j < nb; j += ST_T) {
+      const int jm = j & (Ns - 1);
+      double2 v[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        if (r < R) {
+          double2 x = in[j + r * nb];
+          if (s == 0) {
+            if (pre) x = cmul(x, pre[j + r * nb]);
+            if (scale != 1.0) x = cscale(x, scale);
+          }
+          if (r > 0 && s > 0) {  // twiddle exp(SIGN 2 pi i jm r / (Ns R)); jm = 0 gives 1
+            const int k = (jm * r) << tws;
+            double2 w = X.tw[k & (d / 2 - 1)];
+            if (k >= d / 2) w = cx(-w.x, -w.y);
+            if (SIGN > 0) w.y = -w.y;
+            x = cmul(x, w);
+          }
+          v[r] = x;
+        }
+      }
+      const int idxD = ((j >> lNs) << (lNs + lR)) + jm;
+      if (r4) {
+        const double2 a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]), a2 = cadd(v[1], v[3]);
+        const double2 dd = csub(v[1], v[3]);
+        const double2 a3 = SIGN < 0 ? cx(dd.y, -dd.x) : cx(-dd.y, dd.x);
+        out[idxD] = cadd(a0, a2);
+        out[idxD + Ns] = cadd(a1, a3);
+        out[idxD + 2 * Ns] = csub(a0, a2);
+        out[idxD + 3 * Ns] = csub(a1, a3);
+      } else {
+        out[idxD] = cadd(v[0], v[1]);
+        out[idxD + Ns] = csub(v[0], v[1]);
+      }
+    }
+    __syncthreads();
+    double2* tmp = in;
+    in = out;
+    out = tmp;
+  }
+  if (NST % 2 == 0) {  // even number of stages: the result sits in src
+    for (int i = t; i < d; i += ST_T) dst[i] = in[i];
+    __syncthreads();
+  }
+}
+
 __device__ void transform(const StrangCtx& X, const double2* src, double2* dst, int sign, const double2* pre,
                           double scale) {
   const int d = X.d, t = threadIdx.x;
+  if (X.pow2 && X.log2d >= 8 && X.log2d <= 11) {
+    switch (X.log2d * 2 + (sign > 0)) {
+      case 16: return transform_pow2<8, -1>(X, src, dst, pre, scale);
+      case 17: return transform_pow2<8, +1>(X, src, dst, pre, scale);
+      case 18: return transform_pow2<9, -1>(X, src, dst, pre, scale);
+      case 19: return transform_pow2<9, +1>(X, src, dst, pre, scale);
+      case 20: return transform_pow2<10, -1>(X, src, dst, pre, scale);
+      case 21: return transform_pow2<10, +1>(X, src, dst, pre, scale);
+      case 22: return transform_pow2<11, -1>(X, src, dst, pre, scale);
+      default: return transform_pow2<11, +1>(X, src, dst, pre, scale);
+    }
+  }
   if (X.pow2) {
     // Stockham autosort, radix 4 (plus one radix-2 stage when log2 d is odd): no bit-reversal
     // pass and half the barriers of radix 2.  Ping-pongs between dst and src (src is scratch
@@ -236,7 +313,7 @@ __device__ __forceinline__ double potential_du_at(const StrangCtx& X, const DevP
 // psi (in X.A) -> strang_step(psi); uses B, S.
 __device__ void strang_forward(const StrangCtx& X, const DevProblem& P, double u, double dt) {
   transform(X, X.A, X.B, -1, nullptr, 1.0);
-  transform(X, X.B, X.S, +1, P.kin_fwd, X.inv_n);  // psi_a
+  transform(X, X.B, X.S, +1, X.kf, X.inv_n);  // psi_a
   const PotStep ps = pot_step(X, P, u);
   for (int i = threadIdx.x; i < X.d; i += ST_T) {
     const double2 pa = X.S[i];
@@ -247,7 +324,7 @@ __device__ void strang_forward(const StrangCtx& X, const DevProblem& P, double u
   }
   __syncthreads();
   transform(X, X.S, X.B, -1, nullptr, 1.0);
-  transform(X, X.B, X.A, +1, P.kin_fwd, X.inv_n);
+  transform(X, X.B, X.A, +1, X.kf, X.inv_n);
 }
 
 // chi_{j+1} (in X.A), psi_j (in X.Q) -> chi_j (in X.A); returns Im sum conj(chi_b) dV psi_b.
@@ -255,9 +332,9 @@ __device__ double strang_backward(const StrangCtx& X, const DevProblem& P, doubl
                                   bool want_grad) {
   const int d = X.d;
   transform(X, X.Q, X.B, -1, nullptr, 1.0);
-  transform(X, X.B, X.S, +1, P.kin_fwd, X.inv_n);  // psi_a in S
+  transform(X, X.B, X.S, +1, X.kf, X.inv_n);  // psi_a in S
   transform(X, X.A, X.B, -1, nullptr, 1.0);
-  transform(X, X.B, X.A, +1, P.kin_adj, X.inv_n);  // chi_b in A
+  transform(X, X.B, X.A, +1, X.ka, X.inv_n);  // chi_b in A
   double g = 0.0;
   const PotStep pst = pot_step(X, P, u);
   for (int i = threadIdx.x; i < d; i += ST_T) {
@@ -282,7 +359,7 @@ __device__ double strang_backward(const StrangCtx& X, const DevProblem& P, doubl
   }
   __syncthreads();
   transform(X, X.B, X.S, -1, nullptr, 1.0);
-  transform(X, X.S, X.A, +1, P.kin_adj, X.inv_n);
+  transform(X, X.S, X.A, +1, X.ka, X.inv_n);
   return want_grad ? block_sum(X, g) : 0.0;
 }
 
@@ -310,6 +387,24 @@ __device__ __forceinline__ StrangCtx make_ctx(const DevProblem& P, unsigned char
   }
   X.kx = reinterpret_cast<double2*>(X.red + ST_T / 32);
   X.pf = reinterpret_cast<double*>(X.kx + d);
+  if (d > ST_STAGE_MAXD) {  // 2048 points: the tables stay in global memory (L2)
+    X.kf = P.kin_fwd;
+    X.ka = P.kin_adj;
+    X.kf2 = P.kin_fwd2;
+    X.ka2 = P.kin_adj2;
+  } else {
+    double2* ph = reinterpret_cast<double2*>(X.pf + 2 * QOC_MAX_POT_TERMS);
+    for (int i = threadIdx.x; i < d; i += ST_T) {
+      ph[i] = P.kin_fwd[i];
+      ph[d + i] = P.kin_adj[i];
+      ph[2 * d + i] = P.kin_fwd2[i];
+      ph[3 * d + i] = P.kin_adj2[i];
+    }
+    X.kf = ph;
+    X.ka = ph + d;
+    X.kf2 = ph + 2 * d;
+    X.ka2 = ph + 3 * d;
+  }
   for (int i = threadIdx.x; i < d; i += ST_T) {
     double sn, cn;
     sincos(P.pp[2] * P.grid_x[i], &sn, &cn);
@@ -322,7 +417,7 @@ __device__ __forceinline__ StrangCtx make_ctx(const DevProblem& P, unsigned char
 size_t strang_smem(int d) {
   const bool pow2 = (d & (d - 1)) == 0;
   return sizeof(double2) * (4 * (size_t)d + (pow2 ? (d / 2 > 0 ? d / 2 : 1) : 0)) + sizeof(double) * (ST_T / 32) +
-         sizeof(double2) * (size_t)d + sizeof(double) * 2 * QOC_MAX_POT_TERMS;
+         sizeof(double2) * (size_t)d + sizeof(double) * 2 * QOC_MAX_POT_TERMS + (d > ST_STAGE_MAXD ? 0 : sizeof(double2) * 4 * (size_t)d);
 }
 
 __device__ __forceinline__ void load_vec(double2* dst, const double2* src, int d) {
@@ -345,7 +440,7 @@ __device__ __forceinline__ void store_vec(double2* dst, const double2* src, int 
 // psi (in X.A) -> psi_a(0) = K_h psi (in X.S)
 __device__ void merged_begin_forward(const StrangCtx& X, const DevProblem& P) {
   transform(X, X.A, X.B, -1, nullptr, 1.0);
-  transform(X, X.B, X.S, +1, P.kin_fwd, X.inv_n);
+  transform(X, X.B, X.S, +1, X.kf, X.inv_n);
 }
 // psi_a(j) in X.S -> potential + nonlinear phase, then either psi_a(j+1) in X.S (last = false)
 // or the step's end state psi_{j+1} in X.A (last = true).  node_out != null also writes
@@ -363,22 +458,22 @@ __device__ void merged_forward_step(const StrangCtx& X, const DevProblem& P, dou
   __syncthreads();
   transform(X, X.S, X.B, -1, nullptr, 1.0);  // spectrum of psi_b
   if (last) {
-    transform(X, X.B, X.A, +1, P.kin_fwd, X.inv_n);
+    transform(X, X.B, X.A, +1, X.kf, X.inv_n);
     return;
   }
   if (node_out) {
     for (int i = threadIdx.x; i < X.d; i += ST_T) X.Q[i] = X.B[i];
     __syncthreads();
-    transform(X, X.Q, X.A, +1, P.kin_fwd, X.inv_n);  // psi_{j+1}
+    transform(X, X.Q, X.A, +1, X.kf, X.inv_n);  // psi_{j+1}
     for (int i = threadIdx.x; i < X.d; i += ST_T) node_out[i] = X.A[i];
     __syncthreads();
   }
-  transform(X, X.B, X.S, +1, P.kin_fwd2, X.inv_n);  // psi_a(j+1) = K_h K_h psi_b
+  transform(X, X.B, X.S, +1, X.kf2, X.inv_n);  // psi_a(j+1) = K_h K_h psi_b
 }
 // chi_len (in X.A) -> chi_b(len-1) = K_h^dag chi_len (in X.A)
 __device__ void merged_begin_adjoint(const StrangCtx& X, const DevProblem& P) {
   transform(X, X.A, X.B, -1, nullptr, 1.0);
-  transform(X, X.B, X.A, +1, P.kin_adj, X.inv_n);
+  transform(X, X.B, X.A, +1, X.ka, X.inv_n);
 }
 // chi_b(j) in X.A, psi_a(j) at pa_g (global) -> chi_b(j-1) in X.A (first = false) or chi_j in X.A
 // (first = true, the sweep's last stage); returns Im sum conj(chi_b) dV psi_b.  node_out != null
@@ -411,16 +506,16 @@ __device__ double merged_adjoint_step(const StrangCtx& X, const DevProblem& P, d
   __syncthreads();
   transform(X, X.B, X.S, -1, nullptr, 1.0);  // spectrum of chi_a
   if (first) {
-    transform(X, X.S, X.A, +1, P.kin_adj, X.inv_n);
+    transform(X, X.S, X.A, +1, X.ka, X.inv_n);
   } else {
     if (node_out) {
       for (int i = threadIdx.x; i < d; i += ST_T) X.Q[i] = X.S[i];
       __syncthreads();
-      transform(X, X.Q, X.A, +1, P.kin_adj, X.inv_n);  // chi_j
+      transform(X, X.Q, X.A, +1, X.ka, X.inv_n);  // chi_j
       for (int i = threadIdx.x; i < d; i += ST_T) node_out[i] = X.A[i];
       __syncthreads();
     }
-    transform(X, X.S, X.A, +1, P.kin_adj2, X.inv_n);  // chi_b(j-1) = K_h^dag K_h^dag chi_a
+    transform(X, X.S, X.A, +1, X.ka2, X.inv_n);  // chi_b(j-1) = K_h^dag K_h^dag chi_a
   }
   return want_grad ? block_sum(X, g) : 0.0;
 }
