@@ -891,6 +891,17 @@ __device__ void solve_apply(int d, const double2* W, const double2* x, double2* 
   __syncthreads();
 }
 
+// B = I + s i H(v) inverted in place: pivot-free when dt/2 ||H(v)||_1 < 1 (strict column diagonal
+// dominance, where partial pivoting never swaps), else the pivoting path.  One channel.
+__device__ void mono_inverse(const DevProblem& P, int b, double v, double shalf, const BigSmem& S) {
+  build(P, b, &v, shalf, S.W);
+  const double* nb = P.norm1 + (size_t)b * 3;  // ||H0||_1, ||A_0||_1, ||B_0||_1
+  double bound = nb[0] + fabs(v) * nb[1];
+  if (P.has_quad) bound += 0.5 * v * v * nb[2];
+  if (0.5 * P.dt * bound < 1.0) invert_nopivot(P.d, S);
+  else invert(P.d, S);
+}
+
 __global__ void __launch_bounds__(BT) monotonic_kernel(DevProblem P, DevRun R, int weighted, double fp_tol,
                                                         int fp_max_iter, int* stats) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -916,8 +927,7 @@ __global__ void __launch_bounds__(BT) monotonic_kernel(DevProblem P, DevRun R, i
   copy_vec(d, R.task_targ + tix, S.x);
   for (int i = threadIdx.x; i < d; i += BT) chi[(size_t)len * d + i] = S.x[i];
   for (int j = len - 1; j >= 0; --j) {
-    build(P, b, u + j, half, S.W);
-    invert(d, S);
+    mono_inverse(P, b, u[j], half, S);
     cayley(d, S.W, S.x, S.y, true);
     copy_vec(d, S.y, S.x);
     for (int i = threadIdx.x; i < d; i += BT) chi[(size_t)j * d + i] = S.x[i];
@@ -928,8 +938,7 @@ __global__ void __launch_bounds__(BT) monotonic_kernel(DevProblem P, DevRun R, i
   int rejected = 0;
   for (int j = 0; j < len; ++j) {
     const double uj = u[j], aj = P.alpha[node0 + j] * scale;
-    build(P, b, &uj, half, S.W);
-    invert(d, S);
+    mono_inverse(P, b, uj, half, S);
     solve_apply(d, S.W, S.x, S.y);  // psi~
     for (int i = threadIdx.x; i < d; i += BT) {
       double2 a = cx(0.0, 0.0), q = cx(0.0, 0.0);
@@ -944,8 +953,7 @@ __global__ void __launch_bounds__(BT) monotonic_kernel(DevProblem P, DevRun R, i
     __syncthreads();
     double m_mu = 0.0, m_pol = 0.0;
     auto pairings_at = [&](double v) {
-      build(P, b, &v, -half, S.W);  // I - L(v)
-      invert(d, S);
+      mono_inverse(P, b, v, -half, S);  // I - L(v)
       solve_apply(d, S.W, chin, chit);
       double sm = 0.0, sp = 0.0;
       for (int i = threadIdx.x; i < d; i += BT) {
@@ -982,8 +990,7 @@ __global__ void __launch_bounds__(BT) monotonic_kernel(DevProblem P, DevRun R, i
     }
     __syncthreads();
     if (threadIdx.x == 0) u[j] = v;
-    build(P, b, &v, half, S.W);
-    invert(d, S);
+    mono_inverse(P, b, v, half, S);
     cayley(d, S.W, S.x, S.y, false);
     copy_vec(d, S.y, S.x);
   }
