@@ -246,10 +246,9 @@ __global__ void __launch_bounds__(NT) newton_begin_kernel(DevProblem P, DevRun R
   }
   const double* u = R.u + T.off;
   const double* g0 = N.g0 + T.off;
-  double su = 0.0, sg = 0.0;
+  double su = 0.0;
   for (int e = threadIdx.x; e < T.nel; e += NT) {
     su += u[e] * u[e];
-    sg += g0[e] * g0[e];
     N.x[T.off + e] = 0.0;
     N.up[T.off + e] = u[e];  // valid controls for the lockstep gradient launches of idle tasks
     N.um[T.off + e] = u[e];
@@ -261,7 +260,6 @@ __global__ void __launch_bounds__(NT) newton_begin_kernel(DevProblem P, DevRun R
     const double be = T.weight * g0[e];
     sb += be * be;
   }
-  (void)sg;
   const double bnorm = sqrt(block_sum(sb, red));
   if (threadIdx.x == 0) {
     T.sc[C_BNORM] = bnorm;
