@@ -68,7 +68,7 @@ def test_batch_members_stop_independently(ctx):
         assert np.max(np.abs(g.record.objectives() - r.record.objectives())) < 1e-11
 
 
-@pytest.mark.parametrize("kind", ["batch", "rotor", "bitflip", "strang"])
+@pytest.mark.parametrize("kind", ["batch", "rotor", "bitflip", "strang", "density", "gpe256", "newton", "monotonic"])
 def test_run_to_run_bitwise_determinism(ctx, kind):
     # fixed-order reductions everywhere (no atomics on the data path): two runs of the same
     # problem give bit-identical controls and records (acceptance_main.cpp:143-157 asks the same
@@ -81,6 +81,14 @@ def test_run_to_run_bitwise_determinism(ctx, kind):
         w = problems.rotor21(subintervals=32, iterations=9, rho=100.0)
     elif kind == "bitflip":
         w = problems.ising10(nspins=7, steps=64, T=0.5, iterations=4, subintervals=8, rho=2.0)
+    elif kind == "density":  # assembled plan, tensor-core products, kept inverses
+        w = problems.spins_preset(quick=False, subintervals=8, iterations=4, steps=256)
+    elif kind == "gpe256":  # merged kinetic half steps, compile-time FFT stages
+        w = problems.gpe1024(subintervals=8, iterations=4, rho=5.0, points=256, steps=400, T=0.2)
+    elif kind in ("newton", "monotonic"):
+        p, u = O.dense_fixture(7003, dim=3, steps=24, channels=1, quadratic=True, alpha=1.0)
+        cfg = I.IsmConfig(subintervals=4, max_outer=4, eta=0.0)
+        w = type("W", (), {"problem": p, "u0": u, "config": cfg, "solver": I.SolverSpec(kind=kind, step_size=0.2)})
     else:
         p, u = O.strang_fixture(3300, steps=24)
         cfg = I.IsmConfig(subintervals=4, max_outer=9, eta=0.0, variant="split", log_exact_objective=True)
