@@ -94,11 +94,19 @@ __device__ __forceinline__ double basis_sum(const StrangCtx& X, const DevProblem
 // src and dst are distinct shared-memory vectors.  Ends with a __syncthreads.
 // Power-of-two sizes known at compile time: the same radix-4 Stockham stages with every stride,
 // twiddle shift and trip count folded to constants and the stage loop unrolled.
-template <int LOG2D, int SIGN>
-__device__ void transform_pow2(const StrangCtx& X, const double2* src, double2* dst, const double2* pre, double scale) {
+// The out-of-line wrapper below serves the sizes other than 1024 (every size inlined at ~20 call
+// sites costs minutes of compile time); the work
+// vectors and the twiddle table are passed as offsets into the dynamic shared memory so that the
+// stage loads and stores stay shared-memory instructions across the call.
+template <int LOG2D, int SIGN, bool PRE>
+__device__ __forceinline__ void transform_pow2_core(int src_off, int dst_off, int tw_off, const double2* pre, double scale) {
+  extern __shared__ __align__(16) unsigned char fft_smem[];
   constexpr int d = 1 << LOG2D, NS4 = LOG2D / 2, NST = NS4 + (LOG2D & 1);
   const int t = threadIdx.x;
-  double2* in = const_cast<double2*>(src);
+  double2* const base = reinterpret_cast<double2*>(fft_smem);
+  const double2* const twv = base + tw_off;
+  double2* const dst = base + dst_off;
+  double2* in = base + src_off;
   double2* out = dst;
 #pragma unroll
   for (int s = 0; s < NST; ++s) {
@@ -114,13 +122,13 @@ __device__ void transform_pow2(const StrangCtx& X, const double2* src, double2* 
       for (int r = 0; r < 4; ++r) {
         if (r < R) {
           double2 x = in[j + r * nb];
-          if (s == 0) {
+          if (PRE && s == 0) {  // PRE = false: plain transform (no pre-multiply, scale 1)
             if (pre) x = cmul(x, pre[j + r * nb]);
             if (scale != 1.0) x = cscale(x, scale);
           }
           if (r > 0 && s > 0) {  // twiddle exp(SIGN 2 pi i jm r / (Ns R)); jm = 0 gives 1
             const int k = (jm * r) << tws;
-            double2 w = X.tw[k & (d / 2 - 1)];
+            double2 w = twv[k & (d / 2 - 1)];
             if (k >= d / 2) w = cx(-w.x, -w.y);
             if (SIGN > 0) w.y = -w.y;
             x = cmul(x, w);
@@ -153,20 +161,34 @@ __device__ void transform_pow2(const StrangCtx& X, const double2* src, double2* 
   }
 }
 
-__device__ void transform(const StrangCtx& X, const double2* src, double2* dst, int sign, const double2* pre,
-                          double scale) {
+template <int LOG2D, int SIGN, bool PRE>
+__device__ __noinline__ void transform_pow2(int src_off, int dst_off, int tw_off, const double2* pre, double scale) {
+  transform_pow2_core<LOG2D, SIGN, PRE>(src_off, dst_off, tw_off, pre, scale);
+}
+
+__device__ __noinline__ void transform_other(const StrangCtx& X, const double2* src, double2* dst, int sign,
+                                             const double2* pre, double scale) {
   const int d = X.d, t = threadIdx.x;
   if (X.pow2 && X.log2d >= 8 && X.log2d <= 11) {
+    // every work vector and the twiddle table are carved from the dynamic shared memory whose
+    // first vector is X.A (make_ctx)
+    const int so = (int)(src - X.A), dof = (int)(dst - X.A), to = (int)(X.tw - X.A);
+    const bool plain = pre == nullptr && scale == 1.0;
+#define QOC_FFT_CASE(LG, SG)                                                   \
+  if (plain) transform_pow2<LG, SG, false>(so, dof, to, pre, scale);           \
+  else transform_pow2<LG, SG, true>(so, dof, to, pre, scale);                  \
+  return;
     switch (X.log2d * 2 + (sign > 0)) {
-      case 16: return transform_pow2<8, -1>(X, src, dst, pre, scale);
-      case 17: return transform_pow2<8, +1>(X, src, dst, pre, scale);
-      case 18: return transform_pow2<9, -1>(X, src, dst, pre, scale);
-      case 19: return transform_pow2<9, +1>(X, src, dst, pre, scale);
-      case 20: return transform_pow2<10, -1>(X, src, dst, pre, scale);
-      case 21: return transform_pow2<10, +1>(X, src, dst, pre, scale);
-      case 22: return transform_pow2<11, -1>(X, src, dst, pre, scale);
-      default: return transform_pow2<11, +1>(X, src, dst, pre, scale);
+      case 16: QOC_FFT_CASE(8, -1)
+      case 17: QOC_FFT_CASE(8, +1)
+      case 18: QOC_FFT_CASE(9, -1)
+      case 19: QOC_FFT_CASE(9, +1)
+      case 20: QOC_FFT_CASE(10, -1)
+      case 21: QOC_FFT_CASE(10, +1)
+      case 22: QOC_FFT_CASE(11, -1)
+      default: QOC_FFT_CASE(11, +1)
     }
+#undef QOC_FFT_CASE
   }
   if (X.pow2) {
     // Stockham autosort, radix 4 (plus one radix-2 stage when log2 d is odd): no bit-reversal
@@ -254,6 +276,25 @@ __device__ void transform(const StrangCtx& X, const double2* src, double2* dst, 
     }
     __syncthreads();
   }
+}
+
+// dst = DFT_sign(pre . src) unnormalised; 1024 points (BASELINE config 4) run the compile-time
+// stages inlined at the call site, every other size goes through one out-of-line function.
+__device__ __forceinline__ void transform(const StrangCtx& X, const double2* src, double2* dst, int sign,
+                                          const double2* pre, double scale) {
+  if (X.log2d == 10 && X.pow2) {
+    const int so = (int)(src - X.A), dof = (int)(dst - X.A), to = (int)(X.tw - X.A);
+    const bool plain = pre == nullptr && scale == 1.0;
+    if (sign < 0) {
+      if (plain) transform_pow2_core<10, -1, false>(so, dof, to, pre, scale);
+      else transform_pow2_core<10, -1, true>(so, dof, to, pre, scale);
+    } else {
+      if (plain) transform_pow2_core<10, +1, false>(so, dof, to, pre, scale);
+      else transform_pow2_core<10, +1, true>(so, dof, to, pre, scale);
+    }
+    return;
+  }
+  transform_other(X, src, dst, sign, pre, scale);
 }
 
 __device__ __forceinline__ double block_sum(const StrangCtx& X, double v) {
